@@ -1,0 +1,122 @@
+/* slimpipe.h — the C-ABI of libslimpipe.so, the B200 SlimPipe step.
+ *
+ * Two halves:
+ *   1. Planning (host C++, behind the pipelab headers in include/pipelab/):
+ *      exposed here as JSON-text entry points for the Python host mirror and
+ *      the parity tests.  The C++ API itself (gen_slimpipe, validate_schedule,
+ *      balance_tick, apply_exchange, simulate, ...) is the drop-in for
+ *      reference proj/include/pipelab/{schedule,exchange,simulator,workload}.hpp.
+ *   2. Device (sm_100a CUDA + NCCL): the replacements for what the reference
+ *      only models —
+ *        reference proj/src/attention.cpp:21-111  (chunked online-softmax
+ *            attention, fp64, forward only)      -> sp_attn_fwd / sp_attn_bwd /
+ *                                                   sp_attn_merge
+ *        reference proj/src/simulator.cpp:311-346 (slice memory ledger)
+ *                                                -> the runtime's HBM slot arena
+ *        reference proj/src/simulator.cpp:156-207, 275-309 (exchange transfers,
+ *            CommModel simulator.hpp:23-34)      -> sp_exchange_* + NCCL P2P
+ *        reference proj/src/schedule.cpp:102-130 cross-device edges
+ *                                                -> stage P2P in sp_runtime_step
+ *
+ * Conventions: status codes (SP_OK == 0), never exceptions; device pointers
+ * are plain addresses of caller-owned buffers; `stream` is a cudaStream_t
+ * (0 = legacy default stream); bf16 buffers are passed as void*.
+ * One host thread per GPU; handles are not thread-safe.
+ */
+#ifndef SLIMPIPE_H
+#define SLIMPIPE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void* sp_stream_t; /* cudaStream_t */
+
+enum {
+  SP_OK = 0,
+  SP_ERR_INVALID = 1,     /* reference: std::invalid_argument */
+  SP_ERR_RUNTIME = 2,     /* reference: std::runtime_error    */
+  SP_ERR_CUDA = 3,
+  SP_ERR_NCCL = 4,
+  SP_ERR_UNSUPPORTED = 5, /* shape outside what the kernels implement */
+  SP_ERR_NO_DEVICE = 6
+};
+
+const char* sp_status_string(int code);
+const char* sp_last_error(void); /* message of the last failing call on this thread */
+void sp_free(char* p);
+int sp_version(void);
+
+/* ---------------------------------------------------------------- planning
+ * scheme: 0 gpipe 1 terapipe 2 1f1b 3 interleaved_1f1b 4 zbv 5 vhalf 6 slimpipe
+ * mode:   0 off 1 on 2 early.  *out receives a malloc'd JSON string (free with
+ * sp_free) — on error a {"error": kind, "what": message} object. */
+int sp_plan_schedule_json(int scheme, int p, int v, int m, int n, char** out);
+/* reference schedule.cpp:413-579; mutation 0 none, 1 swap BW(1,2)/BW(1,1) on
+ * device 1, 2 drop the last pass of device 2, 3 add a cycle-closing edge */
+int sp_plan_validate_json(int p, int v, int m, int n, int mutation, char** out);
+/* reference exchange.cpp:10-96 */
+int sp_plan_balance_json(const int64_t* loads, const int32_t* devices, int count, int early, char** out);
+/* reference simulator.cpp:56-108 */
+int sp_plan_exchange_json(int p, int v, int m, int n, int mode, double beta_attn, char** out);
+/* reference workload.cpp:87-141; model={L,h,H,a,g,V,bytes,loss_bytes},
+ * par={t,c,p,v}, run={S,m,n,ckpt(0 none,1 selective,2 full)} */
+int sp_plan_activation_json(const int64_t* model, const int64_t* par, const int64_t* run, double offload,
+                            char** out);
+/* reference exchange.cpp:98-111 */
+int sp_plan_exchange_volume(int64_t p, int64_t n, int64_t layers, int64_t mh_num, int64_t mh_den, char** out);
+/* reference simulator.cpp:110-412; cost={alpha,beta,bwd_in,bwd_w},
+ * comm={bandwidth,latency}; mem_rats = 6 (num,den) pairs or NULL (unit model) */
+int sp_plan_simulate_json(int p, int v, int m, int n, int mode, const double* cost, const double* comm,
+                          int64_t seq_len, const int64_t* mem_rats, char** out);
+
+/* ------------------------------------------------- sliced causal attention
+ * Replaces reference attention.cpp:94-111 (chunk_attention) for the
+ * multi-head bf16 slice layout of the step:
+ *   q      bf16 [q_rows][q_stride]   head h occupies columns [h*d, (h+1)*d)
+ *   k_pool bf16 [pool_rows][kv_stride], v_pool likewise; kv head g at [g*d,...)
+ *   chunk_row[c] (host array, n_chunks <= SP_MAX_CHUNKS): first pool row of the
+ *          c-th KV chunk, in attention order; every chunk has chunk_len rows
+ *   causal: query row r attends global key positions
+ *          <= n_chunks*chunk_len - q_rows + r (reference attention.cpp:34-35,
+ *          bottom-right aligned) — only the last chunk is ever masked
+ *   o      bf16 [q_rows][o_stride] normalised output (finalize, :84-92)
+ *   lse    fp32 [heads][q_rows]  natural-log row log-sum-exp of the scaled
+ *          scores (row_max + log(row_sumexp)); -inf for fully masked rows
+ * Query head h reads kv head h / (heads / kv_heads).
+ * Requirements: head_dim in {64, 128}; q_rows, chunk_len multiples of 128;
+ * strides multiples of 8 elements. */
+#define SP_MAX_CHUNKS 64
+int sp_attn_fwd(const void* q, int64_t q_rows, int64_t q_stride, const void* k_pool, const void* v_pool,
+                int64_t pool_rows, int64_t kv_stride, const int32_t* chunk_row, int n_chunks, int chunk_len,
+                int heads, int kv_heads, int head_dim, int causal, void* o, int64_t o_stride, float* lse,
+                sp_stream_t stream);
+
+/* Backward of sp_attn_fwd.  Accumulates (+=) into fp32 buffers:
+ *   dq_acc  fp32 [q_rows][heads*head_dim]
+ *   dk_acc, dv_acc fp32 pools [acc_rows][kv_heads*head_dim]; chunk c's rows
+ *           start at acc_row[c] (host array)
+ * delta_ws: fp32 [heads][q_rows] scratch (receives rowsum(dO*O)).
+ * Runs slices n..1 in the step so a chunk's dK/dV is complete when its own
+ * slice's backward runs (reference schedule.cpp:125-126 edge order). */
+int sp_attn_bwd(const void* q, int64_t q_rows, int64_t q_stride, const void* k_pool, const void* v_pool,
+                int64_t pool_rows, int64_t kv_stride, const int32_t* chunk_row, int n_chunks, int chunk_len,
+                int heads, int kv_heads, int head_dim, int causal, const void* o, int64_t o_stride,
+                const void* dout, int64_t do_stride, const float* lse, float* delta_ws, float* dq_acc,
+                float* dk_acc, float* dv_acc, int64_t acc_rows, const int32_t* acc_row, sp_stream_t stream);
+
+/* Online-softmax merge of two normalised partials over disjoint key sets
+ * (reference merge_partials attention.cpp:63-82 followed by finalize :84-92):
+ *   w_x = exp(lse_x - max), o = (w_a o_a + w_b o_b) / (w_a + w_b),
+ *   lse = max + log(w_a + w_b); rows where both are -inf stay 0 / -inf.
+ * o_out/lse_out may alias o_a/lse_a. */
+int sp_attn_merge(const void* o_a, const float* lse_a, const void* o_b, const float* lse_b, int64_t rows,
+                  int heads, int head_dim, int64_t o_stride, void* o_out, float* lse_out, sp_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SLIMPIPE_H */

@@ -1,0 +1,281 @@
+// extern "C" planning entry points of libslimpipe.so (declared in
+// include/slimpipe.h).  They expose the pipelab planning layer to the Python
+// host mirror and the parity tests as JSON text in the neutral format that
+// oracle/ref_shim.cpp emits for the reference, so plans can be compared
+// byte-for-byte.  Status codes, no exceptions across the ABI.
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <sstream>
+#include <string>
+
+#include "pipelab/exchange.hpp"
+#include "pipelab/schedule.hpp"
+#include "pipelab/simulator.hpp"
+#include "pipelab/workload.hpp"
+#include "slimpipe.h"
+
+using namespace pipelab;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+char* to_c(const std::string& s) {
+  char* p = static_cast<char*>(std::malloc(s.size() + 1));
+  std::memcpy(p, s.c_str(), s.size() + 1);
+  return p;
+}
+
+template <class F>
+int guarded(char** out, F&& body) {
+  try {
+    *out = to_c(body());
+    return SP_OK;
+  } catch (const std::invalid_argument& e) {
+    g_last_error = e.what();
+    *out = to_c(std::string("{\"error\":\"invalid_argument\",\"what\":\"") + e.what() + "\"}");
+    return SP_ERR_INVALID;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    *out = to_c(std::string("{\"error\":\"runtime_error\",\"what\":\"") + e.what() + "\"}");
+    return SP_ERR_RUNTIME;
+  }
+}
+
+GenConfig gen_cfg(int p, int v, int m, int n) {
+  GenConfig c;
+  c.p = p;
+  c.v = v;
+  c.m = m;
+  c.n = n;
+  c.cost.alpha_linear = 1.0;
+  c.cost.beta_attn = 1.0;
+  c.seq_len = n;
+  return c;
+}
+
+std::string q(const Rat& r) { return "\"" + r.str() + "\""; }
+
+std::string g17(double x) {
+  char b[64];
+  std::snprintf(b, sizeof b, "%.17g", x);
+  return b;
+}
+
+template <class C>
+void join(std::ostringstream& os, const C& c) {
+  bool first = true;
+  for (const auto& x : c) {
+    os << (first ? "" : ",") << x;
+    first = false;
+  }
+}
+
+void emit_plan(std::ostringstream& os, const ExchangePlan& p) {
+  os << "{\"transfers\":[";
+  for (std::size_t t = 0; t < p.transfers.size(); ++t) {
+    const Transfer& tr = p.transfers[t];
+    os << (t ? "," : "") << "{\"src\":" << tr.src << ",\"dst\":" << tr.dst << ",\"chunks\":[";
+    join(os, tr.kv_chunk_indices);
+    os << "],\"q\":" << int(tr.carries_query) << ",\"o\":" << int(tr.carries_output) << "}";
+  }
+  os << "],\"loads\":[";
+  join(os, p.resulting_loads);
+  os << "]}";
+}
+
+std::string annotation_json(const ExchangeAnnotation& ann) {
+  std::ostringstream os;
+  os << "{\"mode\":" << int(ann.mode) << ",\"ticks\":[";
+  for (std::size_t t = 0; t < ann.ticks.size(); ++t) {
+    const TickPlan& tp = ann.ticks[t];
+    os << (t ? "," : "") << "{\"tick\":" << tp.tick << ",\"fwd\":" << int(tp.forward)
+       << ",\"junc\":" << int(tp.juncture) << ",\"in\":[";
+    for (std::size_t x = 0; x < tp.loads.size(); ++x)
+      os << (x ? "," : "") << "[" << tp.loads[x].device << "," << tp.loads[x].kv_chunks << "," << tp.passes[x]
+         << "]";
+    os << "],\"plan\":";
+    emit_plan(os, tp.plan);
+    os << "}";
+  }
+  os << "],\"balanced\":[";
+  bool first = true;
+  for (const auto& [pid, c] : ann.balanced_chunks) {
+    os << (first ? "" : ",") << "[" << pid << "," << c << "]";
+    first = false;
+  }
+  os << "]}";
+  return os.str();
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sp_last_error(void) { return g_last_error.c_str(); }
+
+void sp_free(char* p) { std::free(p); }
+
+int sp_plan_schedule_json(int scheme, int p, int v, int m, int n, char** out) {
+  return guarded(out, [&] { return schedule_to_json(generate(Scheme(scheme), gen_cfg(p, v, m, n))); });
+}
+
+int sp_plan_validate_json(int p, int v, int m, int n, int mutation, char** out) {
+  return guarded(out, [&] {
+    Schedule s = gen_slimpipe(gen_cfg(p, v, m, n));
+    if (mutation == 1) {
+      auto& ord = s.device_order[0];
+      int a = -1, b = -1;
+      for (std::size_t x = 0; x < ord.size(); ++x) {
+        const Pass& ps = s.passes[ord[x]];
+        if (ps.kind == PassKind::BackwardFused && ps.microbatch == 1) {
+          if (ps.slice == 2) a = int(x);
+          if (ps.slice == 1) b = int(x);
+        }
+      }
+      if (a >= 0 && b >= 0) std::swap(ord[a], ord[b]);
+    } else if (mutation == 2 && s.device_order.size() > 1) {
+      s.device_order[1].pop_back();
+    } else if (mutation == 3) {
+      s.edges.push_back({s.device_order[0][1], s.device_order[0][0]});
+    }
+    const Diagnostics d = validate_schedule(s);
+    std::ostringstream os;
+    os << "[";
+    for (std::size_t x = 0; x < d.violations.size(); ++x) {
+      const Violation& vi = d.violations[x];
+      os << (x ? "," : "") << "{\"rule\":\"" << vi.rule << "\",\"message\":\"" << vi.message
+         << "\",\"pass\":" << (vi.pass ? *vi.pass : -2) << "}";
+    }
+    os << "]";
+    return os.str();
+  });
+}
+
+int sp_plan_balance_json(const int64_t* loads, const int32_t* devices, int count, int early, char** out) {
+  return guarded(out, [&] {
+    std::vector<TickLoad> tl;
+    for (int x = 0; x < count; ++x) tl.push_back({devices[x], loads[x]});
+    ExchangePlan plan = balance_tick(tl);
+    if (early) plan = to_early_exchange(tl, plan);
+    std::ostringstream os;
+    emit_plan(os, plan);
+    return os.str();
+  });
+}
+
+int sp_plan_exchange_json(int p, int v, int m, int n, int mode, double beta, char** out) {
+  return guarded(out, [&] {
+    GenConfig c = gen_cfg(p, v, m, n);
+    CostModel cm = c.cost;
+    cm.beta_attn = beta;
+    return annotation_json(apply_exchange(gen_slimpipe(c), cm, ExchangeMode(mode)));
+  });
+}
+
+int sp_plan_activation_json(const int64_t* model, const int64_t* par, const int64_t* run, double offload,
+                            char** out) {
+  return guarded(out, [&] {
+    ModelConfig mc;
+    mc.layers = model[0];
+    mc.hidden = model[1];
+    mc.ffn_hidden = model[2];
+    mc.heads = model[3];
+    mc.query_groups = model[4];
+    mc.vocab = model[5];
+    mc.bytes_per_element = model[6];
+    mc.loss_bytes_per_element = model[7];
+    ParallelismConfig pc;
+    pc.tp = par[0];
+    pc.cp = par[1];
+    pc.pp = par[2];
+    pc.stages_per_device = par[3];
+    RunConfig rc;
+    rc.seq_len = run[0];
+    rc.microbatches = run[1];
+    rc.slices = run[2];
+    rc.checkpointing = Checkpointing(run[3]);
+    rc.offload_ratio = offload;
+    const MemoryModel mm = activation_bytes(mc, pc, rc);
+    std::ostringstream os;
+    os << "{\"ptl\":" << q(mm.per_token_layer_bytes) << ",\"mh\":" << q(mm.embedding_bytes)
+       << ",\"ma\":" << q(mm.microbatch_activation_bytes) << ",\"slice_stage\":" << q(mm.slice_stage_bytes)
+       << ",\"logits_slice\":" << q(mm.logits_slice_bytes) << ",\"exchange_slice\":" << q(mm.exchange_slice_bytes)
+       << "}";
+    return os.str();
+  });
+}
+
+int sp_plan_exchange_volume(int64_t p, int64_t n, int64_t L, int64_t mh_num, int64_t mh_den, char** out) {
+  return guarded(out, [&] {
+    return "{\"theta\":" + q(exchange_volume(p, n, L, Rat(mh_num, mh_den))) +
+           ",\"bound\":" + q(exchange_volume_bound(p, n, L, Rat(mh_num, mh_den))) + "}";
+  });
+}
+
+int sp_plan_simulate_json(int p, int v, int m, int n, int mode, const double* cost, const double* comm,
+                          int64_t seq_len, const int64_t* mem_rats, char** out) {
+  return guarded(out, [&] {
+    Schedule s = gen_slimpipe(gen_cfg(p, v, m, n));
+    SimInputs in;
+    in.cost.alpha_linear = cost[0];
+    in.cost.beta_attn = cost[1];
+    in.cost.bwd_input_mult = cost[2];
+    in.cost.bwd_weight_mult = cost[3];
+    in.comm.bandwidth = comm[0];
+    in.comm.latency = comm[1];
+    in.seq_len = seq_len;
+    in.exchange = ExchangeMode(mode);
+    if (mem_rats) {
+      in.memory.per_token_layer_bytes = Rat(mem_rats[0], mem_rats[1]);
+      in.memory.embedding_bytes = Rat(mem_rats[2], mem_rats[3]);
+      in.memory.microbatch_activation_bytes = Rat(mem_rats[4], mem_rats[5]);
+      in.memory.slice_stage_bytes = Rat(mem_rats[6], mem_rats[7]);
+      in.memory.logits_slice_bytes = Rat(mem_rats[8], mem_rats[9]);
+      in.memory.exchange_slice_bytes = Rat(mem_rats[10], mem_rats[11]);
+    } else {
+      in.memory = unit_memory_model(p, v, n);
+    }
+    const SimResult r = simulate(s, in);
+    std::ostringstream os;
+    os << "{\"makespan\":" << g17(r.metrics.makespan) << ",\"bubble\":" << g17(r.metrics.bubble_fraction)
+       << ",\"busy\":[";
+    for (int d = 0; d < p; ++d) os << (d ? "," : "") << g17(r.metrics.device_busy[d]);
+    os << "],\"phases\":[";
+    for (int d = 0; d < p; ++d) {
+      const DevicePhases& ph = r.metrics.phases[d];
+      os << (d ? "," : "") << "[" << g17(ph.warmup_idle) << "," << g17(ph.midstream_idle) << ","
+         << g17(ph.cooldown_idle) << "]";
+    }
+    os << "],\"p2p\":[";
+    for (int d = 0; d < p; ++d) os << (d ? "," : "") << q(r.metrics.p2p_bytes_sent[d]);
+    os << "],\"exchange\":[";
+    for (int d = 0; d < p; ++d) os << (d ? "," : "") << q(r.metrics.exchange_bytes[d]);
+    os << "],\"exchange_per_mb\":" << q(r.metrics.exchange_bytes_per_microbatch_device)
+       << ",\"fticks\":" << r.metrics.forward_ticks << ",\"jticks\":" << r.metrics.juncture_ticks
+       << ",\"memory\":[";
+    for (int d = 0; d < p; ++d) {
+      const DeviceMemory& dm = r.memory.per_device[d];
+      os << (d ? "," : "") << "{\"peak\":" << dm.peak_activation_units << ",\"pool\":" << dm.chunk_pool_size
+         << ",\"final\":" << dm.final_activation_units << ",\"peak_bytes\":" << q(dm.peak_activation_bytes)
+         << ",\"units\":[";
+      for (std::size_t x = 0; x < dm.steps.size(); ++x) os << (x ? "," : "") << dm.steps[x].activation_units;
+      os << "],\"times\":[";
+      for (std::size_t x = 0; x < dm.steps.size(); ++x) os << (x ? "," : "") << g17(dm.steps[x].time);
+      os << "]}";
+    }
+    os << "],\"timeline\":[";
+    for (int d = 0; d < p; ++d) {
+      os << (d ? "," : "") << "[";
+      const auto& tl = r.timeline.per_device[d];
+      for (std::size_t x = 0; x < tl.size(); ++x)
+        os << (x ? "," : "") << "[" << tl[x].pass << "," << g17(tl[x].start) << "," << g17(tl[x].end) << "]";
+      os << "]";
+    }
+    os << "],\"transfers\":" << r.timeline.transfers.size() << "}";
+    return os.str();
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,101 @@
+"""Python mirror of the pipelab planning API (reference
+proj/include/pipelab/{schedule,exchange,simulator,workload}.hpp), backed by the
+C++ implementation in libslimpipe.so.  Names and argument meanings follow the
+reference; errors map std::invalid_argument -> ValueError and
+std::runtime_error -> RuntimeError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+from dataclasses import dataclass
+from fractions import Fraction
+
+from . import native as N
+
+
+def schedule_to_json(p: int, v: int, m: int, n: int, scheme: str = "slimpipe") -> str:
+    """Byte-identical to reference schedule_to_json(generate(scheme, cfg))."""
+    return N._json_call("sp_plan_schedule_json", N.SCHEMES[scheme], p, v, m, n)
+
+
+def gen_slimpipe(p: int, v: int, m: int, n: int) -> dict:
+    """reference schedule.cpp:248-279, returned as the parsed schedule JSON."""
+    return json.loads(schedule_to_json(p, v, m, n, "slimpipe"))
+
+
+def generate(scheme: str, p: int, v: int, m: int, n: int) -> dict:
+    return json.loads(schedule_to_json(p, v, m, n, scheme))
+
+
+def validate_schedule(p: int, v: int, m: int, n: int, mutation: int = 0) -> list[dict]:
+    """Violations of gen_slimpipe(p,v,m,n) (optionally mutated, see slimpipe.h)."""
+    return json.loads(N._json_call("sp_plan_validate_json", p, v, m, n, mutation))
+
+
+def balance_tick(loads: list[int], devices: list[int] | None = None, early: bool = False) -> dict:
+    devices = devices or list(range(1, len(loads) + 1))
+    return json.loads(N._json_call("sp_plan_balance_json", N.arr(C.c_int64, loads), N.arr(C.c_int32, devices),
+                                   len(loads), int(early)))
+
+
+def to_early_exchange(loads: list[int], devices: list[int] | None = None) -> dict:
+    return balance_tick(loads, devices, early=True)
+
+
+def apply_exchange(p: int, v: int, m: int, n: int, mode: str = "on", beta_attn: float = 1.0) -> dict:
+    return json.loads(N._json_call("sp_plan_exchange_json", p, v, m, n, N.MODES[mode], float(beta_attn)))
+
+
+def apply_exchange_text(p: int, v: int, m: int, n: int, mode: str = "on", beta_attn: float = 1.0) -> str:
+    return N._json_call("sp_plan_exchange_json", p, v, m, n, N.MODES[mode], float(beta_attn))
+
+
+@dataclass
+class ModelShape:
+    layers: int
+    hidden: int
+    ffn_hidden: int
+    heads: int
+    query_groups: int
+    vocab: int
+    bytes_per_element: int = 2
+    loss_bytes_per_element: int = 4
+
+    def as_array(self):
+        return [self.layers, self.hidden, self.ffn_hidden, self.heads, self.query_groups, self.vocab,
+                self.bytes_per_element, self.loss_bytes_per_element]
+
+
+CKPT = {"none": 0, "selective": 1, "full": 2}
+
+
+def activation_bytes_text(model: ModelShape, tp: int, cp: int, pp: int, v: int, seq_len: int, m: int, n: int,
+                          ckpt: str = "full", offload: float = 0.0) -> str:
+    return N._json_call("sp_plan_activation_json", N.arr(C.c_int64, model.as_array()),
+                        N.arr(C.c_int64, [tp, cp, pp, v]), N.arr(C.c_int64, [seq_len, m, n, CKPT[ckpt]]),
+                        float(offload))
+
+
+def activation_bytes(*args, **kw) -> dict[str, Fraction]:
+    """reference workload.cpp:87-141; values as exact Fractions."""
+    return {k: Fraction(v) for k, v in json.loads(activation_bytes_text(*args, **kw)).items()}
+
+
+def exchange_volume(p: int, n: int, layers: int, mh: Fraction) -> dict[str, Fraction]:
+    mh = Fraction(mh)
+    d = json.loads(N._json_call("sp_plan_exchange_volume", p, n, layers, mh.numerator, mh.denominator))
+    return {k: Fraction(v) for k, v in d.items()}
+
+
+def simulate_text(p: int, v: int, m: int, n: int, mode: str = "off", cost=(1.0, 0.0, 2.0, 1.0), comm=(0.0, 0.0),
+                  seq_len: int | None = None, mem_rats=None) -> str:
+    seq_len = n if seq_len is None else seq_len
+    mem = N.arr(C.c_int64, mem_rats) if mem_rats is not None else None
+    return N._json_call("sp_plan_simulate_json", p, v, m, n, N.MODES[mode], N.arr(C.c_double, cost),
+                        N.arr(C.c_double, comm), seq_len, mem)
+
+
+def simulate(*args, **kw) -> dict:
+    """reference simulator.cpp:110-412 on gen_slimpipe(p,v,m,n)."""
+    return json.loads(simulate_text(*args, **kw))

@@ -1,0 +1,220 @@
+"""Planning parity (CPU): the product's host C++ (libslimpipe.so) against
+  (a) committed fixtures generated from the compiled reference
+      (tests/golden/make_golden.py), always;
+  (b) the live compiled reference (oracle/_ref/libpipelab_ref.so), when built.
+Bit-exact: schedule JSON bytes, exchange plans, validator diagnostics,
+simulate() doubles (%.17g) and exact-rational byte counts.
+Also re-asserts the reference's own pinned values (tests/test_schedule.cpp,
+tests/test_exchange.cpp, tests/test_simulator.cpp).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import hashlib
+import json
+from fractions import Fraction
+from pathlib import Path
+
+import pytest
+
+import oracle_lib as O
+from paper_2504_14519_b200 import native as N
+from paper_2504_14519_b200 import plan as P
+
+GOLD = Path(__file__).resolve().parent / "golden"
+needs_ref = pytest.mark.skipif(not O.ref_available(), reason="compiled reference not available")
+
+
+def _sha(s: str) -> str:
+    return hashlib.sha256(s.encode()).hexdigest()
+
+
+def _mine_schedule(sch, p, v, m, n):
+    try:
+        return P.schedule_to_json(p, v, m, n, sch)
+    except (ValueError, RuntimeError):
+        return None
+
+
+def test_schedule_bytes_match_golden_grid():
+    gold = json.loads((GOLD / "schedule_sha256.json").read_text())
+    assert len(gold) > 300
+    for key, digest in gold.items():
+        sch, rest = key.split("/")
+        p, v, m, n = (int(x) for x in rest[1:].replace("v", " ").replace("m", " ").replace("n", " ").split())
+        mine = _mine_schedule(sch, p, v, m, n)
+        if digest == "error":
+            assert mine is None, key
+        else:
+            assert mine is not None and _sha(mine) == digest, key
+
+
+def test_schedule_full_text_matches_golden():
+    for key, text in json.loads((GOLD / "schedule_full.json").read_text()).items():
+        p, v, m, n = (int(x) for x in key.split("/")[1][1:].replace("v", " ").replace("m", " ").replace("n", " ").split())
+        assert P.schedule_to_json(p, v, m, n) == text
+
+
+def test_exchange_plans_match_golden():
+    gold = json.loads((GOLD / "exchange_sha256.json").read_text())
+    for key, digest in gold.items():
+        p, v, m, n, mode = (int(x) for x in key[1:].replace("v", " ").replace("m", " ").replace("n", " ")
+                            .replace("ode", " ").split())
+        assert _sha(P.apply_exchange_text(p, v, m, n, ["off", "on", "early"][mode])) == digest, key
+    for key, text in json.loads((GOLD / "exchange_full.json").read_text()).items():
+        p, v, m, n, mode = (int(x) for x in key[1:].replace("v", " ").replace("m", " ").replace("n", " ")
+                            .replace("ode", " ").split())
+        assert P.apply_exchange_text(p, v, m, n, ["off", "on", "early"][mode]) == text
+
+
+def test_simulate_matches_golden():
+    for key, text in json.loads((GOLD / "simulate.json").read_text()).items():
+        p, v, m, n, mode = (int(x) for x in key[1:].replace("v", " ").replace("m", " ").replace("n", " ")
+                            .replace("ode", " ").split())
+        mine = P.simulate_text(p, v, m, n, ["off", "on", "early"][mode], (1.0, 0.3, 2.0, 1.0), (0.5, 0.1), 4 * n)
+        assert mine == text, key
+
+
+@needs_ref
+@pytest.mark.parametrize("scheme", list(N.SCHEMES))
+def test_schedule_bytes_match_live_reference(scheme):
+    code = N.SCHEMES[scheme]
+    for p in (1, 2, 3, 4, 8):
+        for v in (1, 2):
+            for m in (1, 3, 4, 5):
+                for n in ((1, 2, 4, 8, 16) if scheme in ("slimpipe", "terapipe") else (1,)):
+                    ref = O.ref_text("ref_schedule_json", code, p, v, m, n)
+                    mine = _mine_schedule(scheme, p, v, m, n)
+                    if ref.startswith('{"error'):
+                        assert mine is None
+                    else:
+                        assert mine == ref, (scheme, p, v, m, n)
+
+
+@needs_ref
+def test_exchange_validate_simulate_match_live_reference():
+    cost = (1.0, 0.25, 2.0, 0.0)
+    comm = (2.0, 0.05)
+    for p in (1, 2, 3, 4, 8):
+        for v in (1, 2):
+            for m in (1, 2, 4):
+                for n in (p, 2 * p, 4 * p):
+                    for mode in (0, 1, 2):
+                        ref = O.ref_text("ref_exchange_json", p, v, m, n, mode, 0.5)
+                        try:
+                            mine = P.apply_exchange_text(p, v, m, n, ["off", "on", "early"][mode], 0.5)
+                        except ValueError:
+                            mine = None
+                        assert (mine is None) == ref.startswith('{"error'), (p, v, m, n, mode)
+                        if mine is not None:
+                            assert mine == ref
+                        ref_sim = O.ref_text("ref_simulate_json", p, v, m, n, mode, (C.c_double * 4)(*cost),
+                                             (C.c_double * 2)(*comm), 8 * n, None)
+                        if not ref_sim.startswith('{"error'):
+                            assert P.simulate_text(p, v, m, n, ["off", "on", "early"][mode], cost, comm, 8 * n) == ref_sim
+                    for mut in (0, 1, 2, 3):
+                        assert N._json_call("sp_plan_validate_json", p, v, m, n, mut) == \
+                            O.ref_text("ref_validate_json", p, v, m, n, mut)
+
+
+@needs_ref
+def test_balance_random_loads_match_live_reference():
+    import random
+    rnd = random.Random(987654321)
+    for _ in range(3000):
+        p = rnd.randint(1, 12)
+        loads = [rnd.randint(1, 40) for _ in range(p)]
+        devs = sorted(rnd.sample(range(1, 20), p))
+        for early in (0, 1):
+            ref = O.ref_text("ref_balance_json", (C.c_int64 * p)(*loads), (C.c_int32 * p)(*devs), p, early)
+            try:
+                mine = json.dumps(P.balance_tick(loads, devs, bool(early)), separators=(",", ":"))
+            except ValueError:
+                mine = None
+            if ref.startswith('{"error'):
+                assert mine is None
+            else:
+                assert mine == ref, (loads, devs, early)
+
+
+@needs_ref
+def test_activation_and_volume_match_live_reference():
+    presets = [P.ModelShape(40, 5120, 13824, 40, 40, 128000), P.ModelShape(80, 8192, 28672, 64, 8, 128000),
+               P.ModelShape(16, 4096, 11008, 32, 32, 32000), P.ModelShape(4, 256, 1024, 4, 4, 1000)]
+    for mdl in presets:
+        for (t, pp, v, S, n) in [(8, 4, 1, 32768, 8), (1, 8, 1, 262144, 16), (1, 2, 1, 4096, 4), (4, 8, 2, 1 << 20, 32)]:
+            for ck in ("none", "selective", "full"):
+                for off in (0.0, 0.75):
+                    ref = O.ref_text("ref_activation_json", (C.c_int64 * 8)(*mdl.as_array()),
+                                     (C.c_int64 * 4)(t, 1, pp, v), (C.c_int64 * 4)(S, 4, n, P.CKPT[ck]), off)
+                    assert P.activation_bytes_text(mdl, t, 1, pp, v, S, 4, n, ck, off) == ref
+    for p, n in [(1, 4), (2, 4), (4, 8), (8, 16), (8, 32)]:
+        ref = O.ref_text("ref_exchange_volume", p, n, 40, 5368709120, 1)
+        mine = N._json_call("sp_plan_exchange_volume", p, n, 40, 5368709120, 1)
+        assert mine == ref
+
+
+# ---- the reference's own pinned values --------------------------------------
+
+def _trace(sched, d):
+    out = []
+    for pid in sched["device_order"][d - 1]:
+        ps = sched["passes"][pid]
+        out.append(f"{ps['kind']}{ps['microbatch']}.{ps['slice']}s{ps['stage']}")
+    return out
+
+
+def test_fig4_trace_and_warmup_depths():  # reference tests/test_schedule.cpp:113-140
+    s = P.gen_slimpipe(4, 1, 4, 8)
+    assert P.validate_schedule(4, 1, 4, 8) == []
+    d1 = _trace(s, 1)
+    assert d1[:8] == [f"F1.{i}s1" for i in range(1, 9)]
+    assert d1[8:14] == [f"F2.{i}s1" for i in range(1, 7)]
+    assert d1[14:20] == ["BW1.8s1", "F2.7s1", "BW1.7s1", "F2.8s1", "BW1.6s1", "F3.1s1"]
+    for d, w in zip((1, 2, 3, 4), (14, 12, 10, 8)):
+        tr = _trace(s, d)
+        assert next(i for i, x in enumerate(tr) if x.startswith("BW")) == w
+    assert _trace(s, 4)[8:10] == ["BW1.8s4", "F2.1s4"]
+
+
+def test_slimpipe_requires_n_multiple_of_p():  # tests/test_schedule.cpp:142-144
+    with pytest.raises(ValueError):
+        P.gen_slimpipe(4, 1, 2, 6)
+
+
+def test_validator_negative_fixtures():  # tests/test_schedule.cpp:220-265
+    rules = lambda mut: {v["rule"] for v in P.validate_schedule(4, 1, 2, 8, mut)}
+    assert "reverse-order" in rules(1)
+    assert rules(2) & {"order", "coverage"}
+    assert "acyclicity" in rules(3)
+
+
+def test_fig7_plan_and_early_rewrite():  # tests/test_exchange.cpp:43-55, :147-160
+    plan = P.balance_tick([7, 6, 5, 4, 3, 2])
+    assert plan["loads"] == [5, 5, 5, 4, 4, 4]
+    assert [(t["src"], t["dst"], t["chunks"]) for t in plan["transfers"]] == [(1, 6, [6, 7]), (2, 5, [6])]
+    early = P.to_early_exchange([7, 6, 5, 4, 3, 2])
+    assert [t["chunks"] for t in early["transfers"]] == [[1, 2], [1]]
+    assert P.balance_tick([3, 3, 3, 3])["transfers"] == []
+    with pytest.raises(ValueError):
+        P.balance_tick([0, 2])
+
+
+def test_eq2_volume():  # tests/test_exchange.cpp:162-179: p4 n8 -> 1.375 L M_h
+    v = P.exchange_volume(4, 8, 1, Fraction(1))
+    assert v["theta"] == Fraction(11, 8)
+    assert P.exchange_volume(1, 4, 1, Fraction(1))["theta"] == 0
+
+
+def test_ledger_peaks_n_plus_2_p_minus_d():  # tests/test_simulator.cpp:113-172
+    for p, n, m in [(4, 8, 4), (8, 8, 4), (8, 16, 4), (2, 4, 2)]:
+        r = P.simulate(p, 1, m, n)
+        for d, dm in enumerate(r["memory"], start=1):
+            assert dm["peak"] == n + 2 * (p - d)
+            assert dm["pool"] == dm["peak"]
+            assert dm["final"] == 0
+
+
+def test_activation_70b_1m_full_is_160gib():  # verify.cpp:85-96
+    mm = P.activation_bytes(P.ModelShape(80, 8192, 28672, 64, 8, 128000), 8, 1, 1, 1, 1 << 20, 1, 1, "full")
+    assert mm["ma"] == 160 * 2**30
