@@ -13,13 +13,12 @@
 #include "pipelab/schedule.hpp"
 #include "pipelab/simulator.hpp"
 #include "pipelab/workload.hpp"
+#include "errors.hpp"
 #include "slimpipe.h"
 
 using namespace pipelab;
 
 namespace {
-
-thread_local std::string g_last_error;
 
 char* to_c(const std::string& s) {
   char* p = static_cast<char*>(std::malloc(s.size() + 1));
@@ -33,11 +32,11 @@ int guarded(char** out, F&& body) {
     *out = to_c(body());
     return SP_OK;
   } catch (const std::invalid_argument& e) {
-    g_last_error = e.what();
+    sp::last_error() = e.what();
     *out = to_c(std::string("{\"error\":\"invalid_argument\",\"what\":\"") + e.what() + "\"}");
     return SP_ERR_INVALID;
   } catch (const std::exception& e) {
-    g_last_error = e.what();
+    sp::last_error() = e.what();
     *out = to_c(std::string("{\"error\":\"runtime_error\",\"what\":\"") + e.what() + "\"}");
     return SP_ERR_RUNTIME;
   }
@@ -112,8 +111,6 @@ std::string annotation_json(const ExchangeAnnotation& ann) {
 }  // namespace
 
 extern "C" {
-
-const char* sp_last_error(void) { return g_last_error.c_str(); }
 
 void sp_free(char* p) { std::free(p); }
 

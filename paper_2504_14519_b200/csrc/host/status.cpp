@@ -1,6 +1,17 @@
 // Status strings and version of the libslimpipe C-ABI (include/slimpipe.h).
 #include "slimpipe.h"
 
+#include <string>
+
+#include "errors.hpp"
+
+namespace sp {
+std::string& last_error() {
+  thread_local std::string msg;
+  return msg;
+}
+}  // namespace sp
+
 extern "C" {
 
 const char* sp_status_string(int code) {
@@ -17,5 +28,7 @@ const char* sp_status_string(int code) {
 }
 
 int sp_version(void) { return 1; }
+
+const char* sp_last_error(void) { return sp::last_error().c_str(); }
 
 }  // extern "C"
