@@ -99,7 +99,7 @@ int sp_attn_fwd(const void* q, int64_t q_rows, int64_t q_stride, const void* k_p
  *   dq_acc  fp32 [q_rows][heads*head_dim]
  *   dk_acc, dv_acc fp32 pools [acc_rows][kv_heads*head_dim]; chunk c's rows
  *           start at acc_row[c] (host array)
- * delta_ws: fp32 [heads][q_rows] scratch (receives rowsum(dO*O)).
+ * delta_ws: fp32 [2][heads][q_rows] scratch (lse*log2e, then rowsum(dO*O)).
  * Runs slices n..1 in the step so a chunk's dK/dV is complete when its own
  * slice's backward runs (reference schedule.cpp:125-126 edge order). */
 int sp_attn_bwd(const void* q, int64_t q_rows, int64_t q_stride, const void* k_pool, const void* v_pool,

@@ -59,7 +59,7 @@ def attn_bwd(q, k_pool, v_pool, chunk_rows, chunk_len, heads, kv_heads, causal, 
     q_rows = q.shape[0]
     d = dq_acc.shape[1] // heads
     if delta_ws is None:
-        delta_ws = torch.empty(heads, q_rows, dtype=torch.float32, device=q.device)
+        delta_ws = torch.empty(2, heads, q_rows, dtype=torch.float32, device=q.device)
     rows, n = _rows(chunk_rows)
     arows, na = _rows(acc_rows)
     assert na == n
