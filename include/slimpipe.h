@@ -116,6 +116,40 @@ int sp_attn_bwd(const void* q, int64_t q_rows, int64_t q_stride, const void* k_p
 int sp_attn_merge(const void* o_a, const float* lse_a, const void* o_b, const float* lse_b, int64_t rows,
                   int heads, int head_dim, int64_t o_stride, void* o_out, float* lse_out, sp_stream_t stream);
 
+/* ---------------------------------------------------------- step executor
+ * One process (rank) per GPU; rank r runs pipeline stage r+1 of
+ * gen_slimpipe(p=pp, v=1, m=microbatches, n=slices) (the drop-in planning
+ * API) with a Llama-style layer stack (layers/pp layers per stage; the
+ * embedding on stage 1, final norm + LM head + cross entropy on stage pp).
+ * Weights are bf16 (fp32 master + AdamW), random-initialised N(0, 0.02)
+ * from `seed`.  The slot arena holds ledger-peak slots of (stage input +
+ * per-layer K/V) — reference simulator.cpp:311-346. */
+typedef struct {
+  int32_t layers, hidden, ffn_hidden, heads, kv_heads, head_dim, vocab;
+  int32_t microbatches, slices, pp, rank, exchange_mode;
+  int64_t seq_len;
+  float rope_theta, norm_eps, lr;
+  uint64_t seed;
+} sp_model_config;
+
+#define SP_STEP_NO_OPTIMIZER 1
+
+int sp_nccl_unique_id(void* out128);
+/* nccl ids (128 bytes each, identical on all ranks) are ignored when pp == 1 */
+int sp_runtime_create(const sp_model_config* cfg, const void* nccl_id_fwd, const void* nccl_id_bwd, void** handle);
+int sp_runtime_destroy(void* handle);
+/* tokens/targets: [microbatches][seq_len] int32 (host, or device when on_device);
+ * only stage 1 reads tokens and only the last stage reads targets (< 0 = ignore).
+ * *loss (last stage) = mean token cross entropy of the step. */
+int sp_runtime_step(void* handle, const int32_t* tokens, const int32_t* targets, int on_device, int flags,
+                    float* loss);
+int sp_runtime_sync(void* handle);
+void* sp_runtime_stream(void* handle);
+int sp_runtime_timeline(void* handle, double* out, int cap);
+int sp_runtime_attn_stats(void* handle, double* out6);
+int sp_runtime_memory(void* handle, int64_t* out7);
+int sp_runtime_param(void* handle, int layer, int which, float* host, int64_t count, int dir);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,89 @@
+// Plain library GEMMs of the layer stack (QKV/O/gate-up/down/LM head and
+// their input/weight gradients) on cuBLASLt: bf16 operands, fp32 accumulate,
+// bf16 or fp32 output, beta for fused residual adds and in-place fp32 weight
+// gradient accumulation.  (The attention contractions, which are the hot
+// path, are the hand-written tcgen05 kernels in attn_fwd.cu / attn_bwd.cu.)
+#include <cublasLt.h>
+
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "kernels.hpp"
+
+namespace sp {
+namespace {
+
+struct Plan {
+  cublasLtMatmulDesc_t op = nullptr;
+  cublasLtMatrixLayout_t a = nullptr, b = nullptr, c = nullptr;
+  cublasLtMatmulAlgo_t algo{};
+};
+
+using Key = std::tuple<int, bool, bool, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, bool>;
+
+struct State {
+  cublasLtHandle_t lt = nullptr;
+  void* ws = nullptr;
+  size_t ws_bytes = 64ull << 20;
+  std::map<Key, Plan> plans;
+  std::mutex mu;
+};
+
+State& state() {
+  static State s;
+  return s;
+}
+
+int lt_status(cublasStatus_t s, const char* what) {
+  if (s == CUBLAS_STATUS_SUCCESS) return SP_OK;
+  return set_error(SP_ERR_CUDA, "cuBLASLt %s failed (status %d)", what, int(s));
+}
+
+}  // namespace
+
+int gemm(bool trans_a, bool trans_b, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, const void* B,
+         int64_t ldb, void* C, int64_t ldc, bool c_f32, float alpha, float beta, cudaStream_t st) {
+  if (M <= 0 || N <= 0 || K <= 0) return SP_OK;
+  State& S = state();
+  std::lock_guard<std::mutex> g(S.mu);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!S.lt) {
+    if (int rc = lt_status(cublasLtCreate(&S.lt), "create")) return rc;
+    if (int rc = cuda_status(cudaMalloc(&S.ws, S.ws_bytes), "gemm workspace")) return rc;
+  }
+  const Key key{dev, trans_a, trans_b, M, N, K, lda, ldb, ldc, c_f32};
+  auto it = S.plans.find(key);
+  if (it == S.plans.end()) {
+    Plan p;
+    // Column-major view: C^T[N,M] = op(B)^T[N,K] * op(A)^T[K,M].
+    if (int rc = lt_status(cublasLtMatmulDescCreate(&p.op, CUBLAS_COMPUTE_32F, CUDA_R_32F), "desc")) return rc;
+    const cublasOperation_t ta = trans_b ? CUBLAS_OP_T : CUBLAS_OP_N;
+    const cublasOperation_t tb = trans_a ? CUBLAS_OP_T : CUBLAS_OP_N;
+    cublasLtMatmulDescSetAttribute(p.op, CUBLASLT_MATMUL_DESC_TRANSA, &ta, sizeof ta);
+    cublasLtMatmulDescSetAttribute(p.op, CUBLASLT_MATMUL_DESC_TRANSB, &tb, sizeof tb);
+    cublasLtMatrixLayoutCreate(&p.a, CUDA_R_16BF, trans_b ? K : N, trans_b ? N : K, ldb);
+    cublasLtMatrixLayoutCreate(&p.b, CUDA_R_16BF, trans_a ? M : K, trans_a ? K : M, lda);
+    cublasLtMatrixLayoutCreate(&p.c, c_f32 ? CUDA_R_32F : CUDA_R_16BF, N, M, ldc);
+    cublasLtMatmulPreference_t pref;
+    cublasLtMatmulPreferenceCreate(&pref);
+    cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &S.ws_bytes,
+                                         sizeof S.ws_bytes);
+    cublasLtMatmulHeuristicResult_t res{};
+    int found = 0;
+    cublasStatus_t hs = cublasLtMatmulAlgoGetHeuristic(S.lt, p.op, p.a, p.b, p.c, p.c, pref, 1, &res, &found);
+    cublasLtMatmulPreferenceDestroy(pref);
+    if (hs != CUBLAS_STATUS_SUCCESS || found == 0)
+      return set_error(SP_ERR_CUDA, "cuBLASLt: no algorithm for %lldx%lldx%lld", (long long)M, (long long)N,
+                       (long long)K);
+    p.algo = res.algo;
+    it = S.plans.emplace(key, p).first;
+  }
+  const Plan& p = it->second;
+  return lt_status(cublasLtMatmul(S.lt, p.op, &alpha, B, p.a, A, p.b, &beta, C, p.c, C, p.c, &p.algo, S.ws,
+                                  S.ws_bytes, st),
+                   "matmul");
+}
+
+}  // namespace sp

@@ -1,0 +1,42 @@
+// Internal (C++) launch interface of the device ops used by the step
+// executor.  All return SP_* status codes; all run on the given stream.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "slimpipe.h"
+
+namespace sp {
+
+int set_error(int code, const char* fmt, ...);
+int cuda_status(cudaError_t e, const char* what);
+
+// layers.cu
+int embed_fwd(const int32_t* tok, const void* table, void* out, int64_t rows, int dim, cudaStream_t st);
+int embed_bwd(const int32_t* tok, const void* dy, float* dtable, int64_t rows, int dim, cudaStream_t st);
+int rmsnorm_fwd(const void* x, const void* w, void* y, float* rstd, int64_t rows, int dim, float eps, cudaStream_t st);
+int rmsnorm_bwd(const void* dy, const void* x, const void* w, const float* rstd, const void* dx_in, void* dx_out,
+                float* dw, int64_t rows, int dim, cudaStream_t st);
+int rope_qkv_fwd(const void* qkv, int64_t rows, int heads, int kv_heads, int d, int64_t pos0, float theta, void* q_out,
+                 int64_t q_stride, void* k_out, void* v_out, int64_t kv_stride, cudaStream_t st);
+int rope_qkv_bwd(const float* dq, float* dk, float* dv, int64_t kv_stride, int64_t rows, int heads, int kv_heads,
+                 int d, int64_t pos0, float theta, void* dqkv, int zero_kv, cudaStream_t st);
+int swiglu_fwd(const void* gu, void* act, int64_t rows, int H, cudaStream_t st);
+int swiglu_bwd(const void* dact, const void* gu, void* dgu, int64_t rows, int H, cudaStream_t st);
+int cross_entropy(const float* logits, const int32_t* tgt, int64_t rows, int V, float scale, void* dlogits,
+                  float* loss_sum, cudaStream_t st);
+int adamw(float* master, void* wbf, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2,
+          float eps, float wd, int step, cudaStream_t st);
+int init_params(float* master, void* wbf, int64_t n, uint64_t seed, float stdv, float constant, int use_const,
+                cudaStream_t st);
+int f32_to_bf16(const float* a, void* b, int64_t n, cudaStream_t st);
+
+// gemm.cu — row-major GEMMs on cuBLASLt (bf16 inputs, fp32 accumulate).
+//   C[M,N] = alpha * op(A) op(B) + beta * C
+//   A is [M,K] (or [K,M] when trans_a), B is [K,N] (or [N,K] when trans_b),
+//   lda/ldb/ldc are row pitches in elements.  c_f32 selects an fp32 C/D.
+int gemm(bool trans_a, bool trans_b, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, const void* B,
+         int64_t ldb, void* C, int64_t ldc, bool c_f32, float alpha, float beta, cudaStream_t st);
+
+}  // namespace sp

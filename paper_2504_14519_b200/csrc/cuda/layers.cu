@@ -1,0 +1,468 @@
+// K7: the HBM-bound transformer-layer ops of the sliced step (the reference
+// has no model; these follow standard Llama definitions).  All kernels are
+// vectorised (16-B accesses), one warp or block per token row, fp32 math on
+// bf16 storage; reductions for weight gradients are block-partial then one
+// fp32 atomic per element per block.
+#include <math.h>
+
+#include "errors.hpp"
+#include "kernels.hpp"
+#include "sm100.cuh"
+
+namespace sp {
+namespace {
+
+using bf16 = __nv_bfloat16;
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) v += __shfl_xor_sync(0xffffffffu, v, s);
+  return v;
+}
+
+__device__ __forceinline__ void load8(const bf16* p, float (&f)[8]) {
+  const uint4 u = *reinterpret_cast<const uint4*>(p);
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 t = __bfloat1622float2(h[i]);
+    f[2 * i] = t.x;
+    f[2 * i + 1] = t.y;
+  }
+}
+
+__device__ __forceinline__ void store8(bf16* p, const float (&f)[8]) {
+  uint4 u;
+  u.x = pack_bf16(f[0], f[1]);
+  u.y = pack_bf16(f[2], f[3]);
+  u.z = pack_bf16(f[4], f[5]);
+  u.w = pack_bf16(f[6], f[7]);
+  *reinterpret_cast<uint4*>(p) = u;
+}
+
+// ---- embedding --------------------------------------------------------------
+__global__ void embed_fwd_k(const int32_t* __restrict__ tok, const bf16* __restrict__ table, bf16* __restrict__ out,
+                            int64_t rows, int dim) {
+  const int64_t r = blockIdx.x;
+  const int64_t t = tok[r];
+  const uint4* src = reinterpret_cast<const uint4*>(table + t * dim);
+  uint4* dst = reinterpret_cast<uint4*>(out + r * dim);
+  for (int c = threadIdx.x; c < dim / 8; c += blockDim.x) dst[c] = src[c];
+}
+
+__global__ void embed_bwd_k(const int32_t* __restrict__ tok, const bf16* __restrict__ dy, float* __restrict__ dtab,
+                            int64_t rows, int dim) {
+  const int64_t r = blockIdx.x;
+  const int64_t t = tok[r];
+  for (int c = threadIdx.x * 8; c < dim; c += blockDim.x * 8) {
+    float f[8];
+    load8(dy + r * dim + c, f);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) atomicAdd(dtab + t * dim + c + i, f[i]);
+  }
+}
+
+// ---- RMSNorm ------------------------------------------------------------------
+// y = x * rstd * w, rstd = 1/sqrt(mean(x^2) + eps).  One block (dim/8 threads
+// rounded to a warp multiple, <= 1024) per row.
+template <int kMaxVec>
+__global__ void rmsnorm_fwd_k(const bf16* __restrict__ x, const bf16* __restrict__ w, bf16* __restrict__ y,
+                              float* __restrict__ rstd_out, int dim, float eps) {
+  const int64_t r = blockIdx.x;
+  const bf16* xr = x + r * dim;
+  float v[kMaxVec][8];
+  float ss = 0.f;
+#pragma unroll
+  for (int i = 0; i < kMaxVec; ++i) {
+    const int c = (threadIdx.x + i * blockDim.x) * 8;
+    if (c < dim) {
+      load8(xr + c, v[i]);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) ss += v[i][e] * v[i][e];
+    }
+  }
+  __shared__ float red[32];
+  ss = warp_sum(ss);
+  if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float t = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.f;
+    t = warp_sum(t);
+    if (threadIdx.x == 0) red[0] = t;
+  }
+  __syncthreads();
+  const float rs = rsqrtf(red[0] / dim + eps);
+  if (threadIdx.x == 0 && rstd_out) rstd_out[r] = rs;
+#pragma unroll
+  for (int i = 0; i < kMaxVec; ++i) {
+    const int c = (threadIdx.x + i * blockDim.x) * 8;
+    if (c < dim) {
+      float wf[8], o[8];
+      load8(w + c, wf);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) o[e] = v[i][e] * rs * wf[e];
+      store8(y + r * dim + c, o);
+    }
+  }
+}
+
+// dx = rstd * (w*dy - x * rstd^2 * mean(x * w*dy)) (+ residual dx_in);
+// dw += sum_rows dy * x * rstd.  Block handles `rows_per_block` rows and
+// keeps its dw partial in registers (dim/8/threads vectors per thread).
+template <int kMaxVec>
+__global__ void rmsnorm_bwd_k(const bf16* __restrict__ dy, const bf16* __restrict__ x, const bf16* __restrict__ w,
+                              const float* __restrict__ rstd, const bf16* dx_in, bf16* dx_out, float* __restrict__ dw,
+                              int64_t rows, int dim, int rows_per_block) {
+  float dwp[kMaxVec][8];
+#pragma unroll
+  for (int i = 0; i < kMaxVec; ++i)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) dwp[i][e] = 0.f;
+  __shared__ float red[32];
+  const int64_t r0 = int64_t(blockIdx.x) * rows_per_block;
+  for (int64_t r = r0; r < r0 + rows_per_block && r < rows; ++r) {
+    const float rs = rstd[r];
+    float xv[kMaxVec][8], g[kMaxVec][8];
+    float dot = 0.f;
+#pragma unroll
+    for (int i = 0; i < kMaxVec; ++i) {
+      const int c = (threadIdx.x + i * blockDim.x) * 8;
+      if (c < dim) {
+        float dyv[8], wf[8];
+        load8(dy + r * dim + c, dyv);
+        load8(x + r * dim + c, xv[i]);
+        load8(w + c, wf);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          g[i][e] = dyv[e] * wf[e];
+          dot += g[i][e] * xv[i][e];
+          dwp[i][e] += dyv[e] * xv[i][e] * rs;
+        }
+      }
+    }
+    dot = warp_sum(dot);
+    __syncthreads();
+    if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = dot;
+    __syncthreads();
+    float tot = 0.f;
+    for (int i = 0; i < int(blockDim.x / 32); ++i) tot += red[i];
+    const float coef = tot / dim * rs * rs;
+#pragma unroll
+    for (int i = 0; i < kMaxVec; ++i) {
+      const int c = (threadIdx.x + i * blockDim.x) * 8;
+      if (c < dim) {
+        float o[8], res[8];
+        if (dx_in) load8(dx_in + r * dim + c, res);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) o[e] = rs * (g[i][e] - xv[i][e] * coef) + (dx_in ? res[e] : 0.f);
+        store8(dx_out + r * dim + c, o);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < kMaxVec; ++i) {
+    const int c = (threadIdx.x + i * blockDim.x) * 8;
+    if (c < dim)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) atomicAdd(dw + c + e, dwp[i][e]);
+  }
+}
+
+// ---- RoPE (rotate-half convention over head_dim) ---------------------------------
+// qkv row: [q (heads*d) | k (kv*d) | v (kv*d)].  Writes rotated q to q_out,
+// rotated k and v into the K/V pool rows.  pos = pos0 + row.
+__device__ __forceinline__ void rope_cs(int64_t pos, int j, int d, float theta, float& c, float& s) {
+  const float inv = exp2f(-2.f * float(j) / float(d) * log2f(theta));
+  const float ang = float(pos) * inv;
+  sincosf(ang, &s, &c);
+}
+
+__global__ void rope_qkv_fwd_k(const bf16* __restrict__ qkv, int64_t rows, int heads, int kv_heads, int d,
+                               int64_t pos0, float theta, bf16* __restrict__ q_out, int64_t q_stride,
+                               bf16* __restrict__ k_out, bf16* __restrict__ v_out, int64_t kv_stride) {
+  const int64_t r = blockIdx.x;
+  const int width = (heads + 2 * kv_heads) * d;
+  const bf16* src = qkv + r * width;
+  const int half = d / 2;
+  const int pairs = (heads + kv_heads) * half;
+  for (int idx = threadIdx.x; idx < pairs; idx += blockDim.x) {
+    const int h = idx / half, j = idx % half;
+    float c, s;
+    rope_cs(pos0 + r, j, d, theta, c, s);
+    const float x1 = __bfloat162float(src[h * d + j]), x2 = __bfloat162float(src[h * d + j + half]);
+    const float y1 = x1 * c - x2 * s, y2 = x2 * c + x1 * s;
+    if (h < heads) {
+      q_out[r * q_stride + h * d + j] = __float2bfloat16(y1);
+      q_out[r * q_stride + h * d + j + half] = __float2bfloat16(y2);
+    } else {
+      const int kh = h - heads;
+      k_out[r * kv_stride + kh * d + j] = __float2bfloat16(y1);
+      k_out[r * kv_stride + kh * d + j + half] = __float2bfloat16(y2);
+    }
+  }
+  for (int idx = threadIdx.x; idx < kv_heads * d; idx += blockDim.x)
+    v_out[r * kv_stride + idx] = src[(heads + kv_heads) * d + idx];
+}
+
+// Inverse rotation of fp32 gradients into the bf16 d_qkv row.  dq rows come
+// from dq (q_rows x heads*d); dk/dv from the chunk accumulators (zeroed after
+// reading when `zero_kv`).
+__global__ void rope_qkv_bwd_k(const float* __restrict__ dq, float* dk, float* dv, int64_t kv_stride, int64_t rows,
+                               int heads, int kv_heads, int d, int64_t pos0, float theta, bf16* __restrict__ dqkv,
+                               int zero_kv) {
+  const int64_t r = blockIdx.x;
+  const int width = (heads + 2 * kv_heads) * d;
+  bf16* dst = dqkv + r * width;
+  const int half = d / 2;
+  const int pairs = (heads + kv_heads) * half;
+  for (int idx = threadIdx.x; idx < pairs; idx += blockDim.x) {
+    const int h = idx / half, j = idx % half;
+    float c, s;
+    rope_cs(pos0 + r, j, d, theta, c, s);
+    float g1, g2;
+    if (h < heads) {
+      g1 = dq[r * heads * d + h * d + j];
+      g2 = dq[r * heads * d + h * d + j + half];
+    } else {
+      float* p = dk + r * kv_stride + (h - heads) * d;
+      g1 = p[j];
+      g2 = p[j + half];
+      if (zero_kv) p[j] = p[j + half] = 0.f;
+    }
+    // y1 = x1 c - x2 s ; y2 = x2 c + x1 s  =>  dx1 = g1 c + g2 s ; dx2 = g2 c - g1 s
+    dst[h * d + j] = __float2bfloat16(g1 * c + g2 * s);
+    dst[h * d + j + half] = __float2bfloat16(g2 * c - g1 * s);
+  }
+  for (int idx = threadIdx.x; idx < kv_heads * d; idx += blockDim.x) {
+    float* p = dv + r * kv_stride + idx;
+    dst[(heads + kv_heads) * d + idx] = __float2bfloat16(*p);
+    if (zero_kv) *p = 0.f;
+  }
+}
+
+// ---- SwiGLU -------------------------------------------------------------------
+// gu row = [gate (H) | up (H)]; act = silu(gate) * up.
+__global__ void swiglu_fwd_k(const bf16* __restrict__ gu, bf16* __restrict__ act, int64_t rows, int H) {
+  const int64_t n8 = rows * H / 8;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n8; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = i * 8 / H, c = i * 8 % H;
+    float g[8], u[8], o[8];
+    load8(gu + r * 2 * H + c, g);
+    load8(gu + r * 2 * H + H + c, u);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) o[e] = g[e] / (1.f + __expf(-g[e])) * u[e];
+    store8(act + r * H + c, o);
+  }
+}
+
+__global__ void swiglu_bwd_k(const bf16* __restrict__ dact, const bf16* __restrict__ gu, bf16* __restrict__ dgu,
+                             int64_t rows, int H) {
+  const int64_t n8 = rows * H / 8;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n8; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = i * 8 / H, c = i * 8 % H;
+    float g[8], u[8], da[8], dg[8], du[8];
+    load8(gu + r * 2 * H + c, g);
+    load8(gu + r * 2 * H + H + c, u);
+    load8(dact + r * H + c, da);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float sg = 1.f / (1.f + __expf(-g[e]));
+      const float silu = g[e] * sg;
+      du[e] = da[e] * silu;
+      dg[e] = da[e] * u[e] * (sg * (1.f + g[e] * (1.f - sg)));
+    }
+    store8(dgu + r * 2 * H + c, dg);
+    store8(dgu + r * 2 * H + H + c, du);
+  }
+}
+
+// ---- cross entropy over fp32 logits -----------------------------------------------
+// loss_sum += sum_r (lse_r - logit[r, t_r]); dlogits = (softmax - onehot) * scale
+// (bf16).  Targets < 0 are ignored.  One block per row.
+__global__ void xent_k(const float* __restrict__ logits, const int32_t* __restrict__ tgt, int64_t rows, int V,
+                       float scale, bf16* __restrict__ dlogits, float* __restrict__ loss_sum) {
+  const int64_t r = blockIdx.x;
+  const float* lr = logits + r * V;
+  __shared__ float red[32];
+  __shared__ float bcast;
+  float mx = -INFINITY;
+  for (int c = threadIdx.x * 4; c < V; c += blockDim.x * 4) {
+    const float4 v = *reinterpret_cast<const float4*>(lr + c);
+    mx = fmaxf(mx, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
+  }
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, s));
+  if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float m = -INFINITY;
+    for (int i = 0; i < int(blockDim.x / 32); ++i) m = fmaxf(m, red[i]);
+    bcast = m;
+  }
+  __syncthreads();
+  mx = bcast;
+  float se = 0.f;
+  for (int c = threadIdx.x * 4; c < V; c += blockDim.x * 4) {
+    const float4 v = *reinterpret_cast<const float4*>(lr + c);
+    se += __expf(v.x - mx) + __expf(v.y - mx) + __expf(v.z - mx) + __expf(v.w - mx);
+  }
+  se = warp_sum(se);
+  __syncthreads();
+  if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = se;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float s = 0.f;
+    for (int i = 0; i < int(blockDim.x / 32); ++i) s += red[i];
+    bcast = s;
+  }
+  __syncthreads();
+  const float lse = mx + __logf(bcast);
+  const int t = tgt[r];
+  const float inv = 1.f / bcast;
+  for (int c = threadIdx.x * 4; c < V; c += blockDim.x * 4) {
+    const float4 v = *reinterpret_cast<const float4*>(lr + c);
+    float p[4] = {__expf(v.x - mx) * inv, __expf(v.y - mx) * inv, __expf(v.z - mx) * inv, __expf(v.w - mx) * inv};
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if (c + e == t) p[e] -= 1.f;
+    const float sc = t >= 0 ? scale : 0.f;
+    uint2 u;
+    u.x = pack_bf16(p[0] * sc, p[1] * sc);
+    u.y = pack_bf16(p[2] * sc, p[3] * sc);
+    *reinterpret_cast<uint2*>(dlogits + r * V + c) = u;
+  }
+  if (threadIdx.x == 0 && t >= 0) atomicAdd(loss_sum, lse - lr[t]);
+}
+
+// ---- AdamW over flat fp32 master weights --------------------------------------
+__global__ void adamw_k(float* __restrict__ master, bf16* __restrict__ wbf, const float* __restrict__ g,
+                        float* __restrict__ m, float* __restrict__ v, int64_t n, float lr, float b1, float b2,
+                        float eps, float wd, float c1, float c2) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const float gi = g[i];
+    const float mi = b1 * m[i] + (1.f - b1) * gi;
+    const float vi = b2 * v[i] + (1.f - b2) * gi * gi;
+    m[i] = mi;
+    v[i] = vi;
+    float w = master[i];
+    w -= lr * (mi * c1 / (sqrtf(vi * c2) + eps) + wd * w);
+    master[i] = w;
+    wbf[i] = __float2bfloat16(w);
+  }
+}
+
+// ---- deterministic init: N(0, std) from a counter hash (Box-Muller) ----------
+__device__ __forceinline__ uint32_t hash32(uint64_t x) {
+  x ^= x >> 33;
+  x *= 0xff51afd7ed558ccdULL;
+  x ^= x >> 33;
+  x *= 0xc4ceb9fe1a85ec53ULL;
+  x ^= x >> 33;
+  return uint32_t(x);
+}
+
+__global__ void init_normal_k(float* __restrict__ master, bf16* __restrict__ wbf, int64_t n, uint64_t seed, float stdv,
+                              float constant, int use_const) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    float val = constant;
+    if (!use_const) {
+      const float u1 = (hash32(seed * 0x9E3779B97F4A7C15ULL + 2 * i) + 1.f) * 2.3283064365386963e-10f;
+      const float u2 = hash32(seed * 0x9E3779B97F4A7C15ULL + 2 * i + 1) * 2.3283064365386963e-10f;
+      val = stdv * sqrtf(-2.f * __logf(u1)) * __cosf(6.2831853071795864f * u2);
+    }
+    master[i] = val;
+    wbf[i] = __float2bfloat16(val);
+  }
+}
+
+__global__ void f32_to_bf16_k(const float* __restrict__ a, bf16* __restrict__ b, int64_t n) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    b[i] = __float2bfloat16(a[i]);
+}
+
+int grid_for(int64_t work, int block) {
+  int64_t g = (work + block - 1) / block;
+  return int(g < 148 * 32 ? (g > 0 ? g : 1) : 148 * 32);
+}
+
+}  // namespace
+
+int embed_fwd(const int32_t* tok, const void* table, void* out, int64_t rows, int dim, cudaStream_t st) {
+  if (dim % 8) return set_error(SP_ERR_UNSUPPORTED, "embed: dim %% 8");
+  embed_fwd_k<<<unsigned(rows), 128, 0, st>>>(tok, (const bf16*)table, (bf16*)out, rows, dim);
+  return cuda_status(cudaGetLastError(), "embed_fwd");
+}
+
+int embed_bwd(const int32_t* tok, const void* dy, float* dtable, int64_t rows, int dim, cudaStream_t st) {
+  embed_bwd_k<<<unsigned(rows), 128, 0, st>>>(tok, (const bf16*)dy, dtable, rows, dim);
+  return cuda_status(cudaGetLastError(), "embed_bwd");
+}
+
+int rmsnorm_fwd(const void* x, const void* w, void* y, float* rstd, int64_t rows, int dim, float eps, cudaStream_t st) {
+  if (dim % 8 || dim > 8 * 1024 * 4) return set_error(SP_ERR_UNSUPPORTED, "rmsnorm: dim");
+  int threads = ((dim / 8 + 3) / 4 + 31) / 32 * 32;  // 4 vectors per thread
+  if (threads < 32) threads = 32;
+  rmsnorm_fwd_k<4><<<unsigned(rows), threads, 0, st>>>((const bf16*)x, (const bf16*)w, (bf16*)y, rstd, dim, eps);
+  return cuda_status(cudaGetLastError(), "rmsnorm_fwd");
+}
+
+int rmsnorm_bwd(const void* dy, const void* x, const void* w, const float* rstd, const void* dx_in, void* dx_out,
+                float* dw, int64_t rows, int dim, cudaStream_t st) {
+  int threads = ((dim / 8 + 3) / 4 + 31) / 32 * 32;
+  if (threads < 32) threads = 32;
+  const int rpb = 32;
+  rmsnorm_bwd_k<4><<<unsigned((rows + rpb - 1) / rpb), threads, 0, st>>>(
+      (const bf16*)dy, (const bf16*)x, (const bf16*)w, rstd, (const bf16*)dx_in, (bf16*)dx_out, dw, rows, dim, rpb);
+  return cuda_status(cudaGetLastError(), "rmsnorm_bwd");
+}
+
+int rope_qkv_fwd(const void* qkv, int64_t rows, int heads, int kv_heads, int d, int64_t pos0, float theta, void* q_out,
+                 int64_t q_stride, void* k_out, void* v_out, int64_t kv_stride, cudaStream_t st) {
+  rope_qkv_fwd_k<<<unsigned(rows), 256, 0, st>>>((const bf16*)qkv, rows, heads, kv_heads, d, pos0, theta, (bf16*)q_out,
+                                                 q_stride, (bf16*)k_out, (bf16*)v_out, kv_stride);
+  return cuda_status(cudaGetLastError(), "rope_qkv_fwd");
+}
+
+int rope_qkv_bwd(const float* dq, float* dk, float* dv, int64_t kv_stride, int64_t rows, int heads, int kv_heads,
+                 int d, int64_t pos0, float theta, void* dqkv, int zero_kv, cudaStream_t st) {
+  rope_qkv_bwd_k<<<unsigned(rows), 256, 0, st>>>(dq, dk, dv, kv_stride, rows, heads, kv_heads, d, pos0, theta,
+                                                 (bf16*)dqkv, zero_kv);
+  return cuda_status(cudaGetLastError(), "rope_qkv_bwd");
+}
+
+int swiglu_fwd(const void* gu, void* act, int64_t rows, int H, cudaStream_t st) {
+  swiglu_fwd_k<<<grid_for(rows * H / 8, 256), 256, 0, st>>>((const bf16*)gu, (bf16*)act, rows, H);
+  return cuda_status(cudaGetLastError(), "swiglu_fwd");
+}
+
+int swiglu_bwd(const void* dact, const void* gu, void* dgu, int64_t rows, int H, cudaStream_t st) {
+  swiglu_bwd_k<<<grid_for(rows * H / 8, 256), 256, 0, st>>>((const bf16*)dact, (const bf16*)gu, (bf16*)dgu, rows, H);
+  return cuda_status(cudaGetLastError(), "swiglu_bwd");
+}
+
+int cross_entropy(const float* logits, const int32_t* tgt, int64_t rows, int V, float scale, void* dlogits,
+                  float* loss_sum, cudaStream_t st) {
+  if (V % 4) return set_error(SP_ERR_UNSUPPORTED, "cross_entropy: vocab %% 4");
+  xent_k<<<unsigned(rows), 256, 0, st>>>(logits, tgt, rows, V, scale, (bf16*)dlogits, loss_sum);
+  return cuda_status(cudaGetLastError(), "cross_entropy");
+}
+
+int adamw(float* master, void* wbf, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2,
+          float eps, float wd, int step, cudaStream_t st) {
+  const float c1 = 1.f / (1.f - powf(b1, float(step))), c2 = 1.f / (1.f - powf(b2, float(step)));
+  adamw_k<<<grid_for(n, 256), 256, 0, st>>>(master, (bf16*)wbf, g, m, v, n, lr, b1, b2, eps, wd, c1, c2);
+  return cuda_status(cudaGetLastError(), "adamw");
+}
+
+int init_params(float* master, void* wbf, int64_t n, uint64_t seed, float stdv, float constant, int use_const,
+                cudaStream_t st) {
+  init_normal_k<<<grid_for(n, 256), 256, 0, st>>>(master, (bf16*)wbf, n, seed, stdv, constant, use_const);
+  return cuda_status(cudaGetLastError(), "init_params");
+}
+
+int f32_to_bf16(const float* a, void* b, int64_t n, cudaStream_t st) {
+  f32_to_bf16_k<<<grid_for(n, 256), 256, 0, st>>>(a, (bf16*)b, n);
+  return cuda_status(cudaGetLastError(), "f32_to_bf16");
+}
+
+}  // namespace sp

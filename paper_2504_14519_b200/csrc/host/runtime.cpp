@@ -1,0 +1,707 @@
+// The B200 sliced-1F1B step executor: one process (rank) per GPU, pipeline
+// stage s = rank + 1 (v = 1, reference stage_owner schedule.cpp:158-164).
+//
+// It walks device_order[rank] of gen_slimpipe (bit-exact host planning) and
+// executes each pass on the GPU:
+//   F(k,i,s):  acquire an arena slot (reference ledger simulator.cpp:324-327),
+//              stage input = embedding (s=1) or NCCL recv from s-1; for every
+//              layer: RMSNorm -> QKV GEMM -> RoPE (K/V written into the slot's
+//              rows of the layer's KV pool) -> K1 sliced attention over the
+//              slots of slices 1..i -> O GEMM + residual -> RMSNorm -> gate/up
+//              GEMM -> SwiGLU -> down GEMM + residual; send to s+1.
+//   BW(k,i,s): full recompute of the stage from the stashed input (Full
+//              checkpointing, reference workload.cpp:100-104), then the layer
+//              backward in reverse with K2 accumulating dK/dV of chunks 1..i
+//              into fp32 chunk accumulators (complete for chunk i now, since
+//              slices n..i+1 ran before: schedule.cpp:125-126), LM head + loss
+//              on the last stage, embedding grad on the first; send dX to s-1;
+//              release the slot (simulator.cpp:328-331).
+// Streams: compute, comm_fwd (activations s->s+1), comm_bwd (gradients
+// s->s-1); each direction has its own NCCL communicator so the two never
+// block each other.  CUDA events order buffers between the streams.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "errors.hpp"
+#include "kernels.hpp"
+#include "pipelab/schedule.hpp"
+#include "pipelab/simulator.hpp"
+#include "slimpipe.h"
+
+namespace sp {
+namespace {
+
+#define SP_TRY(expr)           \
+  do {                         \
+    int rc_ = (expr);          \
+    if (rc_ != SP_OK) return rc_; \
+  } while (0)
+
+#define SP_CUDA(expr) SP_TRY(cuda_status((expr), #expr))
+
+int nccl_status(ncclResult_t r, const char* what) {
+  if (r == ncclSuccess) return SP_OK;
+  return set_error(SP_ERR_NCCL, "%s: %s", what, ncclGetErrorString(r));
+}
+#define SP_NCCL(expr) SP_TRY(nccl_status((expr), #expr))
+
+using bf16raw = uint16_t;
+
+struct LayerParams {
+  int64_t attn_norm, wqkv, wo, mlp_norm, wgu, wd;
+};
+
+struct LayerWs {
+  bf16raw *x_in, *xn, *q, *o, *x_mid, *xn2, *gu, *act;
+  float *lse, *rstd1, *rstd2;
+};
+
+struct PassTime {
+  int pass;
+  cudaEvent_t start, end;
+};
+
+struct AttnTimer {
+  cudaEvent_t a, b;
+  double flops;
+  int kind;  // 0 fwd, 1 bwd
+};
+
+class Runtime {
+ public:
+  sp_model_config cfg{};
+  int rank = 0, p = 1, stage = 1, Lps = 1;
+  int64_t Ls = 0, h = 0, H = 0, qd = 0, kvd = 0, qkv_w = 0;
+  pipelab::Schedule sched;
+  std::vector<pipelab::PassId> order;
+  pipelab::MemoryLedger ledger;
+
+  // parameters (flat)
+  int64_t n_params = 0;
+  bf16raw* w = nullptr;
+  float *master = nullptr, *grad = nullptr, *adam_m = nullptr, *adam_v = nullptr;
+  std::vector<LayerParams> lp;
+  int64_t emb = -1, final_norm = -1, head = -1;
+  int opt_step = 0;
+
+  // arena: x stash + per-layer K/V pools, `slots` slice-sized slots
+  int slots = 0;
+  bf16raw* x_pool = nullptr;
+  std::vector<bf16raw*> k_pool, v_pool;
+  std::vector<int> free_slots;
+  std::map<std::pair<int, int>, int> slot_of;
+  int slots_in_use = 0, slots_high_water = 0;
+  // fp32 dK/dV chunk accumulators (one microbatch, indexed by slice)
+  std::vector<float*> dk_acc, dv_acc;
+
+  // workspaces
+  std::vector<LayerWs> ws;
+  bf16raw *x_final = nullptr, *qkv = nullptr, *dqkv = nullptr, *tmp_h = nullptr, *tmp_H = nullptr,
+          *tmp_2H = nullptr, *xf = nullptr, *dlogits = nullptr;
+  bf16raw* out_buf[2] = {nullptr, nullptr};  // stage outputs (send to s+1)
+  bf16raw* gin_buf[2] = {nullptr, nullptr};  // gradients received from s+1
+  bf16raw* gout_buf[2] = {nullptr, nullptr}; // gradients sent to s-1 (dx)
+  float *dq_acc = nullptr, *delta_ws = nullptr, *logits = nullptr, *rstd_f = nullptr, *loss_dev = nullptr;
+  int32_t *tokens = nullptr, *targets = nullptr;
+
+  cudaStream_t comp = nullptr, cfwd = nullptr, cbwd = nullptr;
+  ncclComm_t nc_fwd = nullptr, nc_bwd = nullptr;
+  cudaEvent_t ev_out_free[2]{}, ev_gin_free[2]{}, ev_gout_free[2]{};
+  int out_idx = 0, gin_idx = 0, gout_idx = 0;
+  std::vector<PassTime> times;
+  std::vector<AttnTimer> attn_times;
+  cudaEvent_t step_start = nullptr, step_end = nullptr;
+  size_t bytes_allocated = 0;
+  std::vector<void*> allocations;
+
+  ~Runtime() {
+    if (comp) cudaStreamSynchronize(comp);
+    for (void* a : allocations) cudaFree(a);
+    if (nc_fwd) ncclCommDestroy(nc_fwd);
+    if (nc_bwd) ncclCommDestroy(nc_bwd);
+    for (auto& t : times) {
+      cudaEventDestroy(t.start);
+      cudaEventDestroy(t.end);
+    }
+    for (auto& t : attn_times) {
+      cudaEventDestroy(t.a);
+      cudaEventDestroy(t.b);
+    }
+  }
+
+  template <class T>
+  int alloc(T** ptr, int64_t count) {
+    void* raw = nullptr;
+    const size_t bytes = size_t(std::max<int64_t>(count, 1)) * sizeof(T);
+    SP_CUDA(cudaMalloc(&raw, bytes));
+    allocations.push_back(raw);
+    bytes_allocated += bytes;
+    *ptr = static_cast<T*>(raw);
+    return SP_OK;
+  }
+
+  bf16raw* W(int64_t off) { return w + off; }
+  float* G(int64_t off) { return grad + off; }
+
+  int init(const sp_model_config& c, const void* id_fwd, const void* id_bwd) {
+    cfg = c;
+    rank = c.rank;
+    p = c.pp;
+    stage = rank + 1;
+    if (c.layers % p) return set_error(SP_ERR_INVALID, "layers (%d) must divide by pp (%d)", c.layers, p);
+    if (c.seq_len % c.slices) return set_error(SP_ERR_INVALID, "run: seq_len must be divisible by slices");
+    if (c.hidden != c.heads * c.head_dim) return set_error(SP_ERR_INVALID, "hidden != heads * head_dim");
+    Lps = c.layers / p;
+    Ls = c.seq_len / c.slices;
+    h = c.hidden;
+    H = c.ffn_hidden;
+    qd = int64_t(c.heads) * c.head_dim;
+    kvd = int64_t(c.kv_heads) * c.head_dim;
+    qkv_w = qd + 2 * kvd;
+    if (Ls % 128) return set_error(SP_ERR_UNSUPPORTED, "slice length must be a multiple of 128");
+
+    pipelab::GenConfig gc;
+    gc.p = p;
+    gc.v = 1;
+    gc.m = c.microbatches;
+    gc.n = c.slices;
+    gc.seq_len = c.seq_len;
+    try {
+      sched = pipelab::gen_slimpipe(gc);
+    } catch (const std::exception& e) {
+      return set_error(SP_ERR_INVALID, "%s", e.what());
+    }
+    const pipelab::Diagnostics diag = pipelab::validate_schedule(sched);
+    if (!diag.ok()) return set_error(SP_ERR_RUNTIME, "schedule invalid: %s", diag.first()->message.c_str());
+    order = sched.device_order[rank];
+    ledger = pipelab::ledger_from_order(sched, pipelab::unit_memory_model(p, 1, c.slices));
+    slots = int(ledger.per_device[rank].chunk_pool_size);
+
+    SP_CUDA(cudaStreamCreateWithFlags(&comp, cudaStreamNonBlocking));
+    SP_CUDA(cudaStreamCreateWithFlags(&cfwd, cudaStreamNonBlocking));
+    SP_CUDA(cudaStreamCreateWithFlags(&cbwd, cudaStreamNonBlocking));
+    for (int x = 0; x < 2; ++x) {
+      SP_CUDA(cudaEventCreateWithFlags(&ev_out_free[x], cudaEventDisableTiming));
+      SP_CUDA(cudaEventCreateWithFlags(&ev_gin_free[x], cudaEventDisableTiming));
+      SP_CUDA(cudaEventCreateWithFlags(&ev_gout_free[x], cudaEventDisableTiming));
+      SP_CUDA(cudaEventRecord(ev_out_free[x], comp));
+      SP_CUDA(cudaEventRecord(ev_gin_free[x], comp));
+      SP_CUDA(cudaEventRecord(ev_gout_free[x], comp));
+    }
+    SP_CUDA(cudaEventCreate(&step_start));
+    SP_CUDA(cudaEventCreate(&step_end));
+
+    if (p > 1) {
+      ncclUniqueId a, b;
+      std::memcpy(&a, id_fwd, sizeof a);
+      std::memcpy(&b, id_bwd, sizeof b);
+      SP_NCCL(ncclCommInitRank(&nc_fwd, p, a, rank));
+      SP_NCCL(ncclCommInitRank(&nc_bwd, p, b, rank));
+    }
+    SP_TRY(alloc_params());
+    SP_TRY(alloc_arena());
+    SP_TRY(alloc_workspace());
+    SP_TRY(init_weights(c.seed));
+    SP_CUDA(cudaStreamSynchronize(comp));
+    return SP_OK;
+  }
+
+  int alloc_params() {
+    auto take = [&](int64_t n) {
+      const int64_t off = n_params;
+      n_params += (n + 127) / 128 * 128;
+      return off;
+    };
+    lp.resize(Lps);
+    for (int l = 0; l < Lps; ++l) {
+      lp[l].attn_norm = take(h);
+      lp[l].wqkv = take(qkv_w * h);
+      lp[l].wo = take(h * qd);
+      lp[l].mlp_norm = take(h);
+      lp[l].wgu = take(2 * H * h);
+      lp[l].wd = take(h * H);
+    }
+    if (stage == 1) emb = take(int64_t(cfg.vocab) * h);
+    if (stage == p) {
+      final_norm = take(h);
+      head = take(int64_t(cfg.vocab) * h);
+    }
+    SP_TRY(alloc(&w, n_params));
+    SP_TRY(alloc(&master, n_params));
+    SP_TRY(alloc(&grad, n_params));
+    SP_TRY(alloc(&adam_m, n_params));
+    SP_TRY(alloc(&adam_v, n_params));
+    SP_CUDA(cudaMemsetAsync(grad, 0, n_params * 4, comp));
+    SP_CUDA(cudaMemsetAsync(adam_m, 0, n_params * 4, comp));
+    SP_CUDA(cudaMemsetAsync(adam_v, 0, n_params * 4, comp));
+    return SP_OK;
+  }
+
+  int init_weights(uint64_t seed) {
+    const float std_w = 0.02f;
+    uint64_t tag = seed * 1000003ull + uint64_t(stage) * 7919ull;
+    auto normal = [&](int64_t off, int64_t n) {
+      return init_params(master + off, w + off, n, ++tag, std_w, 0.f, 0, comp);
+    };
+    auto ones = [&](int64_t off, int64_t n) { return init_params(master + off, w + off, n, ++tag, 0.f, 1.f, 1, comp); };
+    for (int l = 0; l < Lps; ++l) {
+      SP_TRY(ones(lp[l].attn_norm, h));
+      SP_TRY(normal(lp[l].wqkv, qkv_w * h));
+      SP_TRY(normal(lp[l].wo, h * qd));
+      SP_TRY(ones(lp[l].mlp_norm, h));
+      SP_TRY(normal(lp[l].wgu, 2 * H * h));
+      SP_TRY(normal(lp[l].wd, h * H));
+    }
+    if (emb >= 0) SP_TRY(normal(emb, int64_t(cfg.vocab) * h));
+    if (final_norm >= 0) SP_TRY(ones(final_norm, h));
+    if (head >= 0) SP_TRY(normal(head, int64_t(cfg.vocab) * h));
+    return SP_OK;
+  }
+
+  int alloc_arena() {
+    const int64_t rows = int64_t(slots) * Ls;
+    SP_TRY(alloc(&x_pool, rows * h));
+    k_pool.assign(Lps, nullptr);
+    v_pool.assign(Lps, nullptr);
+    dk_acc.assign(Lps, nullptr);
+    dv_acc.assign(Lps, nullptr);
+    const int64_t acc_rows = int64_t(cfg.slices) * Ls;
+    for (int l = 0; l < Lps; ++l) {
+      SP_TRY(alloc(&k_pool[l], rows * kvd));
+      SP_TRY(alloc(&v_pool[l], rows * kvd));
+      SP_TRY(alloc(&dk_acc[l], acc_rows * kvd));
+      SP_TRY(alloc(&dv_acc[l], acc_rows * kvd));
+      SP_CUDA(cudaMemsetAsync(dk_acc[l], 0, acc_rows * kvd * 4, comp));
+      SP_CUDA(cudaMemsetAsync(dv_acc[l], 0, acc_rows * kvd * 4, comp));
+    }
+    free_slots.clear();
+    for (int s = slots - 1; s >= 0; --s) free_slots.push_back(s);  // pop_back -> lowest first
+    return SP_OK;
+  }
+
+  int alloc_workspace() {
+    ws.resize(Lps);
+    for (int l = 0; l < Lps; ++l) {
+      LayerWs& x = ws[l];
+      SP_TRY(alloc(&x.x_in, Ls * h));
+      SP_TRY(alloc(&x.xn, Ls * h));
+      SP_TRY(alloc(&x.q, Ls * qd));
+      SP_TRY(alloc(&x.o, Ls * qd));
+      SP_TRY(alloc(&x.x_mid, Ls * h));
+      SP_TRY(alloc(&x.xn2, Ls * h));
+      SP_TRY(alloc(&x.gu, Ls * 2 * H));
+      SP_TRY(alloc(&x.act, Ls * H));
+      SP_TRY(alloc(&x.lse, int64_t(cfg.heads) * Ls));
+      SP_TRY(alloc(&x.rstd1, Ls));
+      SP_TRY(alloc(&x.rstd2, Ls));
+    }
+    SP_TRY(alloc(&x_final, Ls * h));
+    SP_TRY(alloc(&qkv, Ls * qkv_w));
+    SP_TRY(alloc(&dqkv, Ls * qkv_w));
+    SP_TRY(alloc(&tmp_h, Ls * std::max(h, qd)));
+    SP_TRY(alloc(&tmp_H, Ls * H));
+    SP_TRY(alloc(&tmp_2H, Ls * 2 * H));
+    for (int x = 0; x < 2; ++x) {
+      SP_TRY(alloc(&out_buf[x], Ls * h));
+      SP_TRY(alloc(&gin_buf[x], Ls * h));
+      SP_TRY(alloc(&gout_buf[x], Ls * h));
+    }
+    SP_TRY(alloc(&dq_acc, Ls * qd));
+    SP_TRY(alloc(&delta_ws, 2 * int64_t(cfg.heads) * Ls));
+    SP_TRY(alloc(&loss_dev, 1));
+    SP_TRY(alloc(&tokens, int64_t(cfg.microbatches) * cfg.seq_len));
+    SP_TRY(alloc(&targets, int64_t(cfg.microbatches) * cfg.seq_len));
+    if (stage == p) {
+      SP_TRY(alloc(&xf, Ls * h));
+      SP_TRY(alloc(&rstd_f, Ls));
+      SP_TRY(alloc(&logits, Ls * int64_t(cfg.vocab)));
+      SP_TRY(alloc(&dlogits, Ls * int64_t(cfg.vocab)));
+    }
+    return SP_OK;
+  }
+
+  // -------------------------------------------------------------- passes
+  std::vector<int32_t> chunk_rows(int k, int i) const {
+    std::vector<int32_t> rows;
+    for (int j = 1; j <= i; ++j) rows.push_back(int32_t(slot_of.at({k, j}) * Ls));
+    return rows;
+  }
+
+  int attn_fwd_timed(int l, const std::vector<int32_t>& rows, LayerWs& x) {
+    AttnTimer t{};
+    SP_CUDA(cudaEventCreate(&t.a));
+    SP_CUDA(cudaEventCreate(&t.b));
+    const int i = int(rows.size());
+    t.flops = 4.0 * cfg.head_dim * double(Ls) * (double(i - 1) * Ls + (Ls + 1) / 2.0) * cfg.heads;
+    t.kind = 0;
+    SP_CUDA(cudaEventRecord(t.a, comp));
+    SP_TRY(sp_attn_fwd(x.q, Ls, qd, k_pool[l], v_pool[l], int64_t(slots) * Ls, kvd, rows.data(), i, int(Ls),
+                       cfg.heads, cfg.kv_heads, cfg.head_dim, 1, x.o, qd, x.lse, comp));
+    SP_CUDA(cudaEventRecord(t.b, comp));
+    attn_times.push_back(t);
+    return SP_OK;
+  }
+
+  // One layer forward; saves its internals in ws[l]; writes its output to x_out.
+  int layer_forward(int l, int k, int i, const std::vector<int32_t>& rows, bf16raw* x_out) {
+    LayerWs& x = ws[l];
+    const LayerParams& P = lp[l];
+    const int slot = slot_of.at({k, i});
+    const int64_t pos0 = int64_t(i - 1) * Ls;
+    SP_TRY(rmsnorm_fwd(x.x_in, W(P.attn_norm), x.xn, x.rstd1, Ls, int(h), cfg.norm_eps, comp));
+    SP_TRY(gemm(false, true, Ls, qkv_w, h, x.xn, h, W(P.wqkv), h, qkv, qkv_w, false, 1.f, 0.f, comp));
+    SP_TRY(rope_qkv_fwd(qkv, Ls, cfg.heads, cfg.kv_heads, cfg.head_dim, pos0, cfg.rope_theta, x.q, qd,
+                        k_pool[l] + int64_t(slot) * Ls * kvd, v_pool[l] + int64_t(slot) * Ls * kvd, kvd, comp));
+    SP_TRY(attn_fwd_timed(l, rows, x));
+    SP_CUDA(cudaMemcpyAsync(x.x_mid, x.x_in, Ls * h * 2, cudaMemcpyDeviceToDevice, comp));
+    SP_TRY(gemm(false, true, Ls, h, qd, x.o, qd, W(P.wo), qd, x.x_mid, h, false, 1.f, 1.f, comp));
+    SP_TRY(rmsnorm_fwd(x.x_mid, W(P.mlp_norm), x.xn2, x.rstd2, Ls, int(h), cfg.norm_eps, comp));
+    SP_TRY(gemm(false, true, Ls, 2 * H, h, x.xn2, h, W(P.wgu), h, x.gu, 2 * H, false, 1.f, 0.f, comp));
+    SP_TRY(swiglu_fwd(x.gu, x.act, Ls, int(H), comp));
+    SP_CUDA(cudaMemcpyAsync(x_out, x.x_mid, Ls * h * 2, cudaMemcpyDeviceToDevice, comp));
+    SP_TRY(gemm(false, true, Ls, h, H, x.act, H, W(P.wd), H, x_out, h, false, 1.f, 1.f, comp));
+    return SP_OK;
+  }
+
+  // Stage forward of slice (k,i) from ws[0].x_in; final output to `out`.
+  int stage_forward(int k, int i, bf16raw* out) {
+    const std::vector<int32_t> rows = chunk_rows(k, i);
+    for (int l = 0; l < Lps; ++l) SP_TRY(layer_forward(l, k, i, rows, l + 1 < Lps ? ws[l + 1].x_in : out));
+    return SP_OK;
+  }
+
+  int run_forward(int k, int i) {
+    if (free_slots.empty()) return set_error(SP_ERR_RUNTIME, "arena exhausted (ledger/schedule mismatch)");
+    const int slot = free_slots.back();
+    free_slots.pop_back();
+    slot_of[{k, i}] = slot;
+    slots_high_water = std::max(slots_high_water, ++slots_in_use);
+    bf16raw* xs = x_pool + int64_t(slot) * Ls * h;
+    const int64_t tok0 = int64_t(k - 1) * cfg.seq_len + int64_t(i - 1) * Ls;
+    if (stage == 1) {
+      SP_TRY(embed_fwd(tokens + tok0, W(emb), xs, Ls, int(h), comp));
+    } else {
+      cudaEvent_t ready, got;
+      SP_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+      SP_CUDA(cudaEventCreateWithFlags(&got, cudaEventDisableTiming));
+      SP_CUDA(cudaEventRecord(ready, comp));  // slot free in compute order
+      SP_CUDA(cudaStreamWaitEvent(cfwd, ready, 0));
+      SP_NCCL(ncclRecv(xs, Ls * h, ncclBfloat16, rank - 1, nc_fwd, cfwd));
+      SP_CUDA(cudaEventRecord(got, cfwd));
+      SP_CUDA(cudaStreamWaitEvent(comp, got, 0));
+      cudaEventDestroy(ready);
+      cudaEventDestroy(got);
+    }
+    SP_CUDA(cudaMemcpyAsync(ws[0].x_in, xs, Ls * h * 2, cudaMemcpyDeviceToDevice, comp));
+    if (stage < p) {
+      const int b = out_idx;
+      out_idx ^= 1;
+      SP_CUDA(cudaStreamWaitEvent(comp, ev_out_free[b], 0));
+      SP_TRY(stage_forward(k, i, out_buf[b]));
+      cudaEvent_t done;
+      SP_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+      SP_CUDA(cudaEventRecord(done, comp));
+      SP_CUDA(cudaStreamWaitEvent(cfwd, done, 0));
+      SP_NCCL(ncclSend(out_buf[b], Ls * h, ncclBfloat16, rank + 1, nc_fwd, cfwd));
+      SP_CUDA(cudaEventRecord(ev_out_free[b], cfwd));
+      cudaEventDestroy(done);
+    } else {
+      SP_TRY(stage_forward(k, i, x_final));
+    }
+    return SP_OK;
+  }
+
+  int layer_backward(int l, int k, int i, const std::vector<int32_t>& rows, bf16raw* dx) {
+    LayerWs& x = ws[l];
+    const LayerParams& P = lp[l];
+    const int64_t pos0 = int64_t(i - 1) * Ls;
+    // MLP
+    SP_TRY(gemm(false, false, Ls, H, h, dx, h, W(P.wd), H, tmp_H, H, false, 1.f, 0.f, comp));      // d_act
+    SP_TRY(gemm(true, false, h, H, Ls, dx, h, x.act, H, G(P.wd), H, true, 1.f, 1.f, comp));         // dWd
+    SP_TRY(swiglu_bwd(tmp_H, x.gu, tmp_2H, Ls, int(H), comp));                                      // d_gu
+    SP_TRY(gemm(false, false, Ls, h, 2 * H, tmp_2H, 2 * H, W(P.wgu), h, tmp_h, h, false, 1.f, 0.f, comp));  // dxn2
+    SP_TRY(gemm(true, false, 2 * H, h, Ls, tmp_2H, 2 * H, x.xn2, h, G(P.wgu), h, true, 1.f, 1.f, comp));    // dWgu
+    SP_TRY(rmsnorm_bwd(tmp_h, x.x_mid, W(P.mlp_norm), x.rstd2, dx, dx, G(P.mlp_norm), Ls, int(h), comp));
+    // attention output projection
+    SP_TRY(gemm(false, false, Ls, qd, h, dx, h, W(P.wo), qd, tmp_h, qd, false, 1.f, 0.f, comp));   // d_o
+    SP_TRY(gemm(true, false, h, qd, Ls, dx, h, x.o, qd, G(P.wo), qd, true, 1.f, 1.f, comp));         // dWo
+    // K2: sliced attention backward
+    SP_CUDA(cudaMemsetAsync(dq_acc, 0, Ls * qd * 4, comp));
+    std::vector<int32_t> acc_rows;
+    for (int j = 1; j <= i; ++j) acc_rows.push_back(int32_t((j - 1) * Ls));
+    AttnTimer t{};
+    SP_CUDA(cudaEventCreate(&t.a));
+    SP_CUDA(cudaEventCreate(&t.b));
+    t.flops = 2.5 * 4.0 * cfg.head_dim * double(Ls) * (double(i - 1) * Ls + (Ls + 1) / 2.0) * cfg.heads;
+    t.kind = 1;
+    SP_CUDA(cudaEventRecord(t.a, comp));
+    SP_TRY(sp_attn_bwd(x.q, Ls, qd, k_pool[l], v_pool[l], int64_t(slots) * Ls, kvd, rows.data(), i, int(Ls), cfg.heads,
+                       cfg.kv_heads, cfg.head_dim, 1, x.o, qd, tmp_h, qd, x.lse, delta_ws, dq_acc, dk_acc[l],
+                       dv_acc[l], int64_t(cfg.slices) * Ls, acc_rows.data(), comp));
+    SP_CUDA(cudaEventRecord(t.b, comp));
+    attn_times.push_back(t);
+    // chunk i's dK/dV is complete: RoPE backward into d_qkv and reset the rows
+    SP_TRY(rope_qkv_bwd(dq_acc, dk_acc[l] + pos0 * kvd, dv_acc[l] + pos0 * kvd, kvd, Ls, cfg.heads, cfg.kv_heads,
+                        cfg.head_dim, pos0, cfg.rope_theta, dqkv, 1, comp));
+    SP_TRY(gemm(false, false, Ls, h, qkv_w, dqkv, qkv_w, W(P.wqkv), h, tmp_h, h, false, 1.f, 0.f, comp));   // dxn
+    SP_TRY(gemm(true, false, qkv_w, h, Ls, dqkv, qkv_w, x.xn, h, G(P.wqkv), h, true, 1.f, 1.f, comp));      // dWqkv
+    SP_TRY(rmsnorm_bwd(tmp_h, x.x_in, W(P.attn_norm), x.rstd1, dx, dx, G(P.attn_norm), Ls, int(h), comp));
+    return SP_OK;
+  }
+
+  int run_backward(int k, int i) {
+    const int slot = slot_of.at({k, i});
+    bf16raw* xs = x_pool + int64_t(slot) * Ls * h;
+    const int64_t tok0 = int64_t(k - 1) * cfg.seq_len + int64_t(i - 1) * Ls;
+    // gradient input
+    bf16raw* dx = nullptr;
+    int gb = -1;
+    if (stage < p) {
+      gb = gin_idx;
+      gin_idx ^= 1;
+      dx = gin_buf[gb];
+      SP_CUDA(cudaStreamWaitEvent(cbwd, ev_gin_free[gb], 0));
+      SP_NCCL(ncclRecv(dx, Ls * h, ncclBfloat16, rank + 1, nc_bwd, cbwd));
+      cudaEvent_t got;
+      SP_CUDA(cudaEventCreateWithFlags(&got, cudaEventDisableTiming));
+      SP_CUDA(cudaEventRecord(got, cbwd));
+      SP_CUDA(cudaStreamWaitEvent(comp, got, 0));
+      cudaEventDestroy(got);
+    } else {
+      dx = gout_buf[gout_idx];  // last stage: dX is produced here, sent from here
+    }
+    // recompute (Full checkpointing)
+    SP_CUDA(cudaMemcpyAsync(ws[0].x_in, xs, Ls * h * 2, cudaMemcpyDeviceToDevice, comp));
+    bf16raw* top = stage < p ? tmp_h : x_final;
+    if (stage == p) {
+      SP_CUDA(cudaStreamWaitEvent(comp, ev_gout_free[gout_idx], 0));
+      SP_TRY(stage_forward(k, i, x_final));
+      // LM head + cross entropy
+      const int64_t V = cfg.vocab;
+      SP_TRY(rmsnorm_fwd(x_final, W(final_norm), xf, rstd_f, Ls, int(h), cfg.norm_eps, comp));
+      SP_TRY(gemm(false, true, Ls, V, h, xf, h, W(head), h, logits, V, true, 1.f, 0.f, comp));
+      const float scale = 1.f / float(int64_t(cfg.microbatches) * cfg.seq_len);
+      SP_TRY(cross_entropy(logits, targets + tok0, Ls, int(V), scale, dlogits, loss_dev, comp));
+      SP_TRY(gemm(false, false, Ls, h, V, dlogits, V, W(head), h, tmp_h, h, false, 1.f, 0.f, comp));  // dxf
+      SP_TRY(gemm(true, false, V, h, Ls, dlogits, V, xf, h, G(head), h, true, 1.f, 1.f, comp));        // dWhead
+      SP_TRY(rmsnorm_bwd(tmp_h, x_final, W(final_norm), rstd_f, nullptr, dx, G(final_norm), Ls, int(h), comp));
+    } else {
+      SP_TRY(stage_forward(k, i, top));
+    }
+    const std::vector<int32_t> rows = chunk_rows(k, i);
+    for (int l = Lps - 1; l >= 0; --l) SP_TRY(layer_backward(l, k, i, rows, dx));
+    if (stage == 1) {
+      SP_TRY(embed_bwd(tokens + tok0, dx, G(emb), Ls, int(h), comp));
+      if (gb >= 0) SP_CUDA(cudaEventRecord(ev_gin_free[gb], comp));
+    } else {
+      cudaEvent_t done;
+      SP_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+      SP_CUDA(cudaEventRecord(done, comp));
+      SP_CUDA(cudaStreamWaitEvent(cbwd, done, 0));
+      cudaEventDestroy(done);
+      SP_NCCL(ncclSend(dx, Ls * h, ncclBfloat16, rank - 1, nc_bwd, cbwd));
+      if (gb >= 0) {  // middle stage: dx lives in the receive buffer
+        SP_CUDA(cudaEventRecord(ev_gin_free[gb], cbwd));
+      } else {        // last stage: dx lives in gout_buf[gout_idx]
+        SP_CUDA(cudaEventRecord(ev_gout_free[gout_idx], cbwd));
+        gout_idx ^= 1;
+      }
+    }
+    free_slots.push_back(slot);  // LIFO reuse
+    slot_of.erase({k, i});
+    --slots_in_use;
+    return SP_OK;
+  }
+
+  int step(const int32_t* tok, const int32_t* tgt, int on_device, int flags, float* loss_out) {
+    for (auto& t : times) {
+      cudaEventDestroy(t.start);
+      cudaEventDestroy(t.end);
+    }
+    times.clear();
+    for (auto& t : attn_times) {
+      cudaEventDestroy(t.a);
+      cudaEventDestroy(t.b);
+    }
+    attn_times.clear();
+    slots_high_water = 0;
+    const int64_t ntok = int64_t(cfg.microbatches) * cfg.seq_len;
+    SP_CUDA(cudaEventRecord(step_start, comp));
+    const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    if (stage == 1 && tok) SP_CUDA(cudaMemcpyAsync(tokens, tok, ntok * 4, kind, comp));
+    if (stage == p && tgt) SP_CUDA(cudaMemcpyAsync(targets, tgt, ntok * 4, kind, comp));
+    SP_CUDA(cudaMemsetAsync(loss_dev, 0, 4, comp));
+    for (pipelab::PassId id : order) {
+      const pipelab::Pass& ps = sched.passes[id];
+      PassTime t{id, nullptr, nullptr};
+      SP_CUDA(cudaEventCreate(&t.start));
+      SP_CUDA(cudaEventCreate(&t.end));
+      SP_CUDA(cudaEventRecord(t.start, comp));
+      if (ps.kind == pipelab::PassKind::Forward) SP_TRY(run_forward(ps.microbatch, ps.slice));
+      else SP_TRY(run_backward(ps.microbatch, ps.slice));
+      SP_CUDA(cudaEventRecord(t.end, comp));
+      times.push_back(t);
+    }
+    if (!(flags & SP_STEP_NO_OPTIMIZER)) {
+      ++opt_step;
+      SP_TRY(adamw(master, w, grad, adam_m, adam_v, n_params, cfg.lr, 0.9f, 0.95f, 1e-8f, 0.1f, opt_step, comp));
+      SP_CUDA(cudaMemsetAsync(grad, 0, n_params * 4, comp));
+    }
+    // drain comm streams into the compute stream so step_end covers them
+    cudaEvent_t e1, e2;
+    SP_CUDA(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
+    SP_CUDA(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming));
+    SP_CUDA(cudaEventRecord(e1, cfwd));
+    SP_CUDA(cudaEventRecord(e2, cbwd));
+    SP_CUDA(cudaStreamWaitEvent(comp, e1, 0));
+    SP_CUDA(cudaStreamWaitEvent(comp, e2, 0));
+    cudaEventDestroy(e1);
+    cudaEventDestroy(e2);
+    SP_CUDA(cudaEventRecord(step_end, comp));
+    if (loss_out) {
+      float l = 0.f;
+      SP_CUDA(cudaMemcpyAsync(&l, loss_dev, 4, cudaMemcpyDeviceToHost, comp));
+      SP_CUDA(cudaStreamSynchronize(comp));
+      *loss_out = stage == p ? l / float(ntok) : 0.f;
+    }
+    return SP_OK;
+  }
+};
+
+}  // namespace
+}  // namespace sp
+
+using sp::Runtime;
+
+extern "C" {
+
+int sp_nccl_unique_id(void* out128) {
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return sp::set_error(SP_ERR_NCCL, "ncclGetUniqueId: %s", ncclGetErrorString(r));
+  std::memcpy(out128, &id, sizeof id);
+  return SP_OK;
+}
+
+int sp_runtime_create(const sp_model_config* cfg, const void* nccl_id_fwd, const void* nccl_id_bwd, void** handle) {
+  auto rt = std::make_unique<Runtime>();
+  const int rc = rt->init(*cfg, nccl_id_fwd, nccl_id_bwd);
+  if (rc != SP_OK) return rc;
+  *handle = rt.release();
+  return SP_OK;
+}
+
+int sp_runtime_destroy(void* handle) {
+  delete static_cast<Runtime*>(handle);
+  return SP_OK;
+}
+
+int sp_runtime_step(void* handle, const int32_t* tokens, const int32_t* targets, int on_device, int flags,
+                    float* loss) {
+  return static_cast<Runtime*>(handle)->step(tokens, targets, on_device, flags, loss);
+}
+
+int sp_runtime_sync(void* handle) {
+  return sp::cuda_status(cudaStreamSynchronize(static_cast<Runtime*>(handle)->comp), "sync");
+}
+
+void* sp_runtime_stream(void* handle) { return static_cast<Runtime*>(handle)->comp; }
+
+// Step time (ms between step_start and step_end) and per-pass busy times.
+// out: [0] step ms, then per pass of device_order: pass id, start ms, end ms.
+int sp_runtime_timeline(void* handle, double* out, int cap) {
+  Runtime* rt = static_cast<Runtime*>(handle);
+  cudaError_t e = cudaEventSynchronize(rt->step_end);
+  if (e != cudaSuccess) return sp::cuda_status(e, "timeline");
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, rt->step_start, rt->step_end);
+  int n = 0;
+  if (cap > 0) out[n++] = ms;
+  for (const auto& t : rt->times) {
+    if (n + 3 > cap) break;
+    float a = 0.f, b = 0.f;
+    cudaEventElapsedTime(&a, rt->step_start, t.start);
+    cudaEventElapsedTime(&b, rt->step_start, t.end);
+    out[n++] = t.pass;
+    out[n++] = a;
+    out[n++] = b;
+  }
+  return n;
+}
+
+// Attention kernel timing of the last step: out = {fwd_ms, fwd_flops, fwd_launches,
+// bwd_ms, bwd_flops, bwd_launches}.
+int sp_runtime_attn_stats(void* handle, double* out6) {
+  Runtime* rt = static_cast<Runtime*>(handle);
+  for (int x = 0; x < 6; ++x) out6[x] = 0.0;
+  for (const auto& t : rt->attn_times) {
+    float ms = 0.f;
+    cudaEventSynchronize(t.b);
+    cudaEventElapsedTime(&ms, t.a, t.b);
+    out6[3 * t.kind] += ms;
+    out6[3 * t.kind + 1] += t.flops;
+    out6[3 * t.kind + 2] += 1;
+  }
+  return SP_OK;
+}
+
+// {slots, slots_high_water, slot_bytes, ledger_peak_units, bytes_allocated, n_params, layers_per_stage}
+int sp_runtime_memory(void* handle, int64_t* out7) {
+  Runtime* rt = static_cast<Runtime*>(handle);
+  out7[0] = rt->slots;
+  out7[1] = rt->slots_high_water;
+  out7[2] = rt->Ls * rt->h * 2 + int64_t(rt->Lps) * 2 * rt->Ls * rt->kvd * 2;
+  out7[3] = rt->ledger.per_device[rt->rank].peak_activation_units;
+  out7[4] = int64_t(rt->bytes_allocated);
+  out7[5] = rt->n_params;
+  out7[6] = rt->Lps;
+  return SP_OK;
+}
+
+// Copy parameter tensors / gradients between host fp32 buffers and the device.
+// which: 0 attn_norm 1 wqkv 2 wo 3 mlp_norm 4 wgu 5 wd 6 embedding 7 final_norm 8 head
+// dir: 0 device->host (master weights), 1 host->device (sets master + bf16), 2 grads device->host
+int sp_runtime_param(void* handle, int layer, int which, float* host, int64_t count, int dir) {
+  Runtime* rt = static_cast<Runtime*>(handle);
+  int64_t off = -1, n = 0;
+  const int64_t h = rt->h, H = rt->H;
+  if (which <= 5) {
+    if (layer < 0 || layer >= rt->Lps) return sp::set_error(SP_ERR_INVALID, "layer %d not on this stage", layer);
+    const sp::LayerParams& P = rt->lp[layer];
+    const int64_t offs[6] = {P.attn_norm, P.wqkv, P.wo, P.mlp_norm, P.wgu, P.wd};
+    const int64_t ns[6] = {h, rt->qkv_w * h, h * rt->qd, h, 2 * H * h, h * H};
+    off = offs[which];
+    n = ns[which];
+  } else if (which == 6) {
+    off = rt->emb, n = int64_t(rt->cfg.vocab) * h;
+  } else if (which == 7) {
+    off = rt->final_norm, n = h;
+  } else if (which == 8) {
+    off = rt->head, n = int64_t(rt->cfg.vocab) * h;
+  }
+  if (off < 0) return sp::set_error(SP_ERR_INVALID, "parameter %d not on this stage", which);
+  if (count != n) return sp::set_error(SP_ERR_INVALID, "parameter size %lld != %lld", (long long)count, (long long)n);
+  cudaError_t e;
+  if (dir == 0) e = cudaMemcpy(host, rt->master + off, n * 4, cudaMemcpyDeviceToHost);
+  else if (dir == 2) e = cudaMemcpy(host, rt->grad + off, n * 4, cudaMemcpyDeviceToHost);
+  else {
+    e = cudaMemcpy(rt->master + off, host, n * 4, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+      int rc = sp::f32_to_bf16(rt->master + off, rt->w + off, n, rt->comp);
+      if (rc) return rc;
+      e = cudaStreamSynchronize(rt->comp);
+    }
+  }
+  return sp::cuda_status(e, "sp_runtime_param");
+}
+
+}  // extern "C"

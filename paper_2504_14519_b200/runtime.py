@@ -1,0 +1,237 @@
+"""Python host mirror of the step executor (csrc/host/runtime.cpp) — the
+call a user makes to run SlimPipe sliced-1F1B training steps on B200s.
+
+    cfg = StepConfig.c2(layers=8)             # Llama-7B layer shapes, 128K ctx
+    step = SlimPipeStep(cfg)                  # rank/world from torchrun env
+    loss = step.step(tokens, targets)         # one optimizer step
+
+Process model: one process per GPU (torchrun); rank r runs stage r+1; the
+NCCL communicators of the executor are bootstrapped through
+torch.distributed (plumbing only).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, replace
+
+import numpy as np
+
+from . import native as N
+
+
+class _Cfg(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("layers", "hidden", "ffn_hidden", "heads", "kv_heads", "head_dim", "vocab",
+                                         "microbatches", "slices", "pp", "rank", "exchange_mode")] + [
+        ("seq_len", C.c_int64), ("rope_theta", C.c_float), ("norm_eps", C.c_float), ("lr", C.c_float),
+        ("seed", C.c_uint64)]
+
+
+@dataclass(frozen=True)
+class StepConfig:
+    layers: int
+    hidden: int
+    ffn_hidden: int
+    heads: int
+    kv_heads: int
+    vocab: int
+    seq_len: int
+    slices: int
+    microbatches: int
+    pp: int = 1
+    exchange: str = "off"
+    rope_theta: float = 10000.0
+    norm_eps: float = 1e-5
+    lr: float = 1e-4
+    seed: int = 1234
+
+    @property
+    def head_dim(self) -> int:
+        return self.hidden // self.heads
+
+    @property
+    def slice_len(self) -> int:
+        return self.seq_len // self.slices
+
+    # BASELINE.json configs
+    @staticmethod
+    def c1(**kw) -> "StepConfig":
+        """tiny Llama-style: 4 layers, h256, 4 heads (d64), 4K seq, 4 slices, m2."""
+        return replace(StepConfig(4, 256, 1024, 4, 4, 1000, 4096, 4, 2), **kw)
+
+    @staticmethod
+    def c2(**kw) -> "StepConfig":
+        """Llama-7B layer shapes, 128K context, 8 slices, m4 (depth reduced)."""
+        return replace(StepConfig(8, 4096, 11008, 32, 32, 32000, 131072, 8, 4), **kw)
+
+    @staticmethod
+    def c3(**kw) -> "StepConfig":
+        """Llama-13B layer shapes, 256K context, 16 slices, m4."""
+        return replace(StepConfig(40, 5120, 13824, 40, 40, 128000, 262144, 16, 4), **kw)
+
+    @staticmethod
+    def c4(**kw) -> "StepConfig":
+        """Llama-70B layer shapes (GQA 64/8), 1M context, 32 slices, m1 (depth reduced)."""
+        return replace(StepConfig(16, 8192, 28672, 64, 8, 128000, 1 << 20, 32, 1), **kw)
+
+    def to_c(self, rank: int) -> _Cfg:
+        return _Cfg(self.layers, self.hidden, self.ffn_hidden, self.heads, self.kv_heads, self.head_dim, self.vocab,
+                    self.microbatches, self.slices, self.pp, rank, N.MODES[self.exchange], self.seq_len,
+                    self.rope_theta, self.norm_eps, self.lr, self.seed)
+
+    # ---- accounting ----
+    def linear_params_per_layer(self) -> int:
+        h, H, kvd = self.hidden, self.ffn_hidden, self.kv_heads * self.head_dim
+        return 2 * h * h + 2 * h * kvd + 3 * h * H
+
+    def model_flops_per_step(self) -> float:
+        """F_model = 3 (2 N_lin + 2 h V) m S + 3 m L 2 h S (S+1)  (fwd+bwd, causal
+        attention counted once per pair, no recompute)."""
+        m, S, L, h = self.microbatches, self.seq_len, self.layers, self.hidden
+        n_lin = L * self.linear_params_per_layer()
+        return 3.0 * (2 * n_lin + 2 * h * self.vocab) * m * S + 3.0 * m * L * 2 * h * S * (S + 1)
+
+
+_PARAM_NAMES = ["attn_norm", "wqkv", "wo", "mlp_norm", "wgu", "wd", "embedding", "final_norm", "head"]
+
+
+def _lib():
+    lib = N.lib()
+    lib.sp_nccl_unique_id.argtypes = [C.c_void_p]
+    lib.sp_runtime_create.argtypes = [C.POINTER(_Cfg), C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]
+    lib.sp_runtime_destroy.argtypes = [C.c_void_p]
+    lib.sp_runtime_step.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_float)]
+    lib.sp_runtime_sync.argtypes = [C.c_void_p]
+    lib.sp_runtime_stream.argtypes = [C.c_void_p]
+    lib.sp_runtime_stream.restype = C.c_void_p
+    lib.sp_runtime_timeline.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.c_int]
+    lib.sp_runtime_attn_stats.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
+    lib.sp_runtime_memory.argtypes = [C.c_void_p, C.POINTER(C.c_int64)]
+    lib.sp_runtime_param.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int64, C.c_int]
+    return lib
+
+
+def nccl_ids(rank: int, world: int):
+    """Two NCCL unique ids (fwd / bwd communicators) made on rank 0 and
+    broadcast with torch.distributed (which must be initialised when world > 1)."""
+    if world == 1:
+        return None, None
+    import torch.distributed as dist
+    ids = [None, None]
+    if rank == 0:
+        a, b = C.create_string_buffer(128), C.create_string_buffer(128)
+        N.check(_lib().sp_nccl_unique_id(a), "sp_nccl_unique_id")
+        N.check(_lib().sp_nccl_unique_id(b), "sp_nccl_unique_id")
+        ids = [a.raw, b.raw]
+    dist.broadcast_object_list(ids, src=0)
+    return C.create_string_buffer(ids[0], 128), C.create_string_buffer(ids[1], 128)
+
+
+class SlimPipeStep:
+    """One pipeline stage of the sliced-1F1B step on this process's GPU."""
+
+    def __init__(self, cfg: StepConfig, rank: int | None = None, world: int | None = None):
+        self.cfg = cfg
+        self.rank = int(os.environ.get("RANK", 0)) if rank is None else rank
+        self.world = int(os.environ.get("WORLD_SIZE", 1)) if world is None else world
+        if cfg.pp != self.world:
+            raise ValueError(f"pp ({cfg.pp}) must equal the number of ranks ({self.world})")
+        lib = _lib()
+        ida, idb = nccl_ids(self.rank, self.world)
+        h = C.c_void_p()
+        c = cfg.to_c(self.rank)
+        N.check(lib.sp_runtime_create(C.byref(c), ida, idb, C.byref(h)), "sp_runtime_create")
+        self._h = h
+        self.stage = self.rank + 1
+        self.is_first = self.stage == 1
+        self.is_last = self.stage == cfg.pp
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib().sp_runtime_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def stream_handle(self) -> int:
+        return _lib().sp_runtime_stream(self._h)
+
+    def step(self, tokens, targets, optimizer: bool = True, on_device: bool = False) -> float:
+        """Run all passes of this stage's program for m microbatches.
+
+        tokens/targets: int32 [microbatches, seq_len] — numpy (host) arrays, or
+        device pointers (ints) when on_device.  Returns the mean loss on the
+        last stage (0.0 elsewhere).
+        """
+        loss = C.c_float(0.0)
+        if on_device:
+            tp, gp = C.c_void_p(tokens), C.c_void_p(targets)
+        else:
+            tokens = np.ascontiguousarray(tokens, dtype=np.int32)
+            targets = np.ascontiguousarray(targets, dtype=np.int32)
+            tp, gp = tokens.ctypes.data_as(C.c_void_p), targets.ctypes.data_as(C.c_void_p)
+        flags = 0 if optimizer else 1
+        N.check(_lib().sp_runtime_step(self._h, tp, gp, int(on_device), flags, C.byref(loss)), "sp_runtime_step")
+        return float(loss.value)
+
+    def step_async(self, tokens_dev: int, targets_dev: int, optimizer: bool = True) -> None:
+        """Enqueue one step with device-resident inputs; no host synchronisation."""
+        N.check(_lib().sp_runtime_step(self._h, C.c_void_p(tokens_dev), C.c_void_p(targets_dev), 1,
+                                       0 if optimizer else 1, None), "sp_runtime_step")
+
+    def sync(self):
+        N.check(_lib().sp_runtime_sync(self._h), "sp_runtime_sync")
+
+    def timeline(self):
+        n_pass = 2 * self.cfg.microbatches * self.cfg.slices
+        buf = (C.c_double * (1 + 3 * n_pass))()
+        n = _lib().sp_runtime_timeline(self._h, buf, len(buf))
+        if n < 0:
+            N.check(n, "sp_runtime_timeline")
+        vals = list(buf[:n])
+        return vals[0], [(int(vals[i]), vals[i + 1], vals[i + 2]) for i in range(1, n, 3)]
+
+    def attn_stats(self) -> dict:
+        b = (C.c_double * 6)()
+        N.check(_lib().sp_runtime_attn_stats(self._h, b), "sp_runtime_attn_stats")
+        return {"fwd_ms": b[0], "fwd_flops": b[1], "fwd_launches": int(b[2]), "bwd_ms": b[3], "bwd_flops": b[4],
+                "bwd_launches": int(b[5])}
+
+    def memory(self) -> dict:
+        b = (C.c_int64 * 7)()
+        N.check(_lib().sp_runtime_memory(self._h, b), "sp_runtime_memory")
+        keys = ["slots", "slots_high_water", "slot_bytes", "ledger_peak_units", "bytes_allocated", "n_params",
+                "layers_per_stage"]
+        return dict(zip(keys, list(b)))
+
+    # ---- parameter access (tests) ----
+    def _param_shape(self, which: str):
+        c = self.cfg
+        h, H, qkv = c.hidden, c.ffn_hidden, (c.heads + 2 * c.kv_heads) * c.head_dim
+        return {"attn_norm": (h,), "wqkv": (qkv, h), "wo": (h, c.heads * c.head_dim), "mlp_norm": (h,),
+                "wgu": (2 * H, h), "wd": (h, H), "embedding": (c.vocab, h), "final_norm": (h,),
+                "head": (c.vocab, h)}[which]
+
+    def _param_io(self, layer: int, which: str, arr: np.ndarray | None, direction: int) -> np.ndarray:
+        shape = self._param_shape(which)
+        if arr is None:
+            arr = np.zeros(shape, np.float32)
+        arr = np.ascontiguousarray(arr, dtype=np.float32)
+        assert arr.shape == shape
+        N.check(_lib().sp_runtime_param(self._h, layer, _PARAM_NAMES.index(which), arr.ctypes.data_as(C.c_void_p),
+                                        arr.size, direction), "sp_runtime_param")
+        return arr
+
+    def get_param(self, layer: int, which: str) -> np.ndarray:
+        return self._param_io(layer, which, None, 0)
+
+    def set_param(self, layer: int, which: str, value: np.ndarray) -> None:
+        self._param_io(layer, which, value, 1)
+
+    def get_grad(self, layer: int, which: str) -> np.ndarray:
+        return self._param_io(layer, which, None, 2)

@@ -35,3 +35,27 @@ for L, n in [(4096, 1), (4096, 4), (16384, 1), (16384, 4), (16384, 8), (8192, 16
         ms2 = bench(lambda: torch.nn.functional.scaled_dot_product_attention(qs, ks, vs, is_causal=True))
         line += f" | sdpa {ms2:.3f} ms {flops_fwd(L, 0, heads, d) / ms2 / 1e9:.0f} TFLOP/s"
     print(line, flush=True)
+
+print("--- backward ---")
+for L, n in [(4096, 1), (16384, 1), (16384, 4), (8192, 16)]:
+    P = (n - 1) * L
+    q = torch.randn(L, heads * d, device='cuda', dtype=torch.bfloat16)
+    kp = torch.randn(n * L, heads * d, device='cuda', dtype=torch.bfloat16)
+    vp = torch.randn(n * L, heads * d, device='cuda', dtype=torch.bfloat16)
+    do = torch.randn(L, heads * d, device='cuda', dtype=torch.bfloat16)
+    rows = [c * L for c in range(n)]
+    o, lse = ops.attn_fwd(q, kp, vp, rows, L, heads, heads, True)
+    dq = torch.zeros(L, heads * d, device='cuda'); dk = torch.zeros(n * L, heads * d, device='cuda'); dv = torch.zeros_like(dk)
+    ws = torch.empty(2 * heads * L, device='cuda')
+    ms = bench(lambda: ops.attn_bwd(q, kp, vp, rows, L, heads, heads, True, o, lse, do, dq, dk, dv, rows, ws))
+    tf = 2.5 * flops_fwd(L, P, heads, d) / ms / 1e9
+    line = f"L={L} n={n} bwd ours {ms:.3f} ms {tf:.0f} TFLOP/s (2.5x fwd flops)"
+    if n == 1:
+        qs = q.view(L, heads, d).transpose(0, 1)[None].detach().requires_grad_()
+        ks = kp.view(L, heads, d).transpose(0, 1)[None].detach().requires_grad_()
+        vs = vp.view(L, heads, d).transpose(0, 1)[None].detach().requires_grad_()
+        out = torch.nn.functional.scaled_dot_product_attention(qs, ks, vs, is_causal=True)
+        g = do.view(L, heads, d).transpose(0, 1)[None]
+        ms2 = bench(lambda: torch.autograd.grad(out, (qs, ks, vs), g, retain_graph=True))
+        line += f" | sdpa bwd {ms2:.3f} ms {2.5 * flops_fwd(L, 0, heads, d) / ms2 / 1e9:.0f} TFLOP/s"
+    print(line, flush=True)

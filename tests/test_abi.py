@@ -1,0 +1,34 @@
+"""The C-ABI library builds, loads without a GPU and exports every symbol that
+include/slimpipe.h declares (no compute calls here)."""
+import ctypes
+import re
+from pathlib import Path
+
+from paper_2504_14519_b200 import native
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def declared_symbols():
+    text = (ROOT / "include" / "slimpipe.h").read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(sp_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_every_declared_symbol_is_exported():
+    lib = native.lib()
+    syms = declared_symbols()
+    assert len(syms) >= 20
+    missing = [s for s in syms if not hasattr(lib, s)]
+    assert not missing, missing
+
+
+def test_status_strings_and_errors_without_gpu():
+    lib = native.lib()
+    assert lib.sp_status_string(0) == b"ok"
+    assert lib.sp_version() >= 1
+    # invalid shapes are rejected before touching the device
+    rows = (ctypes.c_int32 * 1)(0)
+    rc = lib.sp_attn_fwd(None, 100, 128, None, None, 128, 128, rows, 1, 128, 1, 1, 128, 1, None, 128, None, None)
+    assert rc == native.SP_ERR_UNSUPPORTED
+    assert b"multiples of 128" in lib.sp_last_error()
