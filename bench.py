@@ -1,0 +1,370 @@
+#!/usr/bin/env python
+"""SlimPipe sliced-1F1B training step on B200 — benchmark (one JSON line).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 ... bench.py --gpus N
+
+Workload (BASELINE.json configs[1]): Llama-7B layer shapes
+(h 4096, 32 heads x d128, FFN 11008, V 32000), depth reduced to --layers
+(default 8), 128K-token microbatches cut into 8 slices of 16K, m=4
+microbatches, pipeline PP = N GPUs (layers/N per stage), synthetic tokens,
+random-init weights, bf16 compute with fp32 accumulation/master weights,
+AdamW step included.  Total work per step is fixed as N grows ("strong").
+
+value      tokens/s of the whole job, inputs resident in HBM, K steps timed
+           with CUDA events on the executor's stream, max over ranks.
+e2e        same metric through the public API (SlimPipeStep.step) with the
+           tokens/targets copied from pinned host memory each step and the
+           loss read back each step.
+roofline   the dominant kernel (sliced attention backward, K2): algorithmic
+           FLOPs per launch / mean launch time (CUDA events on the launching
+           stream) vs the measured sustained bf16 peak.
+cpu_baseline  the reference's own chunk_attention (oracle/_ref, fp64, all host
+           threads) on a bounded sample of the same attention, extrapolated
+           to the step's model FLOPs.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d, "measured"
+    return dict(PEAKS_FALLBACK), "fallback"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--layers", type=int, default=8)
+    ap.add_argument("--seq-len", type=int, default=131072)
+    ap.add_argument("--slices", type=int, default=8)
+    ap.add_argument("--microbatches", type=int, default=4)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def make_cfg(args, world):
+    from paper_2504_14519_b200.runtime import StepConfig
+    return StepConfig.c2(layers=args.layers, seq_len=args.seq_len, slices=args.slices,
+                         microbatches=args.microbatches, pp=world)
+
+
+def workload_name(cfg):
+    return (f"c2 Llama-7B layer shapes x{cfg.layers} layers, {cfg.seq_len // 1024}K ctx, n={cfg.slices} slices, "
+            f"m={cfg.microbatches}, PP={cfg.pp}")
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self):
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        sm.sort()
+        med = sm[len(sm) // 2] if sm else None
+        return {"sm_mhz": med, "sm_max_mhz": mx or None, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------- CPU baseline
+def cpu_baseline(cfg, seconds: float):
+    """Reference chunk_attention (fp64, all host threads) on a bounded sample
+    of the step's attention, extrapolated to tokens/s of the full step."""
+    threads = os.cpu_count() or 1
+    ls, nch, d = 512, 4, 128
+    flops_head = 4.0 * d * ls * ((nch - 1) * ls + (ls + 1) / 2.0)
+    ref_so = ROOT / "oracle" / "_ref" / "libpipelab_ref.so"
+    if ref_so.exists():
+        lib = C.CDLL(str(ref_so))
+        lib.ref_time_chunk_attention.restype = C.c_double
+        lib.ref_time_chunk_attention.argtypes = [C.c_int] * 5 + [C.c_ulonglong]
+        run = lambda heads: lib.ref_time_chunk_attention(heads, ls, nch, d, threads, 20240817)
+        kind = "reference"
+    else:  # C restatement (port)
+        sys.path.insert(0, str(ROOT / "oracle"))
+        import numpy as np
+        import model_oracle as MO
+        rng = np.random.default_rng(20240817)
+
+        def run(heads):
+            q = rng.uniform(-1, 1, (ls, heads, d)).astype(np.float32)
+            k = rng.uniform(-1, 1, (nch * ls, heads, d)).astype(np.float32)
+            t0 = time.perf_counter()
+            MO.attn_fwd(q, k, k, ls)
+            return time.perf_counter() - t0
+        kind = "port"
+    t = run(threads)  # calibrate
+    heads = max(threads, int(threads * seconds / max(t, 1e-3)))
+    t = run(heads)
+    rate = heads * flops_head / t  # FLOP/s
+    tok_s = cfg.microbatches * cfg.seq_len * rate / cfg.model_flops_per_step()
+    sample = (f"{'reference' if kind == 'reference' else 'C-port'} chunk_attention fp64: {heads} heads x "
+              f"(Ls={ls} causal over {nch} chunks, d={d}) = {heads * flops_head / 1e9:.1f} GFLOP in {t:.1f} s "
+              f"({rate / 1e9:.2f} GFLOP/s on {threads} threads), extrapolated to the step's "
+              f"{cfg.model_flops_per_step() / 1e15:.1f} PFLOP of model FLOPs")
+    return {"value": tok_s, "unit": "tokens/s", "cores": threads, "kind": kind, "sample": sample,
+            "gflops": rate / 1e9, "seconds": t}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    cfg = make_cfg(args, world)
+    if rank != 0:
+        return 0
+    vals = []
+    for _ in range(args.warmup):
+        cpu_baseline(cfg, min(3.0, args.cpu_seconds))
+    base = None
+    for _ in range(args.steps):
+        base = cpu_baseline(cfg, args.cpu_seconds)
+        vals.append(base["value"])
+    value = sum(vals) / len(vals)
+    ms = cfg.microbatches * cfg.seq_len / value * 1e3
+    line = {"metric": "tokens/s", "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": workload_name(cfg), "global_batch": cfg.microbatches, "seq_len": cfg.seq_len,
+                       "parallelism": f"pp{cfg.pp}"},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": base["cores"], "kind": base["kind"],
+                             "sample": base["sample"]},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------- ours
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if world != args.gpus:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}; using {world}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2504_14519_b200 import native
+    from paper_2504_14519_b200 import plan as PL
+    from paper_2504_14519_b200.runtime import SlimPipeStep
+
+    cfg = make_cfg(args, world)
+    step = SlimPipeStep(cfg, rank, world)
+    lib = native.lib()
+    stream = torch.cuda.ExternalStream(step.stream_handle)
+
+    rng = np.random.default_rng(1234)
+    tok_host = torch.from_numpy(rng.integers(0, cfg.vocab, (cfg.microbatches, cfg.seq_len), dtype=np.int32))
+    tgt_host = torch.roll(tok_host, -1, dims=1)
+    tok_pin = tok_host.pin_memory()
+    tgt_pin = tgt_host.pin_memory()
+    tok_dev = tok_host.cuda()
+    tgt_dev = tgt_host.cuda()
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        step.step_async(tok_dev.data_ptr(), tgt_dev.data_ptr())
+    step.sync()
+    torch.cuda.synchronize()
+
+    # ---- timed region (value): device-resident inputs
+    clocks = ClockSampler()
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    launches0 = lib.sp_launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step.step_async(tok_dev.data_ptr(), tgt_dev.data_ptr())
+    ev1.record(stream)
+    step.sync()
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    launches = lib.sp_launch_count() - launches0
+    ms_total = max_over_ranks(ev0.elapsed_time(ev1))
+    ms_step = ms_total / args.steps
+    tokens_per_step = cfg.microbatches * cfg.seq_len
+    value = tokens_per_step * args.steps / (ms_total / 1e3)
+
+    # last timed step: per-pass busy (bubble) and attention kernel timings
+    step_ms, passes = step.timeline()
+    busy = sum(e - s for _, s, e in passes)
+    makespan = max_over_ranks(step_ms)
+    busy_all = sum_over_ranks(busy)
+    bubble = (world * makespan - busy_all) / busy_all if busy_all > 0 else 0.0
+    at = step.attn_stats()
+    mem = step.memory()
+    at_tot = {k: sum_over_ranks(float(v)) for k, v in at.items()}
+    launches_all = int(sum_over_ranks(float(launches)))
+
+    # ---- e2e through the public API: pinned host inputs, loss read back every step
+    e2e = None
+    if not args.no_e2e:
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        loss = 0.0
+        for _ in range(args.steps):
+            loss = step.step(tok_pin.numpy(), tgt_pin.numpy())
+        torch.cuda.synchronize()
+        barrier()
+        wall = max_over_ranks(time.perf_counter() - t0)
+        e2e = {"value": tokens_per_step * args.steps / wall, "unit": "tokens/s",
+               "h2d_bytes_per_step": 2 * tokens_per_step * 4, "d2h_bytes_per_step": 4 * world,
+               "timer": "host wall clock around SlimPipeStep.step (includes H2D/D2H), max over ranks"}
+        if world > 1:
+            t = torch.tensor([loss], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)  # only the last stage is non-zero
+            loss = float(t.item())
+        e2e["loss"] = loss
+
+    peaks, peak_src = load_peaks()
+    peak_tf = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
+    mfu = cfg.model_flops_per_step() / (ms_step / 1e3) / world / (peak_tf * 1e12)
+    mfu_nominal = cfg.model_flops_per_step() / (ms_step / 1e3) / world / 2.25e15
+    # dominant kernel: whichever attention direction has the larger total time
+    kind = "bwd" if at_tot["bwd_ms"] >= at_tot["fwd_ms"] else "fwd"
+    n_l = max(1.0, at_tot[f"{kind}_launches"])
+    achieved = (at_tot[f"{kind}_flops"] / n_l) / (at_tot[f"{kind}_ms"] / n_l / 1e3) / 1e12
+    traffic = None
+    prof = ROOT / "profiles" / "roofline_traffic.json"
+    if prof.exists():
+        traffic = json.loads(prof.read_text()).get(f"attn_{kind}", {}).get("dram_bytes_per_launch")
+    # activation memory: arena slots x slot bytes (x stash + per-layer K/V), max over ranks
+    arena_gb = max_over_ranks(mem["slots"] * mem["slot_bytes"] / 1e9)
+    dkv_gb = cfg.layers // world * cfg.seq_len * 2 * cfg.kv_heads * cfg.head_dim * 4 / 1e9
+    mm = PL.activation_bytes(PL.ModelShape(cfg.layers, cfg.hidden, cfg.ffn_hidden, cfg.heads, cfg.kv_heads,
+                                           cfg.vocab), 1, 1, world, 1, cfg.seq_len, cfg.microbatches, cfg.slices)
+    ledger_gb = float(mm["slice_stage"]) * (cfg.slices + 2 * (world - 1)) / 1e9 if cfg.microbatches * cfg.slices >= \
+        cfg.slices + 2 * (world - 1) else None
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cb = cpu_baseline(cfg, args.cpu_seconds)
+            cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as e:  # never fail the bench line on the baseline leg
+            cpu = {"value": None, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"failed: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": "tokens/s", "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic tokens, random-init weights",
+            "config": {"workload": workload_name(cfg), "model": "llama-7b-shapes", "layers": cfg.layers,
+                       "global_batch": cfg.microbatches, "seq_len": cfg.seq_len, "slices": cfg.slices,
+                       "parallelism": f"pp{world}", "exchange": cfg.exchange,
+                       "l2": "inputs larger than L2 (per-step working set tens of GB)"},
+            "mfu": mfu, "mfu_nominal": mfu_nominal, "mfu_peak_tflops": peak_tf,
+            "bubble_fraction": bubble,
+            "peak_act_gb_per_gpu": arena_gb, "dkv_accum_gb_per_gpu": dkv_gb, "ledger_pred_gb_per_gpu": ledger_gb,
+            "arena_slots": mem["slots"], "arena_high_water": mem["slots_high_water"],
+            "roofline": {"kernel": f"sp_attn_{kind} (sm_100a tcgen05)", "bound": "tensor", "achieved": achieved,
+                         "peak": peak_tf, "unit": "TFLOP/s", "frac": achieved / peak_tf, "traffic": traffic,
+                         "peak_source": f"{peak_src} bf16 sustained",
+                         "attn_fwd_tflops": (at_tot["fwd_flops"] / max(1e-9, at_tot["fwd_ms"] / 1e3)) / 1e12,
+                         "attn_bwd_tflops": (at_tot["bwd_flops"] / max(1e-9, at_tot["bwd_ms"] / 1e3)) / 1e12,
+                         "attn_share_of_step": (at_tot["fwd_ms"] + at_tot["bwd_ms"]) / world / step_ms},
+            "gpu_launches": launches_all,
+            "clocks": clk,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    step.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -49,6 +49,8 @@ const char* sp_status_string(int code);
 const char* sp_last_error(void); /* message of the last failing call on this thread */
 void sp_free(char* p);
 int sp_version(void);
+long long sp_launch_count(void);         /* kernels launched by this library so far */
+long long sp_library_launch_count(void); /* cuBLASLt GEMM calls so far */
 
 /* ---------------------------------------------------------------- planning
  * scheme: 0 gpipe 1 terapipe 2 1f1b 3 interleaved_1f1b 4 zbv 5 vhalf 6 slimpipe

@@ -371,6 +371,7 @@ int launch_bwd(const CUtensorMap& tq, const CUtensorMap& tdo, const CUtensorMap&
     configured = true;
   }
   kern<<<dim3(k_tiles, kv_heads), kThreads, smem, st>>>(tq, tdo, tk, tv, prm);
+  count_launch(1);
   return cuda_status(cudaGetLastError(), "attn_bwd launch");
 }
 
@@ -407,6 +408,7 @@ extern "C" int sp_attn_bwd(const void* q, int64_t q_rows, int64_t q_stride, cons
       attn_bwd_prep<128><<<grid, 256, 0, st>>>(O, o_stride, dO, do_stride, lse, q_rows, heads, lse2, delta);
     else
       attn_bwd_prep<64><<<grid, 256, 0, st>>>(O, o_stride, dO, do_stride, lse, q_rows, heads, lse2, delta);
+    count_launch(1);
     int rc = cuda_status(cudaGetLastError(), "attn_bwd_prep launch");
     if (rc) return rc;
   }

@@ -276,6 +276,7 @@ int launch_fwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& 
     configured = true;
   }
   kern<<<dim3(q_tiles, heads), kThreads, smem, stream>>>(tq, tk, tv, prm);
+  count_launch(1);
   return cuda_status(cudaGetLastError(), "attn_fwd launch");
 }
 

@@ -65,5 +65,6 @@ extern "C" int sp_attn_merge(const void* o_a, const float* lse_a, const void* o_
     attn_merge_kernel<128><<<grid, 256, 0, st>>>(A, lse_a, B, lse_b, rows, heads, o_stride, O, lse_out);
   else
     attn_merge_kernel<64><<<grid, 256, 0, st>>>(A, lse_a, B, lse_b, rows, heads, o_stride, O, lse_out);
+  count_launch(1);
   return cuda_status(cudaGetLastError(), "sp_attn_merge launch");
 }

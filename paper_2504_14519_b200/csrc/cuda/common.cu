@@ -11,7 +11,15 @@
 #include "slimpipe.h"
 #include "sm100.cuh"
 
+#include <atomic>
+
 namespace sp {
+
+static std::atomic<long long> g_own_launches{0}, g_lib_launches{0};
+void count_launch(int n) { g_own_launches += n; }
+void count_library_launch(int n) { g_lib_launches += n; }
+long long own_launches() { return g_own_launches.load(); }
+long long library_launches() { return g_lib_launches.load(); }
 
 int set_error(int code, const char* fmt, ...) {
   char buf[512];
@@ -56,3 +64,6 @@ bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t row_elems, uint
 }
 
 }  // namespace sp
+
+extern "C" long long sp_launch_count(void) { return sp::own_launches(); }
+extern "C" long long sp_library_launch_count(void) { return sp::library_launches(); }

@@ -81,6 +81,7 @@ int gemm(bool trans_a, bool trans_b, int64_t M, int64_t N, int64_t K, const void
     it = S.plans.emplace(key, p).first;
   }
   const Plan& p = it->second;
+  count_library_launch();
   return lt_status(cublasLtMatmul(S.lt, p.op, &alpha, B, p.a, A, p.b, &beta, C, p.c, C, p.c, &p.algo, S.ws,
                                   S.ws_bytes, st),
                    "matmul");

@@ -11,6 +11,8 @@ namespace sp {
 
 int set_error(int code, const char* fmt, ...);
 int cuda_status(cudaError_t e, const char* what);
+void count_launch(int n = 1);          // kernels of this library
+void count_library_launch(int n = 1);  // cuBLASLt calls
 
 // layers.cu
 int embed_fwd(const int32_t* tok, const void* table, void* out, int64_t rows, int dim, cudaStream_t st);

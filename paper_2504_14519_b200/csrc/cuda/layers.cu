@@ -390,11 +390,13 @@ int grid_for(int64_t work, int block) {
 int embed_fwd(const int32_t* tok, const void* table, void* out, int64_t rows, int dim, cudaStream_t st) {
   if (dim % 8) return set_error(SP_ERR_UNSUPPORTED, "embed: dim %% 8");
   embed_fwd_k<<<unsigned(rows), 128, 0, st>>>(tok, (const bf16*)table, (bf16*)out, rows, dim);
+  count_launch();
   return cuda_status(cudaGetLastError(), "embed_fwd");
 }
 
 int embed_bwd(const int32_t* tok, const void* dy, float* dtable, int64_t rows, int dim, cudaStream_t st) {
   embed_bwd_k<<<unsigned(rows), 128, 0, st>>>(tok, (const bf16*)dy, dtable, rows, dim);
+  count_launch();
   return cuda_status(cudaGetLastError(), "embed_bwd");
 }
 
@@ -403,6 +405,7 @@ int rmsnorm_fwd(const void* x, const void* w, void* y, float* rstd, int64_t rows
   int threads = ((dim / 8 + 3) / 4 + 31) / 32 * 32;  // 4 vectors per thread
   if (threads < 32) threads = 32;
   rmsnorm_fwd_k<4><<<unsigned(rows), threads, 0, st>>>((const bf16*)x, (const bf16*)w, (bf16*)y, rstd, dim, eps);
+  count_launch();
   return cuda_status(cudaGetLastError(), "rmsnorm_fwd");
 }
 
@@ -413,6 +416,7 @@ int rmsnorm_bwd(const void* dy, const void* x, const void* w, const float* rstd,
   const int rpb = 32;
   rmsnorm_bwd_k<4><<<unsigned((rows + rpb - 1) / rpb), threads, 0, st>>>(
       (const bf16*)dy, (const bf16*)x, (const bf16*)w, rstd, (const bf16*)dx_in, (bf16*)dx_out, dw, rows, dim, rpb);
+  count_launch();
   return cuda_status(cudaGetLastError(), "rmsnorm_bwd");
 }
 
@@ -420,6 +424,7 @@ int rope_qkv_fwd(const void* qkv, int64_t rows, int heads, int kv_heads, int d, 
                  int64_t q_stride, void* k_out, void* v_out, int64_t kv_stride, cudaStream_t st) {
   rope_qkv_fwd_k<<<unsigned(rows), 256, 0, st>>>((const bf16*)qkv, rows, heads, kv_heads, d, pos0, theta, (bf16*)q_out,
                                                  q_stride, (bf16*)k_out, (bf16*)v_out, kv_stride);
+  count_launch();
   return cuda_status(cudaGetLastError(), "rope_qkv_fwd");
 }
 
@@ -427,16 +432,19 @@ int rope_qkv_bwd(const float* dq, float* dk, float* dv, int64_t kv_stride, int64
                  int d, int64_t pos0, float theta, void* dqkv, int zero_kv, cudaStream_t st) {
   rope_qkv_bwd_k<<<unsigned(rows), 256, 0, st>>>(dq, dk, dv, kv_stride, rows, heads, kv_heads, d, pos0, theta,
                                                  (bf16*)dqkv, zero_kv);
+  count_launch();
   return cuda_status(cudaGetLastError(), "rope_qkv_bwd");
 }
 
 int swiglu_fwd(const void* gu, void* act, int64_t rows, int H, cudaStream_t st) {
   swiglu_fwd_k<<<grid_for(rows * H / 8, 256), 256, 0, st>>>((const bf16*)gu, (bf16*)act, rows, H);
+  count_launch();
   return cuda_status(cudaGetLastError(), "swiglu_fwd");
 }
 
 int swiglu_bwd(const void* dact, const void* gu, void* dgu, int64_t rows, int H, cudaStream_t st) {
   swiglu_bwd_k<<<grid_for(rows * H / 8, 256), 256, 0, st>>>((const bf16*)dact, (const bf16*)gu, (bf16*)dgu, rows, H);
+  count_launch();
   return cuda_status(cudaGetLastError(), "swiglu_bwd");
 }
 
@@ -444,6 +452,7 @@ int cross_entropy(const float* logits, const int32_t* tgt, int64_t rows, int V, 
                   float* loss_sum, cudaStream_t st) {
   if (V % 4) return set_error(SP_ERR_UNSUPPORTED, "cross_entropy: vocab %% 4");
   xent_k<<<unsigned(rows), 256, 0, st>>>(logits, tgt, rows, V, scale, (bf16*)dlogits, loss_sum);
+  count_launch();
   return cuda_status(cudaGetLastError(), "cross_entropy");
 }
 
@@ -451,17 +460,20 @@ int adamw(float* master, void* wbf, const float* g, float* m, float* v, int64_t 
           float eps, float wd, int step, cudaStream_t st) {
   const float c1 = 1.f / (1.f - powf(b1, float(step))), c2 = 1.f / (1.f - powf(b2, float(step)));
   adamw_k<<<grid_for(n, 256), 256, 0, st>>>(master, (bf16*)wbf, g, m, v, n, lr, b1, b2, eps, wd, c1, c2);
+  count_launch();
   return cuda_status(cudaGetLastError(), "adamw");
 }
 
 int init_params(float* master, void* wbf, int64_t n, uint64_t seed, float stdv, float constant, int use_const,
                 cudaStream_t st) {
   init_normal_k<<<grid_for(n, 256), 256, 0, st>>>(master, (bf16*)wbf, n, seed, stdv, constant, use_const);
+  count_launch();
   return cuda_status(cudaGetLastError(), "init_params");
 }
 
 int f32_to_bf16(const float* a, void* b, int64_t n, cudaStream_t st) {
   f32_to_bf16_k<<<grid_for(n, 256), 256, 0, st>>>(a, (bf16*)b, n);
+  count_launch();
   return cuda_status(cudaGetLastError(), "f32_to_bf16");
 }
 

@@ -201,4 +201,5 @@ bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t row_elems, uint
                     uint32_t box_rows);
 int set_error(int code, const char* fmt, ...);
 int cuda_status(cudaError_t e, const char* what);
+void count_launch(int n);
 }  // namespace sp

@@ -379,7 +379,7 @@ class Runtime {
     return SP_OK;
   }
 
-  int run_forward(int k, int i) {
+  int run_forward(int k, int i, cudaEvent_t t0) {
     if (free_slots.empty()) return set_error(SP_ERR_RUNTIME, "arena exhausted (ledger/schedule mismatch)");
     const int slot = free_slots.back();
     free_slots.pop_back();
@@ -388,6 +388,7 @@ class Runtime {
     bf16raw* xs = x_pool + int64_t(slot) * Ls * h;
     const int64_t tok0 = int64_t(k - 1) * cfg.seq_len + int64_t(i - 1) * Ls;
     if (stage == 1) {
+      SP_CUDA(cudaEventRecord(t0, comp));
       SP_TRY(embed_fwd(tokens + tok0, W(emb), xs, Ls, int(h), comp));
     } else {
       cudaEvent_t ready, got;
@@ -398,6 +399,7 @@ class Runtime {
       SP_NCCL(ncclRecv(xs, Ls * h, ncclBfloat16, rank - 1, nc_fwd, cfwd));
       SP_CUDA(cudaEventRecord(got, cfwd));
       SP_CUDA(cudaStreamWaitEvent(comp, got, 0));
+      SP_CUDA(cudaEventRecord(t0, comp));  // busy time starts once the input is here
       cudaEventDestroy(ready);
       cudaEventDestroy(got);
     }
@@ -458,7 +460,7 @@ class Runtime {
     return SP_OK;
   }
 
-  int run_backward(int k, int i) {
+  int run_backward(int k, int i, cudaEvent_t t0) {
     const int slot = slot_of.at({k, i});
     bf16raw* xs = x_pool + int64_t(slot) * Ls * h;
     const int64_t tok0 = int64_t(k - 1) * cfg.seq_len + int64_t(i - 1) * Ls;
@@ -476,7 +478,9 @@ class Runtime {
       SP_CUDA(cudaEventRecord(got, cbwd));
       SP_CUDA(cudaStreamWaitEvent(comp, got, 0));
       cudaEventDestroy(got);
+      SP_CUDA(cudaEventRecord(t0, comp));
     } else {
+      SP_CUDA(cudaEventRecord(t0, comp));
       dx = gout_buf[gout_idx];  // last stage: dX is produced here, sent from here
     }
     // recompute (Full checkpointing)
@@ -545,9 +549,8 @@ class Runtime {
       PassTime t{id, nullptr, nullptr};
       SP_CUDA(cudaEventCreate(&t.start));
       SP_CUDA(cudaEventCreate(&t.end));
-      SP_CUDA(cudaEventRecord(t.start, comp));
-      if (ps.kind == pipelab::PassKind::Forward) SP_TRY(run_forward(ps.microbatch, ps.slice));
-      else SP_TRY(run_backward(ps.microbatch, ps.slice));
+      if (ps.kind == pipelab::PassKind::Forward) SP_TRY(run_forward(ps.microbatch, ps.slice, t.start));
+      else SP_TRY(run_backward(ps.microbatch, ps.slice, t.start));
       SP_CUDA(cudaEventRecord(t.end, comp));
       times.push_back(t);
     }

@@ -33,6 +33,8 @@ _SIGS = {
     "sp_last_error": (C.c_char_p, []),
     "sp_free": (None, [C.c_void_p]),
     "sp_version": (C.c_int, []),
+    "sp_launch_count": (C.c_longlong, []),
+    "sp_library_launch_count": (C.c_longlong, []),
     "sp_plan_schedule_json": (C.c_int, [C.c_int] * 5 + [_charpp]),
     "sp_plan_validate_json": (C.c_int, [C.c_int] * 5 + [_charpp]),
     "sp_plan_balance_json": (C.c_int, [_i64p, _i32p, C.c_int, C.c_int, _charpp]),
