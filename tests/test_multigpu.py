@@ -1,0 +1,25 @@
+"""PP > 1 on real GPUs: runs tests/mp_step_check.py under torchrun when at
+least 2 GPUs are visible (gpurun --gpus 2|4)."""
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parents[1]
+
+
+@pytest.mark.parametrize("pp,m,n", [(2, 2, 4), (2, 1, 2), (4, 2, 4)])
+def test_pipeline_parallel_step_matches_oracle(pp, m, n):
+    if not torch.cuda.is_available() or torch.cuda.device_count() < pp:
+        pytest.skip(f"needs {pp} GPUs")
+    env = dict(os.environ, SP_M=str(m), SP_N=str(n))
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={pp}",
+                        "--master-addr", "127.0.0.1", "--master-port", str(29500 + pp * 10 + m),
+                        str(ROOT / "tests" / "mp_step_check.py")], env=env, capture_output=True, text=True,
+                       timeout=600)
+    print(r.stdout[-3000:], r.stderr[-3000:])
+    assert r.returncode == 0
