@@ -21,7 +21,10 @@
 
 #include "errors.hpp"
 #include "slimpipe.h"
+#include "kernels.hpp"
 #include "sm100.cuh"
+
+#include <cstdlib>
 
 namespace sp {
 namespace {
@@ -412,6 +415,14 @@ extern "C" int sp_attn_bwd(const void* q, int64_t q_rows, int64_t q_stride, cons
     int rc = cuda_status(cudaGetLastError(), "attn_bwd_prep launch");
     if (rc) return rc;
   }
+  for (int c = 0; c < n_chunks; ++c)
+    if (chunk_row[c] < 0 || int64_t(chunk_row[c]) + chunk_len > pool_rows || acc_row[c] < 0 ||
+        int64_t(acc_row[c]) + chunk_len > acc_rows)
+      return set_error(SP_ERR_INVALID, "sp_attn_bwd: chunk %d outside the pool/accumulator", c);
+  if (head_dim == 128 && !getenv("SP_ATTN_BWD_V1"))
+    return attn_bwd_d128(q, q_rows, q_stride, k_pool, v_pool, pool_rows, kv_stride, chunk_row, n_chunks, chunk_len,
+                         heads, kv_heads, causal, dout, do_stride, lse2, delta, dq_acc, dk_acc, dv_acc, acc_rows,
+                         acc_row, st);
   BwdParams prm{};
   prm.q_rows = int(q_rows);
   prm.total_kv = int(total_kv);

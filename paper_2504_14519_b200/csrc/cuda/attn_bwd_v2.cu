@@ -1,0 +1,340 @@
+// K2 (head_dim 128): software-pipelined sliced attention backward, sm_100a.
+//
+// Same math and accumulation contract as attn_bwd.cu (see its header); this
+// variant is the production path for d = 128 and is organised to keep the
+// tensor pipe busy:
+//   * TMEM holds TWO (S^T, dP^T) buffers (2 x 128 cols) + dV (128) + dK (128);
+//     the MMA warp issues S/dP of pair j+1 before dV/dK/dQ of pair j, so the
+//     element math of pair j+1 overlaps the accumulation MMAs of pair j.
+//   * dQ^T of pair j is written into pair j's (now consumed) S^T columns.
+//   * two compute warpgroups (8 warps) split every pair's 64 query columns;
+//   * dQ leaves through TMA bulk reduce-add (cp.reduce.async.bulk.tensor
+//     .add.f32) from a double-buffered smem stage instead of per-thread
+//     global atomics.
+// Warps: 0 TMA producer, 1 TMEM owner + UMMA issuer, 2..9 element math.
+#include <math.h>
+
+#include "errors.hpp"
+#include "kernels.hpp"
+#include "sm100.cuh"
+
+namespace sp {
+namespace {
+
+constexpr int D = 128, BQ = 64, BK = 128, NS = 2;
+constexpr int kThreads = 320;
+constexpr int kCompute = 256;
+constexpr int kSlabQ = BQ * 64, kSlabK = BK * 64;  // elements per slab
+
+struct Params {
+  int q_rows, total_kv, chunk_len, group, causal, n_qtiles;
+  float scale, scale_log2;
+  const float* lse2;
+  const float* delta;
+  float* dk;
+  float* dv;
+  int64_t acc_stride;
+  int chunk_row[SP_MAX_CHUNKS];
+  int acc_row[SP_MAX_CHUNKS];
+};
+
+struct alignas(1024) Smem {
+  __nv_bfloat16 k[BK * D];
+  __nv_bfloat16 v[BK * D];
+  __nv_bfloat16 q[NS][BQ * D];
+  __nv_bfloat16 dout[NS][BQ * D];
+  __nv_bfloat16 p[BK * BQ];
+  __nv_bfloat16 ds[BK * BQ];
+  float stage[2][BQ * D];  // dQ tiles [q][d] on their way to the TMA reduce
+};
+static_assert(sizeof(Smem) % 1024 == 0, "operand tiles stay 1024-aligned");
+
+struct Ctl {  // static shared memory: statistics and barriers
+  float lse2[NS][BQ];
+  float delta[NS][BQ];
+  uint64_t kv_full, q_full[NS], q_empty[NS], sdp_full[2], pds_ready, pds_free, dq_full[2], dq_free[2], acc_done;
+  uint32_t tmem_base;
+};
+
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_bwd_d128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
+                         const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
+                         const __grid_constant__ CUtensorMap tm_dq, const __grid_constant__ Params prm) {
+  extern __shared__ uint8_t smem_raw[];
+  Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(16) Ctl ctl;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int kt = blockIdx.x, kvh = blockIdx.y;
+  const int key0 = kt * BK;
+  const int off = prm.total_kv - prm.q_rows;
+  int t_min = 0;
+  if (prm.causal) {
+    const int num = key0 - off - BQ + 1;
+    t_min = num > 0 ? (num + BQ - 1) / BQ : 0;
+  }
+  const int per_head = prm.n_qtiles - t_min;
+  const int n_pairs = per_head > 0 ? per_head * prm.group : 0;
+  const int chunk = key0 / prm.chunk_len;
+  const int kv_prow = prm.chunk_row[chunk] + key0 % prm.chunk_len;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tm_q);
+    tma_prefetch(&tm_do);
+    tma_prefetch(&tm_k);
+    tma_prefetch(&tm_v);
+    tma_prefetch(&tm_dq);
+    mbar_init(&ctl.kv_full, 1);
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&ctl.q_full[s], 1);
+      mbar_init(&ctl.q_empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&ctl.sdp_full[b], 1);
+      mbar_init(&ctl.dq_full[b], 1);
+      mbar_init(&ctl.dq_free[b], kCompute);
+    }
+    mbar_init(&ctl.pds_ready, kCompute);
+    mbar_init(&ctl.pds_free, 1);
+    mbar_init(&ctl.acc_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(&ctl.tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = ctl.tmem_base;
+  constexpr uint32_t kDV = 256, kDK = 384;
+
+  auto pair_head = [&](int j) { return kvh * prm.group + j / per_head; };
+  auto pair_row = [&](int j) { return (t_min + j % per_head) * BQ; };
+
+  if (warp == 0) {
+    if (lane == 0 && n_pairs > 0) {
+      mbar_arrive_expect_tx(&ctl.kv_full, 2 * BK * D * 2);
+      for (int sl = 0; sl < 2; ++sl) {
+        tma_load_2d(sm.k + sl * kSlabK, &tm_k, &ctl.kv_full, kvh * D + sl * 64, kv_prow);
+        tma_load_2d(sm.v + sl * kSlabK, &tm_v, &ctl.kv_full, kvh * D + sl * 64, kv_prow);
+      }
+      for (int j = 0; j < n_pairs; ++j) {
+        const int s = j % NS, h = pair_head(j), qrow = pair_row(j);
+        mbar_wait(&ctl.q_empty[s], ((j / NS) & 1) ^ 1);
+        mbar_arrive_expect_tx(&ctl.q_full[s], 2 * BQ * D * 2 + 2 * BQ * 4);
+        for (int sl = 0; sl < 2; ++sl) {
+          tma_load_2d(sm.q[s] + sl * kSlabQ, &tm_q, &ctl.q_full[s], h * D + sl * 64, qrow);
+          tma_load_2d(sm.dout[s] + sl * kSlabQ, &tm_do, &ctl.q_full[s], h * D + sl * 64, qrow);
+        }
+        bulk_load(ctl.lse2[s], prm.lse2 + int64_t(h) * prm.q_rows + qrow, BQ * 4, &ctl.q_full[s]);
+        bulk_load(ctl.delta[s], prm.delta + int64_t(h) * prm.q_rows + qrow, BQ * 4, &ctl.q_full[s]);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && n_pairs > 0) {
+      constexpr uint32_t id_s = idesc_bf16_f32(BK, BQ, false, false);  // K Q^T, V dO^T
+      constexpr uint32_t id_acc = idesc_bf16_f32(BK, D, false, true);  // P^T dO, dS^T Q
+      constexpr uint32_t id_dq = idesc_bf16_f32(D, BQ, true, true);    // K^T dS^T
+      const uint32_t k_a = smem_u32(sm.k), v_a = smem_u32(sm.v), p_a = smem_u32(sm.p), ds_a = smem_u32(sm.ds);
+      auto issue_sdp = [&](int j) {
+        const int s = j % NS, b = j & 1;
+        mbar_wait(&ctl.q_full[s], (j / NS) & 1);
+        if (j >= 2) mbar_wait(&ctl.dq_free[b], ((j >> 1) - 1) & 1);  // dQ(j-2) drained from this buffer
+        tc_fence_after();
+        const uint32_t q_a = smem_u32(sm.q[s]), do_a = smem_u32(sm.dout[s]);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t oa = (kk / 4) * (kSlabK * 2) + (kk % 4) * 32;
+          const uint32_t ob = (kk / 4) * (kSlabQ * 2) + (kk % 4) * 32;
+          umma_bf16_ss(tmem + b * 128, smem_desc_sw128(k_a + oa, 16, 1024), smem_desc_sw128(q_a + ob, 16, 1024),
+                       id_s, kk > 0);
+          umma_bf16_ss(tmem + b * 128 + 64, smem_desc_sw128(v_a + oa, 16, 1024),
+                       smem_desc_sw128(do_a + ob, 16, 1024), id_s, kk > 0);
+        }
+        umma_commit(&ctl.sdp_full[b]);
+      };
+      mbar_wait(&ctl.kv_full, 0);
+      issue_sdp(0);
+      for (int j = 0; j < n_pairs; ++j) {
+        const int s = j % NS, b = j & 1;
+        if (j + 1 < n_pairs) issue_sdp(j + 1);
+        mbar_wait(&ctl.pds_ready, j & 1);
+        tc_fence_after();
+        const uint32_t q_a = smem_u32(sm.q[s]), do_a = smem_u32(sm.dout[s]);
+        // dQ^T = K^T dS^T into pair j's S^T columns (K = 128 keys)
+#pragma unroll
+        for (int kk = 0; kk < BK / 16; ++kk) {
+          const uint32_t ok = kk * 16 * 128;
+          umma_bf16_ss(tmem + b * 128, smem_desc_sw128(k_a + ok, kSlabK * 2, 1024),
+                       smem_desc_sw128(ds_a + ok, kSlabK * 2, 1024), id_dq, kk > 0);
+        }
+        umma_commit(&ctl.dq_full[b]);
+        // dV += P^T dO ; dK += dS^T Q   (K = BQ queries)
+#pragma unroll
+        for (int kk = 0; kk < BQ / 16; ++kk) {
+          const uint32_t oa = (kk % 4) * 32;
+          const uint32_t ob = kk * 16 * 128;
+          umma_bf16_ss(tmem + kDV, smem_desc_sw128(p_a + oa, 16, 1024), smem_desc_sw128(do_a + ob, kSlabQ * 2, 1024),
+                       id_acc, (j > 0 || kk > 0) ? 1u : 0u);
+          umma_bf16_ss(tmem + kDK, smem_desc_sw128(ds_a + oa, 16, 1024), smem_desc_sw128(q_a + ob, kSlabQ * 2, 1024),
+                       id_acc, (j > 0 || kk > 0) ? 1u : 0u);
+        }
+        umma_commit(&ctl.q_empty[s]);
+        umma_commit(&ctl.pds_free);
+      }
+      umma_commit(&ctl.acc_done);
+    }
+  } else {
+    // ------------------------------------------------ element math (2 WGs)
+    const int cw = warp - 2;         // 0..7
+    const int wg = cw >> 2;          // column half of every pair
+    const int quarter = warp & 3;    // TMEM lane quarter
+    const int r = quarter * 32 + lane;
+    const int ctid = cw * 32 + lane;  // 0..255
+    const uint32_t lane_off = uint32_t(quarter * 32) << 16;
+    const uint32_t p_a = smem_u32(sm.p), ds_a = smem_u32(sm.ds);
+    const int key_rel = key0 - off + r;
+    const int c0 = wg * 32;
+
+    auto drain = [&](int jj) {
+      const int bb = jj & 1;
+      mbar_wait(&ctl.dq_full[bb], (jj >> 1) & 1);
+      tc_fence_after();
+      float dq[32];
+      tmem_ld32(tmem + lane_off + bb * 128 + c0, dq);  // lane r = d, columns = queries c0..c0+31
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(&ctl.dq_free[bb]);
+      // stage buffer bb is free once the reduce issued two drains ago has read it
+      if (ctid == 0) bulk_wait_read<1>();
+      named_bar_sync(1, kCompute);
+      float* st = sm.stage[bb];
+#pragma unroll
+      for (int x = 0; x < 32; ++x) st[(c0 + x) * D + r] = dq[x];
+      fence_async_smem();
+      named_bar_sync(2, kCompute);
+      if (ctid == 0) {
+        tma_reduce_add_2d(&tm_dq, st, pair_head(jj) * D, pair_row(jj));
+        bulk_commit();
+      }
+    };
+
+    for (int j = 0; j < n_pairs; ++j) {
+      const int s = j % NS, b = j & 1;
+      const int qrow0 = pair_row(j);
+      const bool need_mask = prm.causal && (key0 + BK - 1 - off > qrow0);
+      mbar_wait(&ctl.q_full[s], (j / NS) & 1);
+      mbar_wait(&ctl.sdp_full[b], (j >> 1) & 1);
+      tc_fence_after();
+      float sv[32], dp[32];
+      tmem_ld32(tmem + lane_off + b * 128 + c0, sv);
+      tmem_ld32(tmem + lane_off + b * 128 + 64 + c0, dp);
+      tmem_wait_ld();
+      uint32_t pk[16], dk[16];
+#pragma unroll
+      for (int x = 0; x < 32; x += 2) {
+        float pp[2], dd[2];
+#pragma unroll
+        for (int y = 0; y < 2; ++y) {
+          const int c = c0 + x + y;
+          float pv = fast_exp2(fmaf(sv[x + y], prm.scale_log2, -ctl.lse2[s][c]));
+          if (need_mask && key_rel > qrow0 + c) pv = 0.f;
+          pp[y] = pv;
+          dd[y] = pv * (dp[x + y] - ctl.delta[s][c]) * prm.scale;
+        }
+        pk[x / 2] = pack_bf16(pp[0], pp[1]);
+        dk[x / 2] = pack_bf16(dd[0], dd[1]);
+      }
+      if (j > 0) mbar_wait(&ctl.pds_free, (j - 1) & 1);
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        const uint32_t o = sw128_offset(r, c0 + g * 8);
+        st_shared_v4(p_a + o, pk[4 * g], pk[4 * g + 1], pk[4 * g + 2], pk[4 * g + 3]);
+        st_shared_v4(ds_a + o, dk[4 * g], dk[4 * g + 1], dk[4 * g + 2], dk[4 * g + 3]);
+      }
+      fence_async_smem();
+      tc_fence_before();
+      mbar_arrive(&ctl.pds_ready);
+      if (j > 0) drain(j - 1);
+    }
+    if (n_pairs > 0) {
+      drain(n_pairs - 1);
+      // dK / dV (lane r = key, 128 cols each) += into the fp32 chunk accumulators
+      mbar_wait(&ctl.acc_done, 0);
+      tc_fence_after();
+      const int64_t arow = prm.acc_row[chunk] + key0 % prm.chunk_len + r;
+      float* dst = (wg == 0 ? prm.dk : prm.dv) + arow * prm.acc_stride + kvh * D;
+      const uint32_t col = wg == 0 ? kDK : kDV;
+#pragma unroll
+      for (int ch = 0; ch < D / 32; ++ch) {
+        float a[32];
+        tmem_ld32(tmem + lane_off + col + ch * 32, a);
+        tmem_wait_ld();
+        float4* g4 = reinterpret_cast<float4*>(dst + ch * 32);
+#pragma unroll
+        for (int x = 0; x < 8; ++x) {
+          const float4 o = g4[x];
+          g4[x] = make_float4(o.x + a[4 * x], o.y + a[4 * x + 1], o.z + a[4 * x + 2], o.w + a[4 * x + 3]);
+        }
+      }
+      if (ctid == 0) bulk_wait<0>();
+    }
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+}  // namespace
+
+// Launch the d=128 backward (lse2/delta already prepared by attn_bwd_prep).
+int attn_bwd_d128(const void* q, int64_t q_rows, int64_t q_stride, const void* k_pool, const void* v_pool,
+                  int64_t pool_rows, int64_t kv_stride, const int32_t* chunk_row, int n_chunks, int chunk_len,
+                  int heads, int kv_heads, int causal, const void* dout, int64_t do_stride, const float* lse2,
+                  const float* delta, float* dq_acc, float* dk_acc, float* dv_acc, int64_t acc_rows,
+                  const int32_t* acc_row, cudaStream_t st) {
+  Params prm{};
+  prm.q_rows = int(q_rows);
+  prm.total_kv = n_chunks * chunk_len;
+  prm.chunk_len = chunk_len;
+  prm.group = heads / kv_heads;
+  prm.causal = causal;
+  prm.n_qtiles = int(q_rows / BQ);
+  prm.scale = float(1.0 / sqrt(double(D)));
+  prm.scale_log2 = float(1.4426950408889634 / sqrt(double(D)));
+  prm.lse2 = lse2;
+  prm.delta = delta;
+  prm.dk = dk_acc;
+  prm.dv = dv_acc;
+  prm.acc_stride = int64_t(kv_heads) * D;
+  for (int c = 0; c < n_chunks; ++c) {
+    prm.chunk_row[c] = chunk_row[c];
+    prm.acc_row[c] = acc_row[c];
+  }
+  CUtensorMap tq, tdo, tk, tv, tdq;
+  if (!make_tmap_bf16(&tq, q, uint64_t(q_stride), uint64_t(q_rows), uint64_t(q_stride), BQ) ||
+      !make_tmap_bf16(&tdo, dout, uint64_t(do_stride), uint64_t(q_rows), uint64_t(do_stride), BQ) ||
+      !make_tmap_bf16(&tk, k_pool, uint64_t(kv_stride), uint64_t(pool_rows), uint64_t(kv_stride), BK) ||
+      !make_tmap_bf16(&tv, v_pool, uint64_t(kv_stride), uint64_t(pool_rows), uint64_t(kv_stride), BK) ||
+      !make_tmap_f32(&tdq, dq_acc, uint64_t(heads) * D, uint64_t(q_rows), uint64_t(heads) * D, D, BQ))
+    return set_error(SP_ERR_CUDA, "attn_bwd_d128: cuTensorMapEncodeTiled failed (alignment?)");
+  const size_t smem = sizeof(Smem) + 1024;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(attn_bwd_d128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return cuda_status(e, "attn_bwd_d128: set smem");
+    configured = true;
+  }
+  attn_bwd_d128_kernel<<<dim3(prm.total_kv / BK, kv_heads), kThreads, smem, st>>>(tq, tdo, tk, tv, tdq, prm);
+  count_launch(1);
+  return cuda_status(cudaGetLastError(), "attn_bwd_d128 launch");
+}
+
+}  // namespace sp

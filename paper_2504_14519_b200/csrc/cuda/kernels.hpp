@@ -34,6 +34,13 @@ int init_params(float* master, void* wbf, int64_t n, uint64_t seed, float stdv, 
                 cudaStream_t st);
 int f32_to_bf16(const float* a, void* b, int64_t n, cudaStream_t st);
 
+// attn_bwd_v2.cu — pipelined d=128 backward (lse2/delta prepared by the caller)
+int attn_bwd_d128(const void* q, int64_t q_rows, int64_t q_stride, const void* k_pool, const void* v_pool,
+                  int64_t pool_rows, int64_t kv_stride, const int32_t* chunk_row, int n_chunks, int chunk_len,
+                  int heads, int kv_heads, int causal, const void* dout, int64_t do_stride, const float* lse2,
+                  const float* delta, float* dq_acc, float* dk_acc, float* dv_acc, int64_t acc_rows,
+                  const int32_t* acc_row, cudaStream_t st);
+
 // gemm.cu — row-major GEMMs on cuBLASLt (bf16 inputs, fp32 accumulate).
 //   C[M,N] = alpha * op(A) op(B) + beta * C
 //   A is [M,K] (or [K,M] when trans_a), B is [K,N] (or [N,K] when trans_b),

@@ -185,6 +185,23 @@ __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
 
+// smem tile += into global through TMA (bulk-group completion).
+__device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, const void* src, int32_t c0, int32_t c1) {
+  asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+
 __device__ __forceinline__ float fast_exp2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -199,6 +216,9 @@ namespace sp {
 // pitch `pitch_elems`; box = {64 elements, box_rows}, 128-B swizzle.
 bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t row_elems, uint64_t rows, uint64_t pitch_elems,
                     uint32_t box_rows);
+// fp32 2-D map, no swizzle, box = {box_inner, box_rows} (for TMA reduce-add).
+bool make_tmap_f32(CUtensorMap* map, const void* base, uint64_t row_elems, uint64_t rows, uint64_t pitch_elems,
+                   uint32_t box_inner, uint32_t box_rows);
 int set_error(int code, const char* fmt, ...);
 int cuda_status(cudaError_t e, const char* what);
 void count_launch(int n);
