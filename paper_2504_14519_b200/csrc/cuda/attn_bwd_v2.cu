@@ -200,31 +200,38 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int key_rel = key0 - off + r;
     const int c0 = wg * 32;
 
-    auto drain = [&](int jj) {
+    // dQ of pair jj: (1) TMEM -> registers, freeing its TMEM columns for the
+    // S/dP of pair jj+2 as early as possible; (2) registers -> smem stage ->
+    // TMA reduce-add into dq_acc.
+    float dq[32];
+    auto drain_load = [&](int jj) {
       const int bb = jj & 1;
       mbar_wait(&ctl.dq_full[bb], (jj >> 1) & 1);
       tc_fence_after();
-      float dq[32];
       tmem_ld32(tmem + lane_off + bb * 128 + c0, dq);  // lane r = d, columns = queries c0..c0+31
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(&ctl.dq_free[bb]);
+    };
+    auto drain_store = [&](int jj) {
+      const int bb = jj & 1;
       // stage buffer bb is free once the reduce issued two drains ago has read it
       if (ctid == 0) bulk_wait_read<1>();
       named_bar_sync(1, kCompute);
-      float* st = sm.stage[bb];
+      const uint32_t st = smem_u32(sm.stage[bb]) + uint32_t(c0 * D + r) * 4u;
 #pragma unroll
-      for (int x = 0; x < 32; ++x) st[(c0 + x) * D + r] = dq[x];
+      for (int x = 0; x < 32; ++x) asm volatile("st.shared.f32 [%0], %1;" ::"r"(st + x * D * 4), "f"(dq[x]) : "memory");
       fence_async_smem();
       named_bar_sync(2, kCompute);
       if (ctid == 0) {
-        tma_reduce_add_2d(&tm_dq, st, pair_head(jj) * D, pair_row(jj));
+        tma_reduce_add_2d(&tm_dq, sm.stage[bb], pair_head(jj) * D, pair_row(jj));
         bulk_commit();
       }
     };
 
     for (int j = 0; j < n_pairs; ++j) {
       const int s = j % NS, b = j & 1;
+      if (j > 0) drain_load(j - 1);
       const int qrow0 = pair_row(j);
       const bool need_mask = prm.causal && (key0 + BK - 1 - off > qrow0);
       mbar_wait(&ctl.q_full[s], (j / NS) & 1);
@@ -259,10 +266,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       fence_async_smem();
       tc_fence_before();
       mbar_arrive(&ctl.pds_ready);
-      if (j > 0) drain(j - 1);
+      if (j > 0) drain_store(j - 1);
     }
     if (n_pairs > 0) {
-      drain(n_pairs - 1);
+      drain_load(n_pairs - 1);
+      drain_store(n_pairs - 1);
       // dK / dV (lane r = key, 128 cols each) += into the fp32 chunk accumulators
       mbar_wait(&ctl.acc_done, 0);
       tc_fence_after();
