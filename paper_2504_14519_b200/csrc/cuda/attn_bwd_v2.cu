@@ -18,10 +18,12 @@
 #include "kernels.hpp"
 #include "sm100.cuh"
 
+#include <cstdlib>
+
 namespace sp {
 namespace {
 
-constexpr int D = 128, BQ = 64, BK = 128, NS = 2;
+constexpr int D = 128, BQ = 64, BK = 128, NS = 3;
 constexpr int kThreads = 320;
 constexpr int kCompute = 256;
 constexpr int kSlabQ = BQ * 64, kSlabK = BK * 64;  // elements per slab
@@ -34,6 +36,7 @@ struct Params {
   float* dk;
   float* dv;
   int64_t acc_stride;
+  int trace;  // record a per-pair timeline of CTA (0,0) into g_bwd_trace
   int chunk_row[SP_MAX_CHUNKS];
   int acc_row[SP_MAX_CHUNKS];
 };
@@ -45,7 +48,7 @@ struct alignas(1024) Smem {
   __nv_bfloat16 dout[NS][BQ * D];
   __nv_bfloat16 p[BK * BQ];
   __nv_bfloat16 ds[BK * BQ];
-  float stage[2][BQ * D];  // dQ tiles [q][d] on their way to the TMA reduce
+  float stage[1][BQ * D];  // dQ tile [q][d] on their way to the TMA reduce
 };
 static_assert(sizeof(Smem) % 1024 == 0, "operand tiles stay 1024-aligned");
 
@@ -55,6 +58,12 @@ struct Ctl {  // static shared memory: statistics and barriers
   uint64_t kv_full, q_full[NS], q_empty[NS], sdp_full[2], pds_ready, pds_free, dq_full[2], dq_free[2], acc_done;
   uint32_t tmem_base;
 };
+
+__device__ long long g_bwd_trace[10][512];
+#define TR(e, j)                                                                        \
+  do {                                                                                 \
+    if (tracing && (j) < 512) g_bwd_trace[e][(j)] = clock64();                        \
+  } while (0)
 
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -83,6 +92,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int n_pairs = per_head > 0 ? per_head * prm.group : 0;
   const int chunk = key0 / prm.chunk_len;
   const int kv_prow = prm.chunk_row[chunk] + key0 % prm.chunk_len;
+  const bool tracing = prm.trace && blockIdx.x == 0 && blockIdx.y == 0;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tm_q);
@@ -161,8 +171,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       issue_sdp(0);
       for (int j = 0; j < n_pairs; ++j) {
         const int s = j % NS, b = j & 1;
+        TR(0, j);
         if (j + 1 < n_pairs) issue_sdp(j + 1);
+        TR(1, j);
         mbar_wait(&ctl.pds_ready, j & 1);
+        TR(2, j);
         tc_fence_after();
         const uint32_t q_a = smem_u32(sm.q[s]), do_a = smem_u32(sm.dout[s]);
         // dQ^T = K^T dS^T into pair j's S^T columns (K = 128 keys)
@@ -185,6 +198,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         umma_commit(&ctl.q_empty[s]);
         umma_commit(&ctl.pds_free);
+        TR(3, j);
       }
       umma_commit(&ctl.acc_done);
     }
@@ -216,26 +230,29 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto drain_store = [&](int jj) {
       const int bb = jj & 1;
       // stage buffer bb is free once the reduce issued two drains ago has read it
-      if (ctid == 0) bulk_wait_read<1>();
+      if (ctid == 0) bulk_wait_read<0>();
       named_bar_sync(1, kCompute);
-      const uint32_t st = smem_u32(sm.stage[bb]) + uint32_t(c0 * D + r) * 4u;
+      const uint32_t st = smem_u32(sm.stage[0]) + uint32_t(c0 * D + r) * 4u;
 #pragma unroll
       for (int x = 0; x < 32; ++x) asm volatile("st.shared.f32 [%0], %1;" ::"r"(st + x * D * 4), "f"(dq[x]) : "memory");
       fence_async_smem();
       named_bar_sync(2, kCompute);
       if (ctid == 0) {
-        tma_reduce_add_2d(&tm_dq, sm.stage[bb], pair_head(jj) * D, pair_row(jj));
+        tma_reduce_add_2d(&tm_dq, sm.stage[0], pair_head(jj) * D, pair_row(jj));
         bulk_commit();
       }
     };
 
     for (int j = 0; j < n_pairs; ++j) {
       const int s = j % NS, b = j & 1;
+      const bool tl = ctid == 0;
       if (j > 0) drain_load(j - 1);
+      if (tl) TR(4, j);
       const int qrow0 = pair_row(j);
       const bool need_mask = prm.causal && (key0 + BK - 1 - off > qrow0);
       mbar_wait(&ctl.q_full[s], (j / NS) & 1);
       mbar_wait(&ctl.sdp_full[b], (j >> 1) & 1);
+      if (tl) TR(5, j);
       tc_fence_after();
       float sv[32], dp[32];
       tmem_ld32(tmem + lane_off + b * 128 + c0, sv);
@@ -256,7 +273,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         pk[x / 2] = pack_bf16(pp[0], pp[1]);
         dk[x / 2] = pack_bf16(dd[0], dd[1]);
       }
+      if (tl) TR(6, j);
       if (j > 0) mbar_wait(&ctl.pds_free, (j - 1) & 1);
+      if (tl) TR(7, j);
 #pragma unroll
       for (int g = 0; g < 4; ++g) {
         const uint32_t o = sw128_offset(r, c0 + g * 8);
@@ -266,7 +285,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       fence_async_smem();
       tc_fence_before();
       mbar_arrive(&ctl.pds_ready);
+      if (tl) TR(8, j);
       if (j > 0) drain_store(j - 1);
+      if (tl) TR(9, j);
     }
     if (n_pairs > 0) {
       drain_load(n_pairs - 1);
@@ -322,6 +343,7 @@ int attn_bwd_d128(const void* q, int64_t q_rows, int64_t q_stride, const void* k
   prm.dk = dk_acc;
   prm.dv = dv_acc;
   prm.acc_stride = int64_t(kv_heads) * D;
+  prm.trace = getenv("SP_BWD_TRACE") != nullptr;
   for (int c = 0; c < n_chunks; ++c) {
     prm.chunk_row[c] = chunk_row[c];
     prm.acc_row[c] = acc_row[c];
@@ -345,4 +367,10 @@ int attn_bwd_d128(const void* q, int64_t q_rows, int64_t q_stride, const void* k
   return cuda_status(cudaGetLastError(), "attn_bwd_d128 launch");
 }
 
+int bwd_trace_copy(long long* out) {
+  return cuda_status(cudaMemcpyFromSymbol(out, g_bwd_trace, sizeof(long long) * 10 * 512), "trace copy");
+}
+
 }  // namespace sp
+
+extern "C" int sp_debug_bwd_trace(long long* out) { return sp::bwd_trace_copy(out); }
