@@ -326,7 +326,7 @@ extern "C" int sp_attn_fwd(const void* q, int64_t q_rows, int64_t q_stride, cons
     return set_error(SP_ERR_CUDA, "sp_attn_fwd: cuTensorMapEncodeTiled failed (alignment?)");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int q_tiles = int(q_rows / 128);
-  if (head_dim == 128 && q_rows % 256 == 0 && !getenv("SP_ATTN_FWD_V1"))
+  if (head_dim == 128 && !getenv("SP_ATTN_FWD_V1"))
     return attn_fwd_d128(q, q_rows, q_stride, k_pool, v_pool, pool_rows, kv_stride, chunk_row, n_chunks, chunk_len,
                          heads, kv_heads, causal, o, o_stride, lse, st);
   if (head_dim == 128) return launch_fwd<128, 2>(tq, tk, tv, prm, q_tiles, heads, st);

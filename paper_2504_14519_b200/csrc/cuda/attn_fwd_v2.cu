@@ -1,37 +1,37 @@
-// K1 (head_dim 128): sliced causal attention forward, two query tiles per CTA,
-// P kept in TMEM.  Same semantics as attn_fwd.cu (reference chunk_attention,
+// K1 (head_dim 128): sliced causal attention forward, production path.
+// Same semantics as attn_fwd.cu (reference chunk_attention,
 // proj/src/attention.cpp:21-111: scale 1/sqrt(d), bottom-right causal,
-// finalize O/l, plus LSE); this is the production path for d = 128.
+// finalize O/l, plus the LSE the backward and the exchange merge need).
 //
-// Why: with P staged through shared memory the forward is shared-memory
-// bandwidth bound (S = QK^T and O += PV are both SS-UMMAs at 128 B/clk, plus
-// the P tile write).  Here:
-//   * one CTA owns 256 query rows (two 128-row tiles t = 0, 1) of one head,
-//     so every K/V tile loaded by TMA feeds two query tiles;
-//   * TMEM: tile t has S_t (128 fp32 cols) and O_t (128 cols); the softmax
-//     writes P_t as packed bf16 over the first 64 columns of S_t, and
-//     O_t += P_t V is a TS-UMMA (A from TMEM) — no P traffic in smem;
-//   * the MMA warp interleaves  PV_0(j-1), S_0(j), PV_1(j-1), S_1(j): while
-//     softmax warpgroup 0 works on S_0(j) the tensor core runs tile 1's work
-//     and vice versa (ping-pong).  tcgen05 ops of one thread execute in
-//     order, so when S_t(j) is complete PV_t(j-1) is complete too: the
-//     softmax may rescale O_t in place without another barrier, and S_t(j)
-//     may overwrite P_t(j-1).
-// Warps: 0 TMA producer, 1 TMEM owner + UMMA issuer, 2-5 softmax tile 0,
-// 6-9 softmax tile 1.
+// Organisation (one CTA = 128 query rows of one head):
+//   * TMEM: S double buffer (2 x 128 fp32 cols) + two O accumulators
+//     O_A, O_B (128 cols each) = 512 cols.
+//   * 8 softmax warps: thread (r, half) owns query row r and key columns
+//     [64*half, 64*half+64) of every KV tile, with its OWN running max, sum
+//     and accumulator O_half (split-KV inside the CTA).  No cross-thread
+//     reduction in the loop; the two halves are merged once in the epilogue
+//     exactly like the reference merges partials (attention.cpp:63-92).
+//     The per-tile softmax critical path is 64 exponentials per thread.
+//   * P is written back as packed bf16 over the thread's own S columns and
+//     consumed by TS-UMMAs (A from TMEM): O_half += P_half V[half rows].
+//   * the MMA warp issues S(j+1) before PV(j), so the tensor core computes the
+//     next scores while the softmax of the current tile runs.  tcgen05 ops of
+//     one thread execute in order: S(j+1) may overwrite P(j-1) (issued after
+//     PV(j-1)); the softmax waits for PV(j-1) (o_ready) only when it must
+//     rescale O (lazy rescale: running max grew by > 8 in log2 units).
+// Warps: 0 TMA producer, 1 TMEM owner + UMMA issuer, 2-5 half 0, 6-9 half 1.
 #include <math.h>
 
 #include "errors.hpp"
 #include "kernels.hpp"
 #include "sm100.cuh"
 
-#include <cstdlib>
-
 namespace sp {
 namespace {
 
 constexpr int D = 128, BM = 128, BN = 128, NK = 3, NV = 2;
 constexpr int kThreads = 320;
+constexpr int kSoftmax = 256;
 constexpr int kSlab = 128 * 64;
 
 struct Params {
@@ -44,31 +44,16 @@ struct Params {
 };
 
 struct alignas(1024) Smem {
-  __nv_bfloat16 q[2][BM * D];
+  __nv_bfloat16 q[BM * D];
   __nv_bfloat16 k[NK][BN * D];
   __nv_bfloat16 v[NV][BN * D];
 };
 
 struct Ctl {
-  uint64_t q_full, k_full[NK], k_empty[NK], v_full[NV], v_empty[NV], s_full[2], p_full[2], o_done[2];
+  uint64_t q_full, k_full[NK], k_empty[NK], v_full[NV], v_empty[NV], s_full[2], p_full[2], o_ready;
+  float m_half[2][BM], l_half[2][BM];
   uint32_t tmem_base;
 };
-
-
-// 2^x on the FMA/ALU pipes: x = j + f (j = round(x), |f| <= 1/2), 2^f by a
-// degree-4 polynomial (rel. err < 5e-5, far below the bf16 rounding of P),
-// 2^j added into the exponent bits.  x is clamped at -126 (result ~0).
-__device__ __forceinline__ float poly_exp2(float x) {
-  x = fmaxf(x, -126.f);
-  const float t = x + 12582912.f;  // 1.5 * 2^23: round-to-nearest in the mantissa
-  const int j = __float_as_int(t) - 0x4B400000;
-  const float f = x - (t - 12582912.f);
-  float p = fmaf(0.0096181291f, f, 0.0555041087f);
-  p = fmaf(p, f, 0.2402264923f);
-  p = fmaf(p, f, 0.6931471806f);
-  p = fmaf(p, f, 1.0f);
-  return __int_as_float(__float_as_int(p) + (j << 23));
-}
 
 // D[tmem] (+)= A[tmem] * B[smem]
 __device__ __forceinline__ void umma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
@@ -90,7 +75,6 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
       : "memory");
 }
 
-template <int kPolyEvery>  // 1 in 2*kPolyEvery exponentials on the FMA pipe (0: none)
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_d128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                          const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ Params prm) {
@@ -98,14 +82,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ __align__(16) Ctl ctl;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int block = gridDim.x - 1 - blockIdx.x;  // longest causal ranges first
+  const int tile = gridDim.x - 1 - blockIdx.x;  // longest causal ranges first
   const int head = blockIdx.y;
   const int kvh = head / prm.group;
-  const int row0 = block * 2 * BM;
-  // KV tiles: tile 1 (rows row0+128..) needs n1 tiles, tile 0 needs n1-1 (causal)
-  const int off = prm.total_kv - prm.q_rows;
-  const int n1 = prm.causal ? (off + row0 + 2 * BM) / BN : prm.total_kv / BN;
-  const int n0 = prm.causal ? n1 - 1 : n1;
+  const int row0 = tile * BM;
+  const int n = prm.causal ? (prm.total_kv - prm.q_rows + row0 + BM) / BN : prm.total_kv / BN;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tm_q);
@@ -120,11 +101,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&ctl.v_full[s], 1);
       mbar_init(&ctl.v_empty[s], 1);
     }
-    for (int t = 0; t < 2; ++t) {
-      mbar_init(&ctl.s_full[t], 1);
-      mbar_init(&ctl.p_full[t], 128);
-      mbar_init(&ctl.o_done[t], 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&ctl.s_full[b], 1);
+      mbar_init(&ctl.p_full[b], kSoftmax);
     }
+    mbar_init(&ctl.o_ready, 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(&ctl.tmem_base);
@@ -132,8 +113,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = ctl.tmem_base;
-  auto s_col = [&](int t) { return tmem + t * 256; };
-  auto o_col = [&](int t) { return tmem + t * 256 + 128; };
   auto kv_row = [&](int j) {
     const int key = j * BN;
     return prm.chunk_row[key / prm.chunk_len] + key % prm.chunk_len;
@@ -141,176 +120,178 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_arrive_expect_tx(&ctl.q_full, 2 * BM * D * 2);
-      for (int t = 0; t < 2; ++t)
-        for (int sl = 0; sl < 2; ++sl)
-          tma_load_2d(sm.q[t] + sl * kSlab, &tm_q, &ctl.q_full, head * D + sl * 64, row0 + t * BM);
-      int jk = 0, jv = 0;
+      mbar_arrive_expect_tx(&ctl.q_full, BM * D * 2);
+      for (int sl = 0; sl < 2; ++sl) tma_load_2d(sm.q + sl * kSlab, &tm_q, &ctl.q_full, head * D + sl * 64, row0);
       auto load_k = [&](int j) {
         const int s = j % NK;
         mbar_wait(&ctl.k_empty[s], ((j / NK) & 1) ^ 1);
         mbar_arrive_expect_tx(&ctl.k_full[s], BN * D * 2);
-        for (int sl = 0; sl < 2; ++sl) tma_load_2d(sm.k[s] + sl * kSlab, &tm_k, &ctl.k_full[s], kvh * D + sl * 64, kv_row(j));
+        for (int sl = 0; sl < 2; ++sl)
+          tma_load_2d(sm.k[s] + sl * kSlab, &tm_k, &ctl.k_full[s], kvh * D + sl * 64, kv_row(j));
       };
       auto load_v = [&](int j) {
         const int s = j % NV;
         mbar_wait(&ctl.v_empty[s], ((j / NV) & 1) ^ 1);
         mbar_arrive_expect_tx(&ctl.v_full[s], BN * D * 2);
-        for (int sl = 0; sl < 2; ++sl) tma_load_2d(sm.v[s] + sl * kSlab, &tm_v, &ctl.v_full[s], kvh * D + sl * 64, kv_row(j));
+        for (int sl = 0; sl < 2; ++sl)
+          tma_load_2d(sm.v[s] + sl * kSlab, &tm_v, &ctl.v_full[s], kvh * D + sl * 64, kv_row(j));
       };
-      // K runs one tile ahead of V (S(j) is issued before PV(j))
-      for (; jk < n1 && jk < 1; ++jk) load_k(jk);
-      for (; jv < n1; ++jv) {
-        if (jk < n1) load_k(jk++);
+      // consumption order: S(0), S(1), PV(0), S(2), PV(1), ... (K two ahead of V)
+      int jk = 0;
+      for (; jk < n && jk < 2; ++jk) load_k(jk);
+      for (int jv = 0; jv < n; ++jv) {
         load_v(jv);
+        if (jk < n) load_k(jk++);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t id_s = idesc_bf16_f32(BM, BN, false, false);
       constexpr uint32_t id_o = idesc_bf16_f32(BM, D, false, true);
-      const uint32_t q_a[2] = {smem_u32(sm.q[0]), smem_u32(sm.q[1])};
-      auto issue_s = [&](int t, int j) {
-        const uint32_t k_a = smem_u32(sm.k[j % NK]);
+      const uint32_t q_a = smem_u32(sm.q);
+      auto issue_s = [&](int j) {
+        const int s = j % NK;
+        mbar_wait(&ctl.k_full[s], (j / NK) & 1);
+        tc_fence_after();
+        const uint32_t k_a = smem_u32(sm.k[s]);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t o = (kk / 4) * (kSlab * 2) + (kk % 4) * 32;
-          umma_bf16_ss(s_col(t), smem_desc_sw128(q_a[t] + o, 16, 1024), smem_desc_sw128(k_a + o, 16, 1024), id_s,
-                       kk > 0);
+          umma_bf16_ss(tmem + (j & 1) * 128, smem_desc_sw128(q_a + o, 16, 1024), smem_desc_sw128(k_a + o, 16, 1024),
+                       id_s, kk > 0);
         }
-        umma_commit(&ctl.s_full[t]);
-      };
-      auto issue_pv = [&](int t, int j, int pv_count) {
-        const uint32_t v_a = smem_u32(sm.v[j % NV]);
-#pragma unroll
-        for (int kk = 0; kk < BN / 16; ++kk)
-          umma_bf16_ts(o_col(t), s_col(t) + kk * 8, smem_desc_sw128(v_a + kk * 16 * 128, kSlab * 2, 1024), id_o,
-                       (pv_count > 0 || kk > 0) ? 1u : 0u);
+        umma_commit(&ctl.s_full[j & 1]);
+        umma_commit(&ctl.k_empty[s]);
       };
       mbar_wait(&ctl.q_full, 0);
-      int p_seen[2] = {0, 0};  // P tiles consumed per query tile
-      for (int j = 0; j <= n1; ++j) {
-        const bool has_k = j < n1;
-        if (has_k) {
-          mbar_wait(&ctl.k_full[j % NK], (j / NK) & 1);
-          tc_fence_after();
-        }
-        if (j > 0) mbar_wait(&ctl.v_full[(j - 1) % NV], ((j - 1) / NV) & 1);
-        for (int t = 0; t < 2; ++t) {
-          const int nt = t == 0 ? n0 : n1;
-          if (j > 0 && j - 1 < nt) {  // O_t += P_t(j-1) V(j-1)
-            mbar_wait(&ctl.p_full[t], p_seen[t] & 1);
-            tc_fence_after();
-            issue_pv(t, j - 1, p_seen[t]);
-            ++p_seen[t];
-            if (p_seen[t] == nt) umma_commit(&ctl.o_done[t]);
-          }
-          if (j < nt) issue_s(t, j);
-        }
-        if (j > 0) umma_commit(&ctl.v_empty[(j - 1) % NV]);
-        if (has_k) umma_commit(&ctl.k_empty[j % NK]);
+      tc_fence_after();
+      if (n > 0) issue_s(0);
+      for (int j = 0; j < n; ++j) {
+        // S(j+1) into the other buffer: softmax(j-1) finished with it (p_full
+        // waited in iteration j-1) and P(j-1) is consumed by PV(j-1), issued
+        // before this MMA (in-order tcgen05 pipe).
+        if (j + 1 < n) issue_s(j + 1);
+        mbar_wait(&ctl.p_full[j & 1], (j >> 1) & 1);
+        mbar_wait(&ctl.v_full[j % NV], (j / NV) & 1);
+        tc_fence_after();
+        const uint32_t v_a = smem_u32(sm.v[j % NV]);
+        const uint32_t p_t = tmem + (j & 1) * 128;
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf)
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)  // keys [64hf + 16kk, +16)
+            umma_bf16_ts(tmem + 256 + hf * 128, p_t + hf * 64 + kk * 8,
+                         smem_desc_sw128(v_a + (hf * 64 + kk * 16) * 128, kSlab * 2, 1024), id_o,
+                         (j > 0 || kk > 0) ? 1u : 0u);
+        umma_commit(&ctl.v_empty[j % NV]);
+        umma_commit(&ctl.o_ready);
       }
     }
   } else {
-    // ------------------------------------------------ softmax, one WG per query tile
-    const int t = (warp - 2) >> 2;
+    // ------------------------------------------------ softmax: row r, key half hf
+    const int hf = (warp - 2) >> 2;
     const int quarter = warp & 3;
     const int r = quarter * 32 + lane;
     const uint32_t lane_off = uint32_t(quarter * 32) << 16;
-    const int nt = t == 0 ? n0 : n1;
-    const int qrow = row0 + t * BM + r;
+    const uint32_t o_col = tmem + 256 + hf * 128 + lane_off;
     const float sl2 = prm.scale_log2;
     float m_used = -INFINITY, l = 0.f;
-    for (int j = 0; j < nt; ++j) {
-      mbar_wait(&ctl.s_full[t], j & 1);
+    for (int j = 0; j < n; ++j) {
+      const int b = j & 1;
+      const uint32_t s_col = tmem + b * 128 + hf * 64 + lane_off;
+      mbar_wait(&ctl.s_full[b], (j >> 1) & 1);
       tc_fence_after();
-      // pass 1: row max (S stays in TMEM; re-read in pass 2 — TMEM reads are
-      // cheap, registers are not: 10 warps cap the budget at 168/thread)
-      const bool diag = prm.causal && j == nt - 1;
+      const bool diag = prm.causal && j == n - 1;
+      float sv[64];
+      tmem_ld32(s_col, *reinterpret_cast<float(*)[32]>(&sv[0]));
+      tmem_ld32(s_col + 32, *reinterpret_cast<float(*)[32]>(&sv[32]));
+      tmem_wait_ld();
+      if (diag) {
+#pragma unroll
+        for (int x = 0; x < 64; ++x)
+          if (hf * 64 + x > r) sv[x] = -INFINITY;
+      }
       float mx = -INFINITY;
 #pragma unroll
-      for (int c = 0; c < BN / 32; ++c) {
-        float sv[32];
-        tmem_ld32(s_col(t) + lane_off + c * 32, sv);
-        tmem_wait_ld();
-#pragma unroll
-        for (int x = 0; x < 32; ++x) mx = fmaxf(mx, (diag && c * 32 + x > r) ? -INFINITY : sv[x]);
-      }
+      for (int x = 0; x < 64; ++x) mx = fmaxf(mx, sv[x]);
       const float cand = mx * sl2;
       const bool grow = cand > m_used + 8.0f;
       float corr = 1.f;
       if (grow) {
-        corr = fast_exp2(m_used - cand);
+        corr = fast_exp2(m_used - cand);  // 0 while m_used == -inf
         m_used = cand;
       }
       const float msub = m_used == -INFINITY ? 0.f : m_used;
-      // O_t is stable here (PV_t(j-1) completed before S_t(j)): lazy rescale in place
       if (j > 0 && __any_sync(0xffffffffu, grow)) {
+        mbar_wait(&ctl.o_ready, (j - 1) & 1);  // PV(j-1) complete: O stable
+        tc_fence_after();
 #pragma unroll
         for (int c = 0; c < D / 32; ++c) {
           float ov[32];
-          tmem_ld32(o_col(t) + lane_off + c * 32, ov);
+          tmem_ld32(o_col + c * 32, ov);
           tmem_wait_ld();
 #pragma unroll
           for (int x = 0; x < 32; ++x) ov[x] *= corr;
-          tmem_st32(o_col(t) + lane_off + c * 32, ov);
+          tmem_st32(o_col + c * 32, ov);
         }
       }
       float rs0 = 0.f, rs1 = 0.f;
 #pragma unroll
-      for (int h = 0; h < 4; ++h) {
-        float sv[32];
-        tmem_ld32(s_col(t) + lane_off + h * 32, sv);
-        tmem_wait_ld();
-        if (diag) {
-#pragma unroll
-          for (int x = 0; x < 32; ++x)
-            if (h * 32 + x > r) sv[x] = -INFINITY;
-        }
+      for (int h = 0; h < 2; ++h) {
         uint32_t pk[16];
 #pragma unroll
         for (int x = 0; x < 16; ++x) {
-          const float a = fast_exp2(fmaf(sv[2 * x], sl2, -msub));
-          const float xb = fmaf(sv[2 * x + 1], sl2, -msub);
-          // a share of the exponentials runs on the FMA pipe (MUFU is the
-          // other bottleneck of the tile next to the tensor core)
-          const float b = (kPolyEvery > 0 && x % (kPolyEvery > 0 ? kPolyEvery : 1) == 0) ? poly_exp2(xb) : fast_exp2(xb);
+          const float a = fast_exp2(fmaf(sv[h * 32 + 2 * x], sl2, -msub));
+          const float c = fast_exp2(fmaf(sv[h * 32 + 2 * x + 1], sl2, -msub));
           rs0 += a;
-          rs1 += b;
-          pk[x] = pack_bf16(a, b);
+          rs1 += c;
+          pk[x] = pack_bf16(a, c);
         }
-        tmem_st16(s_col(t) + lane_off + h * 16, pk);
+        tmem_st16(s_col + h * 16, pk);
       }
-      const float rs = rs0 + rs1;
-      l = l * corr + rs;
+      l = l * corr + (rs0 + rs1);
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(&ctl.p_full[t]);
+      mbar_arrive(&ctl.p_full[b]);
     }
-    // epilogue
-    const float inv = l > 0.f ? 1.f / l : 0.f;
-    __nv_bfloat16* orow = prm.o + int64_t(qrow) * prm.o_stride + head * D;
-    if (nt > 0) {
-      mbar_wait(&ctl.o_done[t], 0);
+    // ---------------- epilogue: merge the two halves (reference merge_partials)
+    ctl.m_half[hf][r] = m_used;
+    ctl.l_half[hf][r] = l;
+    if (n > 0) {
+      mbar_wait(&ctl.o_ready, (n - 1) & 1);
       tc_fence_after();
     }
+    named_bar_sync(1, kSoftmax);
+    const float ma = ctl.m_half[0][r], mb = ctl.m_half[1][r];
+    const float m = fmaxf(ma, mb);
+    const float wa = ma == -INFINITY ? 0.f : fast_exp2(ma - m);
+    const float wb = mb == -INFINITY ? 0.f : fast_exp2(mb - m);
+    const float lt = ctl.l_half[0][r] * wa + ctl.l_half[1][r] * wb;
+    const float inv = lt > 0.f ? 1.f / lt : 0.f;
+    const int qrow = row0 + r;
+    __nv_bfloat16* orow = prm.o + int64_t(qrow) * prm.o_stride + head * D + hf * 64;
 #pragma unroll
-    for (int c = 0; c < D / 32; ++c) {
-      float ov[32];
-      if (nt > 0) {
-        tmem_ld32(o_col(t) + lane_off + c * 32, ov);
+    for (int c = 0; c < 2; ++c) {  // this thread writes output columns [64hf + 32c, +32)
+      float oa[32], ob[32];
+      if (n > 0) {
+        tmem_ld32(tmem + 256 + lane_off + hf * 64 + c * 32, oa);
+        tmem_ld32(tmem + 384 + lane_off + hf * 64 + c * 32, ob);
         tmem_wait_ld();
       } else {
 #pragma unroll
-        for (int x = 0; x < 32; ++x) ov[x] = 0.f;
+        for (int x = 0; x < 32; ++x) oa[x] = ob[x] = 0.f;
       }
       uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
 #pragma unroll
-      for (int x = 0; x < 4; ++x)
-        dst[x] = make_uint4(pack_bf16(ov[8 * x] * inv, ov[8 * x + 1] * inv), pack_bf16(ov[8 * x + 2] * inv, ov[8 * x + 3] * inv),
-                            pack_bf16(ov[8 * x + 4] * inv, ov[8 * x + 5] * inv), pack_bf16(ov[8 * x + 6] * inv, ov[8 * x + 7] * inv));
+      for (int x = 0; x < 4; ++x) {
+        float y[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) y[e] = (oa[8 * x + e] * wa + ob[8 * x + e] * wb) * inv;
+        dst[x] = make_uint4(pack_bf16(y[0], y[1]), pack_bf16(y[2], y[3]), pack_bf16(y[4], y[5]), pack_bf16(y[6], y[7]));
+      }
     }
-    prm.lse[int64_t(head) * prm.q_rows + qrow] = l > 0.f ? (m_used + __log2f(l)) * 0.69314718055994530942f : -INFINITY;
+    if (hf == 0)
+      prm.lse[int64_t(head) * prm.q_rows + qrow] = lt > 0.f ? (m + __log2f(lt)) * 0.69314718055994530942f : -INFINITY;
     tc_fence_before();
   }
   __syncthreads();
@@ -342,11 +323,13 @@ int attn_fwd_d128(const void* q, int64_t q_rows, int64_t q_stride, const void* k
       !make_tmap_bf16(&tv, v_pool, uint64_t(kv_stride), uint64_t(pool_rows), uint64_t(kv_stride), BN))
     return set_error(SP_ERR_CUDA, "attn_fwd_d128: cuTensorMapEncodeTiled failed (alignment?)");
   const size_t smem = sizeof(Smem) + 1024;
-  static const int poly = getenv("SP_POLY") ? atoi(getenv("SP_POLY")) : 0;
-  auto kern = poly == 2 ? attn_fwd_d128_kernel<2> : poly == 4 ? attn_fwd_d128_kernel<4> : poly == 8 ? attn_fwd_d128_kernel<8> : attn_fwd_d128_kernel<0>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  if (e != cudaSuccess) return cuda_status(e, "attn_fwd_d128: set smem");
-  kern<<<dim3(unsigned(q_rows / (2 * BM)), heads), kThreads, smem, st>>>(tq, tk, tv, prm);
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(attn_fwd_d128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return cuda_status(e, "attn_fwd_d128: set smem");
+    configured = true;
+  }
+  attn_fwd_d128_kernel<<<dim3(unsigned(q_rows / BM), heads), kThreads, smem, st>>>(tq, tk, tv, prm);
   count_launch(1);
   return cuda_status(cudaGetLastError(), "attn_fwd_d128 launch");
 }
