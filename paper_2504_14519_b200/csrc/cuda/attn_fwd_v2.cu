@@ -26,6 +26,8 @@
 #include "kernels.hpp"
 #include "sm100.cuh"
 
+#include <cstdlib>
+
 namespace sp {
 namespace {
 
@@ -75,6 +77,22 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
       : "memory");
 }
 
+// 2^x on the FMA/ALU pipes: x = j + f (j = round(x), |f| <= 1/2), 2^f by a
+// degree-4 polynomial (rel. err < 5e-5, far below the bf16 rounding of P),
+// 2^j added into the exponent bits.  x is clamped at -126 (result ~0).
+__device__ __forceinline__ float poly_exp2(float x) {
+  x = fmaxf(x, -126.f);
+  const float t = x + 12582912.f;  // 1.5 * 2^23: round-to-nearest in the mantissa
+  const int j = __float_as_int(t) - 0x4B400000;
+  const float f = x - (t - 12582912.f);
+  float p = fmaf(0.0096181291f, f, 0.0555041087f);
+  p = fmaf(p, f, 0.2402264923f);
+  p = fmaf(p, f, 0.6931471806f);
+  p = fmaf(p, f, 1.0f);
+  return __int_as_float(__float_as_int(p) + (j << 23));
+}
+
+template <int kPoly>  // every kPoly-th pair computes its second exponential on the FMA pipe (0: never)
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_d128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                          const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ Params prm) {
@@ -242,7 +260,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int x = 0; x < 16; ++x) {
           const float a = fast_exp2(fmaf(sv[h * 32 + 2 * x], sl2, -msub));
-          const float c = fast_exp2(fmaf(sv[h * 32 + 2 * x + 1], sl2, -msub));
+          const float xc = fmaf(sv[h * 32 + 2 * x + 1], sl2, -msub);
+          const float c = (kPoly > 0 && x % (kPoly > 0 ? kPoly : 1) == 0) ? poly_exp2(xc) : fast_exp2(xc);
           rs0 += a;
           rs1 += c;
           pk[x] = pack_bf16(a, c);
@@ -323,13 +342,14 @@ int attn_fwd_d128(const void* q, int64_t q_rows, int64_t q_stride, const void* k
       !make_tmap_bf16(&tv, v_pool, uint64_t(kv_stride), uint64_t(pool_rows), uint64_t(kv_stride), BN))
     return set_error(SP_ERR_CUDA, "attn_fwd_d128: cuTensorMapEncodeTiled failed (alignment?)");
   const size_t smem = sizeof(Smem) + 1024;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(attn_fwd_d128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return cuda_status(e, "attn_fwd_d128: set smem");
-    configured = true;
-  }
-  attn_fwd_d128_kernel<<<dim3(unsigned(q_rows / BM), heads), kThreads, smem, st>>>(tq, tk, tv, prm);
+  static const int poly = getenv("SP_POLY") ? atoi(getenv("SP_POLY")) : 0;
+  auto kern = poly == 1   ? attn_fwd_d128_kernel<1>
+              : poly == 2 ? attn_fwd_d128_kernel<2>
+              : poly == 4 ? attn_fwd_d128_kernel<4>
+                          : attn_fwd_d128_kernel<0>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e != cudaSuccess) return cuda_status(e, "attn_fwd_d128: set smem");
+  kern<<<dim3(unsigned(q_rows / BM), heads), kThreads, smem, st>>>(tq, tk, tv, prm);
   count_launch(1);
   return cuda_status(cudaGetLastError(), "attn_fwd_d128 launch");
 }
