@@ -110,6 +110,17 @@ int sp_attn_bwd(const void* q, int64_t q_rows, int64_t q_stride, const void* k_p
                 const void* dout, int64_t do_stride, const float* lse, float* delta_ws, float* dq_acc,
                 float* dk_acc, float* dv_acc, int64_t acc_rows, const int32_t* acc_row, sp_stream_t stream);
 
+/* The two halves of sp_attn_bwd, for callers that ship the row statistics to
+ * a peer (workload redistribution): prep writes stats = [lse*log2e ; delta]
+ * (fp32 [2][heads][q_rows]); core consumes them (no O needed). */
+int sp_attn_bwd_prep(const void* o, int64_t o_stride, const void* dout, int64_t do_stride, const float* lse,
+                     int64_t q_rows, int heads, int head_dim, float* stats, sp_stream_t stream);
+int sp_attn_bwd_core(const void* q, int64_t q_rows, int64_t q_stride, const void* k_pool, const void* v_pool,
+                     int64_t pool_rows, int64_t kv_stride, const int32_t* chunk_row, int n_chunks, int chunk_len,
+                     int heads, int kv_heads, int head_dim, int causal, const void* dout, int64_t do_stride,
+                     const float* stats, float* dq_acc, float* dk_acc, float* dv_acc, int64_t acc_rows,
+                     const int32_t* acc_row, sp_stream_t stream);
+
 /* Online-softmax merge of two normalised partials over disjoint key sets
  * (reference merge_partials attention.cpp:63-82 followed by finalize :84-92):
  *   w_x = exp(lse_x - max), o = (w_a o_a + w_b o_b) / (w_a + w_b),
@@ -136,9 +147,15 @@ typedef struct {
 
 #define SP_STEP_NO_OPTIMIZER 1
 
+#define SP_NCCL_IDS 4
 int sp_nccl_unique_id(void* out128);
-/* nccl ids (128 bytes each, identical on all ranks) are ignored when pp == 1 */
-int sp_runtime_create(const sp_model_config* cfg, const void* nccl_id_fwd, const void* nccl_id_bwd, void** handle);
+/* nccl_ids: SP_NCCL_IDS consecutive 128-byte ids, identical on all ranks
+ * (stage activations, stage gradients, forward-tick exchange, backward-tick
+ * exchange); ignored when pp == 1.  exchange_mode: 0 off, 1 on, 2 early
+ * (reference ExchangeMode, simulator.hpp:18) — the per-tick plans of
+ * apply_exchange are executed: Q (+ KV chunks, dO and statistics in backward
+ * ticks) go to the receiving stage, which returns attention partials. */
+int sp_runtime_create(const sp_model_config* cfg, const void* nccl_ids, void** handle);
 int sp_runtime_destroy(void* handle);
 /* tokens/targets: [microbatches][seq_len] int32 (host, or device when on_device);
  * only stage 1 reads tokens and only the last stage reads targets (< 0 = ignore).
@@ -151,6 +168,9 @@ int sp_runtime_timeline(void* handle, double* out, int cap);
 int sp_runtime_attn_stats(void* handle, double* out6);
 int sp_runtime_memory(void* handle, int64_t* out7);
 int sp_runtime_param(void* handle, int layer, int which, float* host, int64_t count, int dir);
+/* {passes with outgoing transfers, passes with incoming transfers, bytes sent
+ *  by this rank through the exchange in the last step} */
+int sp_runtime_exchange_stats(void* handle, int64_t* out3);
 
 #ifdef __cplusplus
 }

@@ -381,13 +381,10 @@ int launch_bwd(const CUtensorMap& tq, const CUtensorMap& tdo, const CUtensorMap&
 }  // namespace
 }  // namespace sp
 
-extern "C" int sp_attn_bwd(const void* q, int64_t q_rows, int64_t q_stride, const void* k_pool, const void* v_pool,
-                           int64_t pool_rows, int64_t kv_stride, const int32_t* chunk_row, int n_chunks,
-                           int chunk_len, int heads, int kv_heads, int head_dim, int causal, const void* o,
-                           int64_t o_stride, const void* dout, int64_t do_stride, const float* lse, float* delta_ws,
-                           float* dq_acc, float* dk_acc, float* dv_acc, int64_t acc_rows, const int32_t* acc_row,
-                           sp_stream_t stream) {
-  using namespace sp;
+namespace sp {
+namespace {
+int bwd_check(int64_t q_rows, int n_chunks, int chunk_len, int heads, int kv_heads, int head_dim, int causal,
+              int64_t q_stride, int64_t kv_stride, int64_t do_stride) {
   if (head_dim != 64 && head_dim != 128)
     return set_error(SP_ERR_UNSUPPORTED, "sp_attn_bwd: head_dim %d not in {64,128}", head_dim);
   if (q_rows <= 0 || q_rows % 128 || chunk_len <= 0 || chunk_len % 128 || n_chunks <= 0 || n_chunks > SP_MAX_CHUNKS)
@@ -395,26 +392,48 @@ extern "C" int sp_attn_bwd(const void* q, int64_t q_rows, int64_t q_stride, cons
                      SP_MAX_CHUNKS);
   if (heads <= 0 || kv_heads <= 0 || heads % kv_heads)
     return set_error(SP_ERR_INVALID, "sp_attn_bwd: heads must be a multiple of kv_heads");
-  if (q_stride % 8 || kv_stride % 8 || o_stride % 8 || do_stride % 8)
+  if (q_stride % 8 || kv_stride % 8 || do_stride % 8)
     return set_error(SP_ERR_INVALID, "sp_attn_bwd: strides must be multiples of 8 elements");
-  const int64_t total_kv = int64_t(n_chunks) * chunk_len;
-  if (causal && total_kv < q_rows) return set_error(SP_ERR_UNSUPPORTED, "sp_attn_bwd: causal needs total_kv >= q_rows");
+  if (causal && int64_t(n_chunks) * chunk_len < q_rows)
+    return set_error(SP_ERR_UNSUPPORTED, "sp_attn_bwd: causal needs total_kv >= q_rows");
+  return SP_OK;
+}
+}  // namespace
+}  // namespace sp
+
+extern "C" int sp_attn_bwd_prep(const void* o, int64_t o_stride, const void* dout, int64_t do_stride, const float* lse,
+                                int64_t q_rows, int heads, int head_dim, float* stats, sp_stream_t stream) {
+  using namespace sp;
+  if (head_dim != 64 && head_dim != 128)
+    return set_error(SP_ERR_UNSUPPORTED, "sp_attn_bwd_prep: head_dim %d not in {64,128}", head_dim);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  float* lse2 = delta_ws;
-  float* delta = delta_ws + int64_t(heads) * q_rows;
-  {
-    const int64_t items = q_rows * heads;
-    const dim3 grid(unsigned((items + 7) / 8));
-    auto* O = static_cast<const __nv_bfloat16*>(o);
-    auto* dO = static_cast<const __nv_bfloat16*>(dout);
-    if (head_dim == 128)
-      attn_bwd_prep<128><<<grid, 256, 0, st>>>(O, o_stride, dO, do_stride, lse, q_rows, heads, lse2, delta);
-    else
-      attn_bwd_prep<64><<<grid, 256, 0, st>>>(O, o_stride, dO, do_stride, lse, q_rows, heads, lse2, delta);
-    count_launch(1);
-    int rc = cuda_status(cudaGetLastError(), "attn_bwd_prep launch");
-    if (rc) return rc;
-  }
+  float* lse2 = stats;
+  float* delta = stats + int64_t(heads) * q_rows;
+  const int64_t items = q_rows * heads;
+  const dim3 grid(unsigned((items + 7) / 8));
+  auto* O = static_cast<const __nv_bfloat16*>(o);
+  auto* dO = static_cast<const __nv_bfloat16*>(dout);
+  if (head_dim == 128)
+    attn_bwd_prep<128><<<grid, 256, 0, st>>>(O, o_stride, dO, do_stride, lse, q_rows, heads, lse2, delta);
+  else
+    attn_bwd_prep<64><<<grid, 256, 0, st>>>(O, o_stride, dO, do_stride, lse, q_rows, heads, lse2, delta);
+  count_launch(1);
+  return cuda_status(cudaGetLastError(), "attn_bwd_prep launch");
+}
+
+extern "C" int sp_attn_bwd_core(const void* q, int64_t q_rows, int64_t q_stride, const void* k_pool,
+                                const void* v_pool, int64_t pool_rows, int64_t kv_stride, const int32_t* chunk_row,
+                                int n_chunks, int chunk_len, int heads, int kv_heads, int head_dim, int causal,
+                                const void* dout, int64_t do_stride, const float* stats, float* dq_acc, float* dk_acc,
+                                float* dv_acc, int64_t acc_rows, const int32_t* acc_row, sp_stream_t stream) {
+  using namespace sp;
+  if (int rc = bwd_check(q_rows, n_chunks, chunk_len, heads, kv_heads, head_dim, causal, q_stride, kv_stride,
+                         do_stride))
+    return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const float* lse2 = stats;
+  const float* delta = stats + int64_t(heads) * q_rows;
+  const int64_t total_kv = int64_t(n_chunks) * chunk_len;
   for (int c = 0; c < n_chunks; ++c)
     if (chunk_row[c] < 0 || int64_t(chunk_row[c]) + chunk_len > pool_rows || acc_row[c] < 0 ||
         int64_t(acc_row[c]) + chunk_len > acc_rows)
@@ -441,9 +460,6 @@ extern "C" int sp_attn_bwd(const void* q, int64_t q_rows, int64_t q_stride, cons
   prm.dv = dv_acc;
   prm.acc_stride = int64_t(kv_heads) * head_dim;
   for (int c = 0; c < n_chunks; ++c) {
-    if (chunk_row[c] < 0 || int64_t(chunk_row[c]) + chunk_len > pool_rows || acc_row[c] < 0 ||
-        int64_t(acc_row[c]) + chunk_len > acc_rows)
-      return set_error(SP_ERR_INVALID, "sp_attn_bwd: chunk %d outside the pool/accumulator", c);
     prm.chunk_row[c] = chunk_row[c];
     prm.acc_row[c] = acc_row[c];
   }
@@ -456,4 +472,21 @@ extern "C" int sp_attn_bwd(const void* q, int64_t q_rows, int64_t q_stride, cons
   const int k_tiles = int(total_kv / 128);
   if (head_dim == 128) return launch_bwd<128>(tq, tdo, tk, tv, prm, k_tiles, kv_heads, st);
   return launch_bwd<64>(tq, tdo, tk, tv, prm, k_tiles, kv_heads, st);
+}
+
+extern "C" int sp_attn_bwd(const void* q, int64_t q_rows, int64_t q_stride, const void* k_pool, const void* v_pool,
+                           int64_t pool_rows, int64_t kv_stride, const int32_t* chunk_row, int n_chunks,
+                           int chunk_len, int heads, int kv_heads, int head_dim, int causal, const void* o,
+                           int64_t o_stride, const void* dout, int64_t do_stride, const float* lse, float* delta_ws,
+                           float* dq_acc, float* dk_acc, float* dv_acc, int64_t acc_rows, const int32_t* acc_row,
+                           sp_stream_t stream) {
+  using namespace sp;
+  if (int rc = bwd_check(q_rows, n_chunks, chunk_len, heads, kv_heads, head_dim, causal, q_stride, kv_stride,
+                         do_stride))
+    return rc;
+  if (o_stride % 8) return set_error(SP_ERR_INVALID, "sp_attn_bwd: strides must be multiples of 8 elements");
+  if (int rc = sp_attn_bwd_prep(o, o_stride, dout, do_stride, lse, q_rows, heads, head_dim, delta_ws, stream)) return rc;
+  return sp_attn_bwd_core(q, q_rows, q_stride, k_pool, v_pool, pool_rows, kv_stride, chunk_row, n_chunks, chunk_len,
+                          heads, kv_heads, head_dim, causal, dout, do_stride, delta_ws, dq_acc, dk_acc, dv_acc,
+                          acc_rows, acc_row, stream);
 }

@@ -33,6 +33,7 @@ int adamw(float* master, void* wbf, const float* g, float* m, float* v, int64_t 
 int init_params(float* master, void* wbf, int64_t n, uint64_t seed, float stdv, float constant, int use_const,
                 cudaStream_t st);
 int f32_to_bf16(const float* a, void* b, int64_t n, cudaStream_t st);
+int add_f32(float* dst, const float* src, int64_t n, cudaStream_t st);  // dst += src
 
 // attn_fwd_v2.cu — two-tile, P-in-TMEM d=128 forward (q_rows % 256 == 0)
 int attn_fwd_d128(const void* q, int64_t q_rows, int64_t q_stride, const void* k_pool, const void* v_pool,

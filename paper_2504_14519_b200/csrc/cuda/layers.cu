@@ -380,6 +380,18 @@ __global__ void f32_to_bf16_k(const float* __restrict__ a, bf16* __restrict__ b,
     b[i] = __float2bfloat16(a[i]);
 }
 
+__global__ void add_f32_k(float* __restrict__ d, const float* __restrict__ s, int64_t n4) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n4; i += int64_t(gridDim.x) * blockDim.x) {
+    float4 a = reinterpret_cast<float4*>(d)[i];
+    const float4 b = reinterpret_cast<const float4*>(s)[i];
+    a.x += b.x;
+    a.y += b.y;
+    a.z += b.z;
+    a.w += b.w;
+    reinterpret_cast<float4*>(d)[i] = a;
+  }
+}
+
 int grid_for(int64_t work, int block) {
   int64_t g = (work + block - 1) / block;
   return int(g < 148 * 32 ? (g > 0 ? g : 1) : 148 * 32);
@@ -469,6 +481,13 @@ int init_params(float* master, void* wbf, int64_t n, uint64_t seed, float stdv, 
   init_normal_k<<<grid_for(n, 256), 256, 0, st>>>(master, (bf16*)wbf, n, seed, stdv, constant, use_const);
   count_launch();
   return cuda_status(cudaGetLastError(), "init_params");
+}
+
+int add_f32(float* dst, const float* src, int64_t n, cudaStream_t st) {
+  if (n % 4) return set_error(SP_ERR_UNSUPPORTED, "add_f32: n %% 4");
+  add_f32_k<<<grid_for(n / 4, 256), 256, 0, st>>>(dst, src, n / 4);
+  count_launch(1);
+  return cuda_status(cudaGetLastError(), "add_f32");
 }
 
 int f32_to_bf16(const float* a, void* b, int64_t n, cudaStream_t st) {

@@ -119,6 +119,38 @@ class Runtime {
   int out_idx = 0, gin_idx = 0, gout_idx = 0;
   std::vector<PassTime> times;
   std::vector<AttnTimer> attn_times;
+
+  // ---- attention workload redistribution (reference exchange.cpp /
+  // simulator.cpp:56-108): per-pass transfer lists of this rank, two classes
+  // (0: forward ticks, 1: backward ticks) each with its own NCCL
+  // communicator, copy stream and high-priority remote-compute stream.
+  struct XOut {  // this rank ships Q (+ KV chunks) of its pass to `peer`
+    int peer;
+    std::vector<int> chunks;  // sender-microbatch chunk ids, 1-based, ascending
+    int base;                 // chunk offset in this rank's partial-receive pool
+  };
+  struct XIn {  // this rank computes a partial for `peer`'s pass
+    int peer, i_src;
+    std::vector<int> chunks;
+    int base;  // chunk offset in the receive pool
+  };
+  struct PassX {
+    int cls = 0;
+    std::vector<XOut> out;
+    std::vector<XIn> in;
+    int in_chunks = 0, out_chunks = 0;
+  };
+  std::map<int, PassX> xplan;
+  pipelab::ExchangeAnnotation ann;
+  ncclComm_t nc_x[2] = {nullptr, nullptr};
+  cudaStream_t cx[2] = {nullptr, nullptr}, rx[2] = {nullptr, nullptr};
+  int x_tout = 0, x_cout = 0, x_tin = 0, x_cin = 0;  // per-class maxima (both classes)
+  struct XBuf {
+    bf16raw *o_rem = nullptr, *rq = nullptr, *rdo = nullptr, *ro = nullptr, *rk = nullptr, *rv = nullptr;
+    float *lse_rem = nullptr, *dq_rem = nullptr, *dk_rem = nullptr, *dv_rem = nullptr;
+    float *rlse = nullptr, *rstats = nullptr, *rdq = nullptr, *rdk = nullptr, *rdv = nullptr;
+  } xb[2];
+  int64_t x_bytes_sent = 0;
   cudaEvent_t step_start = nullptr, step_end = nullptr;
   size_t bytes_allocated = 0;
   std::vector<void*> allocations;
@@ -128,6 +160,8 @@ class Runtime {
     for (void* a : allocations) cudaFree(a);
     if (nc_fwd) ncclCommDestroy(nc_fwd);
     if (nc_bwd) ncclCommDestroy(nc_bwd);
+    for (int c = 0; c < 2; ++c)
+      if (nc_x[c]) ncclCommDestroy(nc_x[c]);
     for (auto& t : times) {
       cudaEventDestroy(t.start);
       cudaEventDestroy(t.end);
@@ -152,7 +186,7 @@ class Runtime {
   bf16raw* W(int64_t off) { return w + off; }
   float* G(int64_t off) { return grad + off; }
 
-  int init(const sp_model_config& c, const void* id_fwd, const void* id_bwd) {
+  int init(const sp_model_config& c, const void* ids) {
     cfg = c;
     rank = c.rank;
     p = c.pp;
@@ -185,6 +219,13 @@ class Runtime {
     order = sched.device_order[rank];
     ledger = pipelab::ledger_from_order(sched, pipelab::unit_memory_model(p, 1, c.slices));
     slots = int(ledger.per_device[rank].chunk_pool_size);
+    if (c.exchange_mode != 0 && p > 1) {
+      if (c.head_dim != 128 && c.head_dim != 64) return set_error(SP_ERR_UNSUPPORTED, "exchange: head_dim");
+      pipelab::CostModel cm;
+      cm.beta_attn = 1.0;  // any beta > 0 gives the identical plan (plan depends on slice indices only)
+      ann = pipelab::apply_exchange(sched, cm, pipelab::ExchangeMode(c.exchange_mode));
+      build_xplan();
+    }
 
     SP_CUDA(cudaStreamCreateWithFlags(&comp, cudaStreamNonBlocking));
     SP_CUDA(cudaStreamCreateWithFlags(&cfwd, cudaStreamNonBlocking));
@@ -201,17 +242,218 @@ class Runtime {
     SP_CUDA(cudaEventCreate(&step_end));
 
     if (p > 1) {
-      ncclUniqueId a, b;
-      std::memcpy(&a, id_fwd, sizeof a);
-      std::memcpy(&b, id_bwd, sizeof b);
-      SP_NCCL(ncclCommInitRank(&nc_fwd, p, a, rank));
-      SP_NCCL(ncclCommInitRank(&nc_bwd, p, b, rank));
+      ncclUniqueId id[SP_NCCL_IDS];
+      std::memcpy(id, ids, sizeof id);
+      SP_NCCL(ncclCommInitRank(&nc_fwd, p, id[0], rank));
+      SP_NCCL(ncclCommInitRank(&nc_bwd, p, id[1], rank));
+      if (!xplan.empty() || c.exchange_mode != 0) {
+        int lo = 0, hi = 0;
+        SP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        for (int k = 0; k < 2; ++k) {
+          SP_NCCL(ncclCommInitRank(&nc_x[k], p, id[2 + k], rank));
+          SP_CUDA(cudaStreamCreateWithFlags(&cx[k], cudaStreamNonBlocking));
+          SP_CUDA(cudaStreamCreateWithPriority(&rx[k], cudaStreamNonBlocking, hi));
+        }
+      }
     }
     SP_TRY(alloc_params());
     SP_TRY(alloc_arena());
     SP_TRY(alloc_workspace());
+    SP_TRY(alloc_exchange());
     SP_TRY(init_weights(c.seed));
     SP_CUDA(cudaStreamSynchronize(comp));
+    return SP_OK;
+  }
+
+  // Per-pass transfer lists of this rank from the tick plans (transfers are
+  // sorted by (src, dst) in every plan, so both ends post their NCCL calls
+  // in the same order).
+  void build_xplan() {
+    const int me = rank + 1;
+    for (const pipelab::TickPlan& tp : ann.ticks) {
+      auto pass_of = [&](int dev) -> int {
+        for (std::size_t x = 0; x < tp.loads.size(); ++x)
+          if (tp.loads[x].device == dev) return tp.passes[x];
+        return -1;
+      };
+      for (const pipelab::Transfer& tr : tp.plan.transfers) {
+        const int sp = pass_of(tr.src), dp = pass_of(tr.dst);
+        if (sp < 0 || dp < 0) continue;
+        std::vector<int> ch(tr.kv_chunk_indices.begin(), tr.kv_chunk_indices.end());
+        if (tr.src == me) {
+          PassX& px = xplan[sp];
+          px.cls = tp.forward ? 0 : 1;
+          px.out.push_back({tr.dst - 1, ch, px.out_chunks});
+          px.out_chunks += int(ch.size());
+        }
+        if (tr.dst == me) {
+          PassX& px = xplan[dp];
+          px.cls = tp.forward ? 0 : 1;
+          px.in.push_back({tr.src - 1, sched.passes[sp].slice, ch, px.in_chunks});
+          px.in_chunks += int(ch.size());
+        }
+      }
+    }
+    for (const auto& [pid, px] : xplan) {
+      x_tout = std::max(x_tout, int(px.out.size()));
+      x_cout = std::max(x_cout, px.out_chunks);
+      x_tin = std::max(x_tin, int(px.in.size()));
+      x_cin = std::max(x_cin, px.in_chunks);
+    }
+  }
+
+  int alloc_exchange() {
+    if (xplan.empty()) return SP_OK;
+    const int64_t a = cfg.heads;
+    for (int c = 0; c < 2; ++c) {
+      XBuf& b = xb[c];
+      if (x_tout > 0) {
+        SP_TRY(alloc(&b.o_rem, x_tout * Ls * qd));
+        SP_TRY(alloc(&b.lse_rem, x_tout * a * Ls));
+        if (c == 1) {
+          SP_TRY(alloc(&b.dq_rem, x_tout * Ls * qd));
+          SP_TRY(alloc(&b.dk_rem, std::max(1, x_cout) * Ls * kvd));
+          SP_TRY(alloc(&b.dv_rem, std::max(1, x_cout) * Ls * kvd));
+        }
+      }
+      if (x_tin > 0) {
+        SP_TRY(alloc(&b.rq, x_tin * Ls * qd));
+        SP_TRY(alloc(&b.ro, x_tin * Ls * qd));
+        SP_TRY(alloc(&b.rlse, x_tin * a * Ls));
+        SP_TRY(alloc(&b.rk, std::max(1, x_cin) * Ls * kvd));
+        SP_TRY(alloc(&b.rv, std::max(1, x_cin) * Ls * kvd));
+        if (c == 1) {
+          SP_TRY(alloc(&b.rdo, x_tin * Ls * qd));
+          SP_TRY(alloc(&b.rstats, x_tin * 2 * a * Ls));
+          SP_TRY(alloc(&b.rdq, x_tin * Ls * qd));
+          SP_TRY(alloc(&b.rdk, std::max(1, x_cin) * Ls * kvd));
+          SP_TRY(alloc(&b.rdv, std::max(1, x_cin) * Ls * kvd));
+        }
+      }
+    }
+    return SP_OK;
+  }
+
+  const PassX* pass_x(int pid) const {
+    auto it = xplan.find(pid);
+    return it == xplan.end() ? nullptr : &it->second;
+  }
+
+  // Event from `from` stream that `to` waits on (created / destroyed here).
+  int link(cudaStream_t from, cudaStream_t to) {
+    cudaEvent_t e;
+    SP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    SP_CUDA(cudaEventRecord(e, from));
+    SP_CUDA(cudaStreamWaitEvent(to, e, 0));
+    cudaEventDestroy(e);
+    return SP_OK;
+  }
+
+  // K chunks then V chunks, one message per chunk (the sender ships them from
+  // their arena slots), landing contiguously at the transfer's pool rows.
+  int recv_chunks(bf16raw* rk, bf16raw* rv, const XIn& xi, int c) {
+    for (std::size_t x = 0; x < xi.chunks.size(); ++x)
+      SP_NCCL(ncclRecv(rk + int64_t(xi.base + x) * Ls * kvd, Ls * kvd, ncclBfloat16, xi.peer, nc_x[c], cx[c]));
+    for (std::size_t x = 0; x < xi.chunks.size(); ++x)
+      SP_NCCL(ncclRecv(rv + int64_t(xi.base + x) * Ls * kvd, Ls * kvd, ncclBfloat16, xi.peer, nc_x[c], cx[c]));
+    return SP_OK;
+  }
+  int send_chunks(int l, int k, const XOut& xo, int c) {
+    for (int ch : xo.chunks)
+      SP_NCCL(ncclSend(k_pool[l] + int64_t(slot_of.at({k, ch})) * Ls * kvd, Ls * kvd, ncclBfloat16, xo.peer, nc_x[c],
+                       cx[c]));
+    for (int ch : xo.chunks)
+      SP_NCCL(ncclSend(v_pool[l] + int64_t(slot_of.at({k, ch})) * Ls * kvd, Ls * kvd, ncclBfloat16, xo.peer, nc_x[c],
+                       cx[c]));
+    x_bytes_sent += 2 * int64_t(xo.chunks.size()) * Ls * kvd * 2;
+    return SP_OK;
+  }
+
+  // Chunks this pass attends itself: {1..i} minus every chunk shipped out;
+  // causal iff the diagonal chunk i stays (early plans never ship it,
+  // reference exchange.cpp:86-89).
+  void own_chunks(int k, int i, const PassX* px, std::vector<int32_t>& rows, std::vector<int32_t>& acc,
+                  int& causal) const {
+    std::vector<char> shipped(i + 1, 0);
+    if (px)
+      for (const XOut& xo : px->out)
+        for (int ch : xo.chunks) shipped[ch] = 1;
+    for (int j = 1; j <= i; ++j)
+      if (!shipped[j]) {
+        rows.push_back(int32_t(slot_of.at({k, j}) * Ls));
+        acc.push_back(int32_t((j - 1) * Ls));
+      }
+    causal = shipped[i] ? 0 : 1;
+  }
+
+  // ---- receiver side: every partial this rank computes for peers in pass px.
+  // Posted at pass start on the class's copy / remote-compute streams; per
+  // layer and transfer: recv (Q [, dO, stats], K/V chunks) -> attention
+  // partial -> send back.  Forward ticks: layers 0..L-1 (forward).  Backward
+  // ticks: layers 0..L-1 (the peer's recompute) then L-1..0 (its backward).
+  int post_remote(const PassX& px) {
+    const int c = px.cls;
+    XBuf& b = xb[c];
+    const int64_t a = cfg.heads;
+    auto fwd_layer = [&]() -> int {
+      for (std::size_t t = 0; t < px.in.size(); ++t) {
+        const XIn& xi = px.in[t];
+        const int nc = int(xi.chunks.size());
+        SP_NCCL(ncclGroupStart());
+        SP_NCCL(ncclRecv(b.rq + t * Ls * qd, Ls * qd, ncclBfloat16, xi.peer, nc_x[c], cx[c]));
+        SP_TRY(recv_chunks(b.rk, b.rv, xi, c));
+        SP_NCCL(ncclGroupEnd());
+        SP_TRY(link(cx[c], rx[c]));
+        std::vector<int32_t> rows;
+        for (int x = 0; x < nc; ++x) rows.push_back(int32_t((xi.base + x) * Ls));
+        const int causal = xi.chunks.back() == xi.i_src;
+        SP_TRY(sp_attn_fwd(b.rq + t * Ls * qd, Ls, qd, b.rk, b.rv, int64_t(std::max(1, x_cin)) * Ls, kvd, rows.data(),
+                           nc, int(Ls), cfg.heads, cfg.kv_heads, cfg.head_dim, causal, b.ro + t * Ls * qd, qd,
+                           b.rlse + t * a * Ls, rx[c]));
+        SP_TRY(link(rx[c], cx[c]));
+        SP_NCCL(ncclGroupStart());
+        SP_NCCL(ncclSend(b.ro + t * Ls * qd, Ls * qd, ncclBfloat16, xi.peer, nc_x[c], cx[c]));
+        SP_NCCL(ncclSend(b.rlse + t * a * Ls, a * Ls, ncclFloat32, xi.peer, nc_x[c], cx[c]));
+        SP_NCCL(ncclGroupEnd());
+      }
+      return SP_OK;
+    };
+    auto bwd_layer = [&]() -> int {
+      for (std::size_t t = 0; t < px.in.size(); ++t) {
+        const XIn& xi = px.in[t];
+        const int nc = int(xi.chunks.size());
+        SP_NCCL(ncclGroupStart());
+        SP_NCCL(ncclRecv(b.rq + t * Ls * qd, Ls * qd, ncclBfloat16, xi.peer, nc_x[c], cx[c]));
+        SP_NCCL(ncclRecv(b.rdo + t * Ls * qd, Ls * qd, ncclBfloat16, xi.peer, nc_x[c], cx[c]));
+        SP_NCCL(ncclRecv(b.rstats + t * 2 * a * Ls, 2 * a * Ls, ncclFloat32, xi.peer, nc_x[c], cx[c]));
+        SP_TRY(recv_chunks(b.rk, b.rv, xi, c));
+        SP_NCCL(ncclGroupEnd());
+        SP_TRY(link(cx[c], rx[c]));
+        std::vector<int32_t> rows;
+        for (int x = 0; x < nc; ++x) rows.push_back(int32_t((xi.base + x) * Ls));
+        const int causal = xi.chunks.back() == xi.i_src;
+        float* dq = b.rdq + t * Ls * qd;
+        float* dk = b.rdk + int64_t(xi.base) * Ls * kvd;
+        float* dv = b.rdv + int64_t(xi.base) * Ls * kvd;
+        SP_CUDA(cudaMemsetAsync(dq, 0, Ls * qd * 4, rx[c]));
+        SP_CUDA(cudaMemsetAsync(dk, 0, nc * Ls * kvd * 4, rx[c]));
+        SP_CUDA(cudaMemsetAsync(dv, 0, nc * Ls * kvd * 4, rx[c]));
+        SP_TRY(sp_attn_bwd_core(b.rq + t * Ls * qd, Ls, qd, b.rk, b.rv, int64_t(std::max(1, x_cin)) * Ls, kvd,
+                                rows.data(), nc, int(Ls), cfg.heads, cfg.kv_heads, cfg.head_dim, causal,
+                                b.rdo + t * Ls * qd, qd, b.rstats + t * 2 * a * Ls, dq, b.rdk, b.rdv,
+                                int64_t(std::max(1, x_cin)) * Ls, rows.data(), rx[c]));
+        SP_TRY(link(rx[c], cx[c]));
+        SP_NCCL(ncclGroupStart());
+        SP_NCCL(ncclSend(dq, Ls * qd, ncclFloat32, xi.peer, nc_x[c], cx[c]));
+        SP_NCCL(ncclSend(dk, nc * Ls * kvd, ncclFloat32, xi.peer, nc_x[c], cx[c]));
+        SP_NCCL(ncclSend(dv, nc * Ls * kvd, ncclFloat32, xi.peer, nc_x[c], cx[c]));
+        SP_NCCL(ncclGroupEnd());
+      }
+      return SP_OK;
+    };
+    for (int l = 0; l < Lps; ++l) SP_TRY(fwd_layer());
+    if (c == 1)
+      for (int l = Lps - 1; l >= 0; --l) SP_TRY(bwd_layer());
     return SP_OK;
   }
 
@@ -336,23 +578,64 @@ class Runtime {
     return rows;
   }
 
-  int attn_fwd_timed(int l, const std::vector<int32_t>& rows, LayerWs& x) {
+  double attn_flops(int n_chunks, int causal) const {  // forward FLOPs
+    const double keys = causal ? double(n_chunks - 1) * Ls + (Ls + 1) / 2.0 : double(n_chunks) * Ls;
+    return 4.0 * cfg.head_dim * double(Ls) * keys * cfg.heads;
+  }
+
+  int attn_fwd_timed(int l, const std::vector<int32_t>& rows, int causal, LayerWs& x) {
     AttnTimer t{};
     SP_CUDA(cudaEventCreate(&t.a));
     SP_CUDA(cudaEventCreate(&t.b));
-    const int i = int(rows.size());
-    t.flops = 4.0 * cfg.head_dim * double(Ls) * (double(i - 1) * Ls + (Ls + 1) / 2.0) * cfg.heads;
+    const int nch = int(rows.size());
+    t.flops = attn_flops(nch, causal);
     t.kind = 0;
     SP_CUDA(cudaEventRecord(t.a, comp));
-    SP_TRY(sp_attn_fwd(x.q, Ls, qd, k_pool[l], v_pool[l], int64_t(slots) * Ls, kvd, rows.data(), i, int(Ls),
-                       cfg.heads, cfg.kv_heads, cfg.head_dim, 1, x.o, qd, x.lse, comp));
+    SP_TRY(sp_attn_fwd(x.q, Ls, qd, k_pool[l], v_pool[l], int64_t(slots) * Ls, kvd, rows.data(), nch, int(Ls),
+                       cfg.heads, cfg.kv_heads, cfg.head_dim, causal, x.o, qd, x.lse, comp));
     SP_CUDA(cudaEventRecord(t.b, comp));
     attn_times.push_back(t);
     return SP_OK;
   }
 
   // One layer forward; saves its internals in ws[l]; writes its output to x_out.
-  int layer_forward(int l, int k, int i, const std::vector<int32_t>& rows, bf16raw* x_out) {
+  // K1 with the pass's transfers: ship Q (+ KV chunks) to each receiver,
+  // attend the retained chunks, merge every returned (O, LSE) partial (K3).
+  int attention_forward(int l, int k, int i, LayerWs& x, const PassX* px) {
+    std::vector<int32_t> rows, acc;
+    int causal = 1;
+    own_chunks(k, i, px, rows, acc, causal);
+    const bool out = px && !px->out.empty();
+    const int c = px ? px->cls : 0;
+    const int64_t a = cfg.heads;
+    if (out) {
+      SP_TRY(link(comp, cx[c]));
+      for (const XOut& xo : px->out) {
+        SP_NCCL(ncclGroupStart());
+        SP_NCCL(ncclSend(x.q, Ls * qd, ncclBfloat16, xo.peer, nc_x[c], cx[c]));
+        SP_TRY(send_chunks(l, k, xo, c));
+        SP_NCCL(ncclGroupEnd());
+        x_bytes_sent += Ls * qd * 2;
+      }
+    }
+    SP_TRY(attn_fwd_timed(l, rows, causal, x));
+    if (out) {
+      XBuf& b = xb[c];
+      for (std::size_t t = 0; t < px->out.size(); ++t) {
+        SP_NCCL(ncclGroupStart());
+        SP_NCCL(ncclRecv(b.o_rem + t * Ls * qd, Ls * qd, ncclBfloat16, px->out[t].peer, nc_x[c], cx[c]));
+        SP_NCCL(ncclRecv(b.lse_rem + t * a * Ls, a * Ls, ncclFloat32, px->out[t].peer, nc_x[c], cx[c]));
+        SP_NCCL(ncclGroupEnd());
+      }
+      SP_TRY(link(cx[c], comp));
+      for (std::size_t t = 0; t < px->out.size(); ++t)
+        SP_TRY(sp_attn_merge(x.o, x.lse, b.o_rem + t * Ls * qd, b.lse_rem + t * a * Ls, Ls, cfg.heads, cfg.head_dim, qd,
+                             x.o, x.lse, comp));
+    }
+    return SP_OK;
+  }
+
+  int layer_forward(int l, int k, int i, bf16raw* x_out, const PassX* px) {
     LayerWs& x = ws[l];
     const LayerParams& P = lp[l];
     const int slot = slot_of.at({k, i});
@@ -361,7 +644,7 @@ class Runtime {
     SP_TRY(gemm(false, true, Ls, qkv_w, h, x.xn, h, W(P.wqkv), h, qkv, qkv_w, false, 1.f, 0.f, comp));
     SP_TRY(rope_qkv_fwd(qkv, Ls, cfg.heads, cfg.kv_heads, cfg.head_dim, pos0, cfg.rope_theta, x.q, qd,
                         k_pool[l] + int64_t(slot) * Ls * kvd, v_pool[l] + int64_t(slot) * Ls * kvd, kvd, comp));
-    SP_TRY(attn_fwd_timed(l, rows, x));
+    SP_TRY(attention_forward(l, k, i, x, px));
     SP_CUDA(cudaMemcpyAsync(x.x_mid, x.x_in, Ls * h * 2, cudaMemcpyDeviceToDevice, comp));
     SP_TRY(gemm(false, true, Ls, h, qd, x.o, qd, W(P.wo), qd, x.x_mid, h, false, 1.f, 1.f, comp));
     SP_TRY(rmsnorm_fwd(x.x_mid, W(P.mlp_norm), x.xn2, x.rstd2, Ls, int(h), cfg.norm_eps, comp));
@@ -373,13 +656,14 @@ class Runtime {
   }
 
   // Stage forward of slice (k,i) from ws[0].x_in; final output to `out`.
-  int stage_forward(int k, int i, bf16raw* out) {
-    const std::vector<int32_t> rows = chunk_rows(k, i);
-    for (int l = 0; l < Lps; ++l) SP_TRY(layer_forward(l, k, i, rows, l + 1 < Lps ? ws[l + 1].x_in : out));
+  int stage_forward(int k, int i, bf16raw* out, const PassX* px) {
+    for (int l = 0; l < Lps; ++l) SP_TRY(layer_forward(l, k, i, l + 1 < Lps ? ws[l + 1].x_in : out, px));
     return SP_OK;
   }
 
-  int run_forward(int k, int i, cudaEvent_t t0) {
+  int run_forward(int pid, int k, int i, cudaEvent_t t0) {
+    const PassX* px = pass_x(pid);
+    if (px && !px->in.empty()) SP_TRY(post_remote(*px));
     if (free_slots.empty()) return set_error(SP_ERR_RUNTIME, "arena exhausted (ledger/schedule mismatch)");
     const int slot = free_slots.back();
     free_slots.pop_back();
@@ -408,7 +692,7 @@ class Runtime {
       const int b = out_idx;
       out_idx ^= 1;
       SP_CUDA(cudaStreamWaitEvent(comp, ev_out_free[b], 0));
-      SP_TRY(stage_forward(k, i, out_buf[b]));
+      SP_TRY(stage_forward(k, i, out_buf[b], px));
       cudaEvent_t done;
       SP_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
       SP_CUDA(cudaEventRecord(done, comp));
@@ -417,12 +701,12 @@ class Runtime {
       SP_CUDA(cudaEventRecord(ev_out_free[b], cfwd));
       cudaEventDestroy(done);
     } else {
-      SP_TRY(stage_forward(k, i, x_final));
+      SP_TRY(stage_forward(k, i, x_final, px));
     }
     return SP_OK;
   }
 
-  int layer_backward(int l, int k, int i, const std::vector<int32_t>& rows, bf16raw* dx) {
+  int layer_backward(int l, int k, int i, bf16raw* dx, const PassX* px) {
     LayerWs& x = ws[l];
     const LayerParams& P = lp[l];
     const int64_t pos0 = int64_t(i - 1) * Ls;
@@ -436,21 +720,61 @@ class Runtime {
     // attention output projection
     SP_TRY(gemm(false, false, Ls, qd, h, dx, h, W(P.wo), qd, tmp_h, qd, false, 1.f, 0.f, comp));   // d_o
     SP_TRY(gemm(true, false, h, qd, Ls, dx, h, x.o, qd, G(P.wo), qd, true, 1.f, 1.f, comp));         // dWo
-    // K2: sliced attention backward
+    // K2: sliced attention backward (+ the pass's transfers: the receiver
+    // returns dQ and dK/dV partials of the shipped chunks, added here)
     SP_CUDA(cudaMemsetAsync(dq_acc, 0, Ls * qd * 4, comp));
-    std::vector<int32_t> acc_rows;
-    for (int j = 1; j <= i; ++j) acc_rows.push_back(int32_t((j - 1) * Ls));
+    std::vector<int32_t> rows, acc_rows;
+    int causal = 1;
+    own_chunks(k, i, px, rows, acc_rows, causal);
+    const bool out = px && !px->out.empty();
+    const int c = px ? px->cls : 1;
+    const int64_t a = cfg.heads;
+    SP_TRY(sp_attn_bwd_prep(x.o, qd, tmp_h, qd, x.lse, Ls, cfg.heads, cfg.head_dim, delta_ws, comp));
+    if (out) {
+      SP_TRY(link(comp, cx[c]));
+      for (const XOut& xo : px->out) {
+        SP_NCCL(ncclGroupStart());
+        SP_NCCL(ncclSend(x.q, Ls * qd, ncclBfloat16, xo.peer, nc_x[c], cx[c]));
+        SP_NCCL(ncclSend(tmp_h, Ls * qd, ncclBfloat16, xo.peer, nc_x[c], cx[c]));
+        SP_NCCL(ncclSend(delta_ws, 2 * a * Ls, ncclFloat32, xo.peer, nc_x[c], cx[c]));
+        SP_TRY(send_chunks(l, k, xo, c));
+        SP_NCCL(ncclGroupEnd());
+        x_bytes_sent += 2 * Ls * qd * 2 + 2 * a * Ls * 4;
+      }
+    }
     AttnTimer t{};
     SP_CUDA(cudaEventCreate(&t.a));
     SP_CUDA(cudaEventCreate(&t.b));
-    t.flops = 2.5 * 4.0 * cfg.head_dim * double(Ls) * (double(i - 1) * Ls + (Ls + 1) / 2.0) * cfg.heads;
+    t.flops = 2.5 * attn_flops(int(rows.size()), causal);
     t.kind = 1;
     SP_CUDA(cudaEventRecord(t.a, comp));
-    SP_TRY(sp_attn_bwd(x.q, Ls, qd, k_pool[l], v_pool[l], int64_t(slots) * Ls, kvd, rows.data(), i, int(Ls), cfg.heads,
-                       cfg.kv_heads, cfg.head_dim, 1, x.o, qd, tmp_h, qd, x.lse, delta_ws, dq_acc, dk_acc[l],
-                       dv_acc[l], int64_t(cfg.slices) * Ls, acc_rows.data(), comp));
+    SP_TRY(sp_attn_bwd_core(x.q, Ls, qd, k_pool[l], v_pool[l], int64_t(slots) * Ls, kvd, rows.data(), int(rows.size()),
+                            int(Ls), cfg.heads, cfg.kv_heads, cfg.head_dim, causal, tmp_h, qd, delta_ws, dq_acc,
+                            dk_acc[l], dv_acc[l], int64_t(cfg.slices) * Ls, acc_rows.data(), comp));
     SP_CUDA(cudaEventRecord(t.b, comp));
     attn_times.push_back(t);
+    if (out) {
+      XBuf& b = xb[c];
+      for (std::size_t tt = 0; tt < px->out.size(); ++tt) {
+        const XOut& xo = px->out[tt];
+        const int64_t nc = int64_t(xo.chunks.size());
+        SP_NCCL(ncclGroupStart());
+        SP_NCCL(ncclRecv(b.dq_rem + tt * Ls * qd, Ls * qd, ncclFloat32, xo.peer, nc_x[c], cx[c]));
+        SP_NCCL(ncclRecv(b.dk_rem + int64_t(xo.base) * Ls * kvd, nc * Ls * kvd, ncclFloat32, xo.peer, nc_x[c], cx[c]));
+        SP_NCCL(ncclRecv(b.dv_rem + int64_t(xo.base) * Ls * kvd, nc * Ls * kvd, ncclFloat32, xo.peer, nc_x[c], cx[c]));
+        SP_NCCL(ncclGroupEnd());
+      }
+      SP_TRY(link(cx[c], comp));
+      for (std::size_t tt = 0; tt < px->out.size(); ++tt) {
+        const XOut& xo = px->out[tt];
+        SP_TRY(add_f32(dq_acc, b.dq_rem + tt * Ls * qd, Ls * qd, comp));
+        for (std::size_t x2 = 0; x2 < xo.chunks.size(); ++x2) {
+          const int64_t dst = int64_t(xo.chunks[x2] - 1) * Ls * kvd, src = int64_t(xo.base + x2) * Ls * kvd;
+          SP_TRY(add_f32(dk_acc[l] + dst, b.dk_rem + src, Ls * kvd, comp));
+          SP_TRY(add_f32(dv_acc[l] + dst, b.dv_rem + src, Ls * kvd, comp));
+        }
+      }
+    }
     // chunk i's dK/dV is complete: RoPE backward into d_qkv and reset the rows
     SP_TRY(rope_qkv_bwd(dq_acc, dk_acc[l] + pos0 * kvd, dv_acc[l] + pos0 * kvd, kvd, Ls, cfg.heads, cfg.kv_heads,
                         cfg.head_dim, pos0, cfg.rope_theta, dqkv, 1, comp));
@@ -460,7 +784,9 @@ class Runtime {
     return SP_OK;
   }
 
-  int run_backward(int k, int i, cudaEvent_t t0) {
+  int run_backward(int pid, int k, int i, cudaEvent_t t0) {
+    const PassX* px = pass_x(pid);
+    if (px && !px->in.empty()) SP_TRY(post_remote(*px));
     const int slot = slot_of.at({k, i});
     bf16raw* xs = x_pool + int64_t(slot) * Ls * h;
     const int64_t tok0 = int64_t(k - 1) * cfg.seq_len + int64_t(i - 1) * Ls;
@@ -488,7 +814,7 @@ class Runtime {
     bf16raw* top = stage < p ? tmp_h : x_final;
     if (stage == p) {
       SP_CUDA(cudaStreamWaitEvent(comp, ev_gout_free[gout_idx], 0));
-      SP_TRY(stage_forward(k, i, x_final));
+      SP_TRY(stage_forward(k, i, x_final, px));
       // LM head + cross entropy
       const int64_t V = cfg.vocab;
       SP_TRY(rmsnorm_fwd(x_final, W(final_norm), xf, rstd_f, Ls, int(h), cfg.norm_eps, comp));
@@ -499,10 +825,9 @@ class Runtime {
       SP_TRY(gemm(true, false, V, h, Ls, dlogits, V, xf, h, G(head), h, true, 1.f, 1.f, comp));        // dWhead
       SP_TRY(rmsnorm_bwd(tmp_h, x_final, W(final_norm), rstd_f, nullptr, dx, G(final_norm), Ls, int(h), comp));
     } else {
-      SP_TRY(stage_forward(k, i, top));
+      SP_TRY(stage_forward(k, i, top, px));
     }
-    const std::vector<int32_t> rows = chunk_rows(k, i);
-    for (int l = Lps - 1; l >= 0; --l) SP_TRY(layer_backward(l, k, i, rows, dx));
+    for (int l = Lps - 1; l >= 0; --l) SP_TRY(layer_backward(l, k, i, dx, px));
     if (stage == 1) {
       SP_TRY(embed_bwd(tokens + tok0, dx, G(emb), Ls, int(h), comp));
       if (gb >= 0) SP_CUDA(cudaEventRecord(ev_gin_free[gb], comp));
@@ -538,6 +863,7 @@ class Runtime {
     }
     attn_times.clear();
     slots_high_water = 0;
+    x_bytes_sent = 0;
     const int64_t ntok = int64_t(cfg.microbatches) * cfg.seq_len;
     SP_CUDA(cudaEventRecord(step_start, comp));
     const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
@@ -549,8 +875,8 @@ class Runtime {
       PassTime t{id, nullptr, nullptr};
       SP_CUDA(cudaEventCreate(&t.start));
       SP_CUDA(cudaEventCreate(&t.end));
-      if (ps.kind == pipelab::PassKind::Forward) SP_TRY(run_forward(ps.microbatch, ps.slice, t.start));
-      else SP_TRY(run_backward(ps.microbatch, ps.slice, t.start));
+      if (ps.kind == pipelab::PassKind::Forward) SP_TRY(run_forward(id, ps.microbatch, ps.slice, t.start));
+      else SP_TRY(run_backward(id, ps.microbatch, ps.slice, t.start));
       SP_CUDA(cudaEventRecord(t.end, comp));
       times.push_back(t);
     }
@@ -567,6 +893,11 @@ class Runtime {
     SP_CUDA(cudaEventRecord(e2, cbwd));
     SP_CUDA(cudaStreamWaitEvent(comp, e1, 0));
     SP_CUDA(cudaStreamWaitEvent(comp, e2, 0));
+    for (int c = 0; c < 2; ++c)
+      if (cx[c]) {
+        SP_TRY(link(cx[c], comp));
+        SP_TRY(link(rx[c], comp));
+      }
     cudaEventDestroy(e1);
     cudaEventDestroy(e2);
     SP_CUDA(cudaEventRecord(step_end, comp));
@@ -595,9 +926,9 @@ int sp_nccl_unique_id(void* out128) {
   return SP_OK;
 }
 
-int sp_runtime_create(const sp_model_config* cfg, const void* nccl_id_fwd, const void* nccl_id_bwd, void** handle) {
+int sp_runtime_create(const sp_model_config* cfg, const void* nccl_ids, void** handle) {
   auto rt = std::make_unique<Runtime>();
-  const int rc = rt->init(*cfg, nccl_id_fwd, nccl_id_bwd);
+  const int rc = rt->init(*cfg, nccl_ids);
   if (rc != SP_OK) return rc;
   *handle = rt.release();
   return SP_OK;
@@ -654,6 +985,19 @@ int sp_runtime_attn_stats(void* handle, double* out6) {
     out6[3 * t.kind + 1] += t.flops;
     out6[3 * t.kind + 2] += 1;
   }
+  return SP_OK;
+}
+
+int sp_runtime_exchange_stats(void* handle, int64_t* out3) {
+  Runtime* rt = static_cast<Runtime*>(handle);
+  int64_t o = 0, i = 0;
+  for (const auto& kv : rt->xplan) {
+    o += kv.second.out.empty() ? 0 : 1;
+    i += kv.second.in.empty() ? 0 : 1;
+  }
+  out3[0] = o;
+  out3[1] = i;
+  out3[2] = rt->x_bytes_sent;
   return SP_OK;
 }
 

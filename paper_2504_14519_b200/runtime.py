@@ -98,7 +98,8 @@ _PARAM_NAMES = ["attn_norm", "wqkv", "wo", "mlp_norm", "wgu", "wd", "embedding",
 def _lib():
     lib = N.lib()
     lib.sp_nccl_unique_id.argtypes = [C.c_void_p]
-    lib.sp_runtime_create.argtypes = [C.POINTER(_Cfg), C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]
+    lib.sp_runtime_create.argtypes = [C.POINTER(_Cfg), C.c_void_p, C.POINTER(C.c_void_p)]
+    lib.sp_runtime_exchange_stats.argtypes = [C.c_void_p, C.POINTER(C.c_int64)]
     lib.sp_runtime_destroy.argtypes = [C.c_void_p]
     lib.sp_runtime_step.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_float)]
     lib.sp_runtime_sync.argtypes = [C.c_void_p]
@@ -111,20 +112,27 @@ def _lib():
     return lib
 
 
+N_NCCL_IDS = 4  # stage fwd, stage bwd, fwd-tick exchange, bwd-tick exchange
+
+
+def make_nccl_ids() -> bytes:
+    out = b""
+    for _ in range(N_NCCL_IDS):
+        buf = C.create_string_buffer(128)
+        N.check(_lib().sp_nccl_unique_id(buf), "sp_nccl_unique_id")
+        out += buf.raw
+    return out
+
+
 def nccl_ids(rank: int, world: int):
-    """Two NCCL unique ids (fwd / bwd communicators) made on rank 0 and
-    broadcast with torch.distributed (which must be initialised when world > 1)."""
+    """The executor's NCCL unique ids, made on rank 0 and broadcast with
+    torch.distributed (which must be initialised when world > 1)."""
     if world == 1:
-        return None, None
+        return None
     import torch.distributed as dist
-    ids = [None, None]
-    if rank == 0:
-        a, b = C.create_string_buffer(128), C.create_string_buffer(128)
-        N.check(_lib().sp_nccl_unique_id(a), "sp_nccl_unique_id")
-        N.check(_lib().sp_nccl_unique_id(b), "sp_nccl_unique_id")
-        ids = [a.raw, b.raw]
+    ids = [make_nccl_ids() if rank == 0 else None]
     dist.broadcast_object_list(ids, src=0)
-    return C.create_string_buffer(ids[0], 128), C.create_string_buffer(ids[1], 128)
+    return C.create_string_buffer(ids[0], 128 * N_NCCL_IDS)
 
 
 class SlimPipeStep:
@@ -137,10 +145,10 @@ class SlimPipeStep:
         if cfg.pp != self.world:
             raise ValueError(f"pp ({cfg.pp}) must equal the number of ranks ({self.world})")
         lib = _lib()
-        ida, idb = nccl_ids(self.rank, self.world)
+        ids = nccl_ids(self.rank, self.world)
         h = C.c_void_p()
         c = cfg.to_c(self.rank)
-        N.check(lib.sp_runtime_create(C.byref(c), ida, idb, C.byref(h)), "sp_runtime_create")
+        N.check(lib.sp_runtime_create(C.byref(c), ids, C.byref(h)), "sp_runtime_create")
         self._h = h
         self.stage = self.rank + 1
         self.is_first = self.stage == 1
@@ -208,6 +216,11 @@ class SlimPipeStep:
         keys = ["slots", "slots_high_water", "slot_bytes", "ledger_peak_units", "bytes_allocated", "n_params",
                 "layers_per_stage"]
         return dict(zip(keys, list(b)))
+
+    def exchange_stats(self) -> dict:
+        b = (C.c_int64 * 3)()
+        N.check(_lib().sp_runtime_exchange_stats(self._h, b), "sp_runtime_exchange_stats")
+        return {"passes_out": b[0], "passes_in": b[1], "bytes_sent": b[2]}
 
     # ---- parameter access (tests) ----
     def _param_shape(self, which: str):

@@ -29,7 +29,9 @@ def main():
     from paper_2504_14519_b200.runtime import SlimPipeStep, StepConfig
     m = int(os.environ.get("SP_M", 2))
     n = int(os.environ.get("SP_N", 4))
-    cfg = StepConfig.c1(pp=world, microbatches=m, slices=n, layers=2 * world)
+    xmode = os.environ.get("SP_X", "off")
+    cfg = StepConfig.c1(pp=world, microbatches=m, slices=n, layers=2 * world, exchange=xmode,
+                        seq_len=1024 * n)
     step = SlimPipeStep(cfg, rank, world)
     rng = np.random.default_rng(0)
     tok = rng.integers(0, cfg.vocab, (cfg.microbatches, cfg.seq_len), dtype=np.int32)
@@ -51,6 +53,7 @@ def main():
             mine["grads"][(None, k)] = step.get_grad(0, k)
     mem = step.memory()
     mine["mem"] = mem
+    mine["x"] = step.exchange_stats()
     allv = [None] * world
     dist.all_gather_object(allv, mine)
     ok = True
@@ -66,7 +69,11 @@ def main():
             W[k] = rnd(P[(None, k)])
         ref_loss, ref_g = MO.Model(W, cfg.heads, cfg.kv_heads, cfg.rope_theta, cfg.norm_eps).step(tok, tgt, n)
         gpu_loss = allv[-1]["loss"]
-        print(f"pp={world} m={m} n={n} loss gpu {gpu_loss:.6f} oracle {ref_loss:.6f}")
+        print(f"pp={world} m={m} n={n} exchange={xmode} loss gpu {gpu_loss:.6f} oracle {ref_loss:.6f}")
+        xs = [d["x"] for d in allv]
+        print("exchange stats per rank:", xs)
+        if xmode != "off":
+            ok &= sum(x["passes_out"] for x in xs) > 0 and sum(x["bytes_sent"] for x in xs) > 0
         ok &= abs(gpu_loss - ref_loss) / abs(ref_loss) < 1e-2
         worst = 0.0
         for (l, k), g in G.items():
