@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--seq-len", type=int, default=131072)
     ap.add_argument("--slices", type=int, default=8)
     ap.add_argument("--microbatches", type=int, default=4)
+    ap.add_argument("--exchange", choices=["off", "on", "early"], default="early",
+                    help="attention workload redistribution (reference ExchangeMode); no effect at PP=1")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -68,12 +70,12 @@ def parse():
 def make_cfg(args, world):
     from paper_2504_14519_b200.runtime import StepConfig
     return StepConfig.c2(layers=args.layers, seq_len=args.seq_len, slices=args.slices,
-                         microbatches=args.microbatches, pp=world)
+                         microbatches=args.microbatches, pp=world, exchange=args.exchange)
 
 
 def workload_name(cfg):
     return (f"c2 Llama-7B layer shapes x{cfg.layers} layers, {cfg.seq_len // 1024}K ctx, n={cfg.slices} slices, "
-            f"m={cfg.microbatches}, PP={cfg.pp}")
+            f"m={cfg.microbatches}, PP={cfg.pp}, exchange={cfg.exchange}")
 
 
 # ----------------------------------------------------------------- clocks
