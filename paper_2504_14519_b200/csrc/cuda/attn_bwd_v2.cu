@@ -6,7 +6,10 @@
 //   * TMEM holds TWO (S^T, dP^T) buffers (2 x 128 cols) + dV (128) + dK (128);
 //     the MMA warp issues S/dP of pair j+1 before dV/dK/dQ of pair j, so the
 //     element math of pair j+1 overlaps the accumulation MMAs of pair j.
-//   * dQ^T of pair j is written into pair j's (now consumed) S^T columns.
+//   * P^T and dS^T go back into TMEM (packed bf16 over the consumed S^T
+//     columns): dV += P^T dO and dK += dS^T Q are TS-UMMAs (A from TMEM),
+//     which keeps their A operands out of the shared-memory bandwidth this
+//     kernel is bound by; dQ^T of pair j lands in its consumed dP^T columns.
 //   * two compute warpgroups (8 warps) split every pair's 64 query columns;
 //   * dQ leaves through TMA bulk reduce-add (cp.reduce.async.bulk.tensor
 //     .add.f32) from a double-buffered smem stage instead of per-thread
@@ -37,6 +40,7 @@ struct Params {
   float* dv;
   int64_t acc_stride;
   int trace;  // record a per-pair timeline of CTA (0,0) into g_bwd_trace
+  int dbg;    // diagnostics only: bit0 skip the dQ stage/reduce, bit1 skip the dQ MMA
   int chunk_row[SP_MAX_CHUNKS];
   int acc_row[SP_MAX_CHUNKS];
 };
@@ -46,7 +50,6 @@ struct alignas(1024) Smem {
   __nv_bfloat16 v[BK * D];
   __nv_bfloat16 q[NS][BQ * D];
   __nv_bfloat16 dout[NS][BQ * D];
-  __nv_bfloat16 p[BK * BQ];
   __nv_bfloat16 ds[BK * BQ];
   float stage[1][BQ * D];  // dQ tile [q][d] on their way to the TMA reduce
 };
@@ -59,7 +62,7 @@ struct Ctl {  // static shared memory: statistics and barriers
   uint32_t tmem_base;
 };
 
-__device__ long long g_bwd_trace[10][512];
+__device__ long long g_bwd_trace[12][512];
 #define TR(e, j)                                                                        \
   do {                                                                                 \
     if (tracing && (j) < 512) g_bwd_trace[e][(j)] = clock64();                        \
@@ -149,11 +152,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr uint32_t id_s = idesc_bf16_f32(BK, BQ, false, false);  // K Q^T, V dO^T
       constexpr uint32_t id_acc = idesc_bf16_f32(BK, D, false, true);  // P^T dO, dS^T Q
       constexpr uint32_t id_dq = idesc_bf16_f32(D, BQ, true, true);    // K^T dS^T
-      const uint32_t k_a = smem_u32(sm.k), v_a = smem_u32(sm.v), p_a = smem_u32(sm.p), ds_a = smem_u32(sm.ds);
+      const uint32_t k_a = smem_u32(sm.k), v_a = smem_u32(sm.v), ds_a = smem_u32(sm.ds);
       auto issue_sdp = [&](int j) {
         const int s = j % NS, b = j & 1;
         mbar_wait(&ctl.q_full[s], (j / NS) & 1);
+        if (j >= 1) TR(10, j - 1);
         if (j >= 2) mbar_wait(&ctl.dq_free[b], ((j >> 1) - 1) & 1);  // dQ(j-2) drained from this buffer
+        if (j >= 1) TR(11, j - 1);
         tc_fence_after();
         const uint32_t q_a = smem_u32(sm.q[s]), do_a = smem_u32(sm.dout[s]);
 #pragma unroll
@@ -178,23 +183,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         TR(2, j);
         tc_fence_after();
         const uint32_t q_a = smem_u32(sm.q[s]), do_a = smem_u32(sm.dout[s]);
-        // dQ^T = K^T dS^T into pair j's S^T columns (K = 128 keys)
+        // dQ^T = K^T dS^T into pair j's (consumed) dP^T columns (K = 128 keys)
 #pragma unroll
         for (int kk = 0; kk < BK / 16; ++kk) {
+          if (prm.dbg & 2) break;
           const uint32_t ok = kk * 16 * 128;
-          umma_bf16_ss(tmem + b * 128, smem_desc_sw128(k_a + ok, kSlabK * 2, 1024),
+          umma_bf16_ss(tmem + b * 128 + 64, smem_desc_sw128(k_a + ok, kSlabK * 2, 1024),
                        smem_desc_sw128(ds_a + ok, kSlabK * 2, 1024), id_dq, kk > 0);
         }
         umma_commit(&ctl.dq_full[b]);
-        // dV += P^T dO ; dK += dS^T Q   (K = BQ queries)
+        // dV += P^T dO ; dK += dS^T Q   (K = BQ queries), A operands from TMEM:
+        // WG w left P^T (packed bf16) at cols 32w+[0,16), dS^T at 32w+[16,32)
 #pragma unroll
         for (int kk = 0; kk < BQ / 16; ++kk) {
-          const uint32_t oa = (kk % 4) * 32;
+          const uint32_t pcol = tmem + b * 128 + (kk >> 1) * 32 + (kk & 1) * 8;
           const uint32_t ob = kk * 16 * 128;
-          umma_bf16_ss(tmem + kDV, smem_desc_sw128(p_a + oa, 16, 1024), smem_desc_sw128(do_a + ob, kSlabQ * 2, 1024),
-                       id_acc, (j > 0 || kk > 0) ? 1u : 0u);
-          umma_bf16_ss(tmem + kDK, smem_desc_sw128(ds_a + oa, 16, 1024), smem_desc_sw128(q_a + ob, kSlabQ * 2, 1024),
-                       id_acc, (j > 0 || kk > 0) ? 1u : 0u);
+          umma_bf16_ts(tmem + kDV, pcol, smem_desc_sw128(do_a + ob, kSlabQ * 2, 1024), id_acc,
+                       (j > 0 || kk > 0) ? 1u : 0u);
+          umma_bf16_ts(tmem + kDK, pcol + 16, smem_desc_sw128(q_a + ob, kSlabQ * 2, 1024), id_acc,
+                       (j > 0 || kk > 0) ? 1u : 0u);
         }
         umma_commit(&ctl.q_empty[s]);
         umma_commit(&ctl.pds_free);
@@ -210,7 +217,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int r = quarter * 32 + lane;
     const int ctid = cw * 32 + lane;  // 0..255
     const uint32_t lane_off = uint32_t(quarter * 32) << 16;
-    const uint32_t p_a = smem_u32(sm.p), ds_a = smem_u32(sm.ds);
+    const uint32_t ds_a = smem_u32(sm.ds);
     const int key_rel = key0 - off + r;
     const int c0 = wg * 32;
 
@@ -222,13 +229,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int bb = jj & 1;
       mbar_wait(&ctl.dq_full[bb], (jj >> 1) & 1);
       tc_fence_after();
-      tmem_ld32(tmem + lane_off + bb * 128 + c0, dq);  // lane r = d, columns = queries c0..c0+31
+      tmem_ld32(tmem + lane_off + bb * 128 + 64 + c0, dq);  // lane r = d, columns = queries c0..c0+31
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(&ctl.dq_free[bb]);
     };
     auto drain_store = [&](int jj) {
       const int bb = jj & 1;
+      if (prm.dbg & 1) return;
       // stage buffer bb is free once the reduce issued two drains ago has read it
       if (ctid == 0) bulk_wait_read<0>();
       named_bar_sync(1, kCompute);
@@ -276,12 +284,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (tl) TR(6, j);
       if (j > 0) mbar_wait(&ctl.pds_free, (j - 1) & 1);
       if (tl) TR(7, j);
+      // P^T / dS^T (packed bf16) over this WG's own S^T columns: A operands of
+      // the dV / dK TS-UMMAs; dS^T also to smem: B operand of dQ^T = K^T dS^T.
+      tmem_st16(tmem + lane_off + b * 128 + wg * 32, pk);
+      tmem_st16(tmem + lane_off + b * 128 + wg * 32 + 16, dk);
 #pragma unroll
-      for (int g = 0; g < 4; ++g) {
-        const uint32_t o = sw128_offset(r, c0 + g * 8);
-        st_shared_v4(p_a + o, pk[4 * g], pk[4 * g + 1], pk[4 * g + 2], pk[4 * g + 3]);
-        st_shared_v4(ds_a + o, dk[4 * g], dk[4 * g + 1], dk[4 * g + 2], dk[4 * g + 3]);
-      }
+      for (int g = 0; g < 4; ++g)
+        st_shared_v4(ds_a + sw128_offset(r, c0 + g * 8), dk[4 * g], dk[4 * g + 1], dk[4 * g + 2], dk[4 * g + 3]);
+      tmem_wait_st();
       fence_async_smem();
       tc_fence_before();
       mbar_arrive(&ctl.pds_ready);
@@ -344,6 +354,7 @@ int attn_bwd_d128(const void* q, int64_t q_rows, int64_t q_stride, const void* k
   prm.dv = dv_acc;
   prm.acc_stride = int64_t(kv_heads) * D;
   prm.trace = getenv("SP_BWD_TRACE") != nullptr;
+  prm.dbg = getenv("SP_BWD_DBG") ? atoi(getenv("SP_BWD_DBG")) : 0;
   for (int c = 0; c < n_chunks; ++c) {
     prm.chunk_row[c] = chunk_row[c];
     prm.acc_row[c] = acc_row[c];
@@ -368,7 +379,7 @@ int attn_bwd_d128(const void* q, int64_t q_rows, int64_t q_stride, const void* k
 }
 
 int bwd_trace_copy(long long* out) {
-  return cuda_status(cudaMemcpyFromSymbol(out, g_bwd_trace, sizeof(long long) * 10 * 512), "trace copy");
+  return cuda_status(cudaMemcpyFromSymbol(out, g_bwd_trace, sizeof(long long) * 12 * 512), "trace copy");
 }
 
 }  // namespace sp

@@ -15,15 +15,15 @@ o, lse = ops.attn_fwd(q, kp, vp, rows, L, heads, heads, True)
 for _ in range(2):
     ops.attn_bwd(q, kp, vp, rows, L, heads, heads, True, o, lse, do, dq, dk, dv, rows, ws)
 torch.cuda.synchronize()
-buf = (C.c_longlong * 5120)()
+buf = (C.c_longlong * 6144)()
 lib = native.lib()
 lib.sp_debug_bwd_trace(buf)
-t = np.array(buf[:], dtype=np.int64).reshape(10, 512)
+t = np.array(buf[:], dtype=np.int64).reshape(12, 512)
 t = t - t[0, 0]
-names = ["mma_top", "sdp_issued", "pds_ready_ok", "mma_done", "drain_ld_ok", "sdp_full_ok", "compute_done", "pds_free_ok", "pds_ready_arr", "drain_st_done"]
+names = ["mma_top", "sdp_issued", "pds_ready_ok", "mma_done", "drain_ld_ok", "sdp_full_ok", "compute_done", "pds_free_ok", "pds_ready_arr", "drain_st_done", "qfull_ok", "dqfree_ok"]
 for j in [1, 2, 3, 50, 51, 52, 100, 101, 200]:
-    print(j, " ".join(f"{names[e]}={t[e, j]}" for e in range(10)))
+    print(j, " ".join(f"{names[e]}={t[e, j]}" for e in range(12)))
 per = np.diff(t[0, 10:250])
 print("mean period (cycles)", per.mean())
-for e in range(1, 10):
+for e in range(1, 12):
     print(names[e], "-", names[0], np.median(t[e, 10:250] - t[0, 10:250]))
