@@ -113,8 +113,17 @@ class Runtime {
   float *dq_acc = nullptr, *delta_ws = nullptr, *logits = nullptr, *rstd_f = nullptr, *loss_dev = nullptr;
   int32_t *tokens = nullptr, *targets = nullptr;
 
-  cudaStream_t comp = nullptr, cfwd = nullptr, cbwd = nullptr;
+  cudaStream_t comp = nullptr;
   ncclComm_t nc_fwd = nullptr, nc_bwd = nullptr;
+  // Stage links: one 2-rank communicator and one stream per (neighbour,
+  // direction), split from nc_fwd / nc_bwd, so a send to a busy neighbour
+  // never blocks a receive from the other one (no head-of-line blocking).
+  // Comm ranks inside a link: lower stage = 0, higher stage = 1.
+  ncclComm_t c_act_in = nullptr, c_act_out = nullptr, c_grad_in = nullptr, c_grad_out = nullptr;
+  cudaStream_t s_act_in = nullptr, s_act_out = nullptr, s_grad_in = nullptr, s_grad_out = nullptr;
+  bf16raw* ain_buf[2] = {nullptr, nullptr};  // activations received from s-1 (ring)
+  cudaEvent_t ev_ain_free[2]{};
+  int ain_idx = 0;
   cudaEvent_t ev_out_free[2]{}, ev_gin_free[2]{}, ev_gout_free[2]{};
   int out_idx = 0, gin_idx = 0, gout_idx = 0;
   std::vector<PassTime> times;
@@ -158,6 +167,8 @@ class Runtime {
   ~Runtime() {
     if (comp) cudaStreamSynchronize(comp);
     for (void* a : allocations) cudaFree(a);
+    for (ncclComm_t cm : {c_act_in, c_act_out, c_grad_in, c_grad_out})
+      if (cm) ncclCommDestroy(cm);
     if (nc_fwd) ncclCommDestroy(nc_fwd);
     if (nc_bwd) ncclCommDestroy(nc_bwd);
     for (int c = 0; c < 2; ++c)
@@ -228,8 +239,8 @@ class Runtime {
     }
 
     SP_CUDA(cudaStreamCreateWithFlags(&comp, cudaStreamNonBlocking));
-    SP_CUDA(cudaStreamCreateWithFlags(&cfwd, cudaStreamNonBlocking));
-    SP_CUDA(cudaStreamCreateWithFlags(&cbwd, cudaStreamNonBlocking));
+    for (cudaStream_t* st : {&s_act_in, &s_act_out, &s_grad_in, &s_grad_out})
+      SP_CUDA(cudaStreamCreateWithFlags(st, cudaStreamNonBlocking));
     for (int x = 0; x < 2; ++x) {
       SP_CUDA(cudaEventCreateWithFlags(&ev_out_free[x], cudaEventDisableTiming));
       SP_CUDA(cudaEventCreateWithFlags(&ev_gin_free[x], cudaEventDisableTiming));
@@ -237,6 +248,8 @@ class Runtime {
       SP_CUDA(cudaEventRecord(ev_out_free[x], comp));
       SP_CUDA(cudaEventRecord(ev_gin_free[x], comp));
       SP_CUDA(cudaEventRecord(ev_gout_free[x], comp));
+      SP_CUDA(cudaEventCreateWithFlags(&ev_ain_free[x], cudaEventDisableTiming));
+      SP_CUDA(cudaEventRecord(ev_ain_free[x], comp));
     }
     SP_CUDA(cudaEventCreate(&step_start));
     SP_CUDA(cudaEventCreate(&step_end));
@@ -246,6 +259,27 @@ class Runtime {
       std::memcpy(id, ids, sizeof id);
       SP_NCCL(ncclCommInitRank(&nc_fwd, p, id[0], rank));
       SP_NCCL(ncclCommInitRank(&nc_bwd, p, id[1], rank));
+      // link (r, r+1) comes from split A when r is even, split B when r is odd
+      auto split = [&](ncclComm_t parent, int color, ncclComm_t* out) -> int {
+        SP_NCCL(ncclCommSplit(parent, color, rank, out, nullptr));
+        return SP_OK;
+      };
+      const int colA = rank / 2;                                   // {0,1} {2,3} ...
+      const int colB = rank == 0 ? NCCL_SPLIT_NOCOLOR : (rank + 1) / 2;  // {1,2} {3,4} ...
+      ncclComm_t fa = nullptr, fb = nullptr, ga = nullptr, gb = nullptr;
+      SP_TRY(split(nc_fwd, (rank == p - 1 && rank % 2 == 0) ? NCCL_SPLIT_NOCOLOR : colA, &fa));
+      SP_TRY(split(nc_fwd, (rank == p - 1 && rank % 2 == 1) ? NCCL_SPLIT_NOCOLOR : colB, &fb));
+      SP_TRY(split(nc_bwd, (rank == p - 1 && rank % 2 == 0) ? NCCL_SPLIT_NOCOLOR : colA, &ga));
+      SP_TRY(split(nc_bwd, (rank == p - 1 && rank % 2 == 1) ? NCCL_SPLIT_NOCOLOR : colB, &gb));
+      const bool even = rank % 2 == 0;
+      if (stage < p) {  // link to the next stage
+        c_act_out = even ? fa : fb;
+        c_grad_in = even ? ga : gb;
+      }
+      if (stage > 1) {  // link to the previous stage (r-1, r): split A iff r-1 even
+        c_act_in = even ? fb : fa;
+        c_grad_out = even ? gb : ga;
+      }
       if (!xplan.empty() || c.exchange_mode != 0) {
         int lo = 0, hi = 0;
         SP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -553,6 +587,7 @@ class Runtime {
     SP_TRY(alloc(&tmp_H, Ls * H));
     SP_TRY(alloc(&tmp_2H, Ls * 2 * H));
     for (int x = 0; x < 2; ++x) {
+      if (stage > 1) SP_TRY(alloc(&ain_buf[x], Ls * h));
       SP_TRY(alloc(&out_buf[x], Ls * h));
       SP_TRY(alloc(&gin_buf[x], Ls * h));
       SP_TRY(alloc(&gout_buf[x], Ls * h));
@@ -675,17 +710,16 @@ class Runtime {
       SP_CUDA(cudaEventRecord(t0, comp));
       SP_TRY(embed_fwd(tokens + tok0, W(emb), xs, Ls, int(h), comp));
     } else {
-      cudaEvent_t ready, got;
-      SP_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-      SP_CUDA(cudaEventCreateWithFlags(&got, cudaEventDisableTiming));
-      SP_CUDA(cudaEventRecord(ready, comp));  // slot free in compute order
-      SP_CUDA(cudaStreamWaitEvent(cfwd, ready, 0));
-      SP_NCCL(ncclRecv(xs, Ls * h, ncclBfloat16, rank - 1, nc_fwd, cfwd));
-      SP_CUDA(cudaEventRecord(got, cfwd));
-      SP_CUDA(cudaStreamWaitEvent(comp, got, 0));
+      // receive into a ring buffer as soon as one is free (decoupled from this
+      // rank's compute progress), then copy into the slot at pass start
+      const int b = ain_idx;
+      ain_idx ^= 1;
+      SP_CUDA(cudaStreamWaitEvent(s_act_in, ev_ain_free[b], 0));
+      SP_NCCL(ncclRecv(ain_buf[b], Ls * h, ncclBfloat16, 0, c_act_in, s_act_in));
+      SP_TRY(link(s_act_in, comp));
       SP_CUDA(cudaEventRecord(t0, comp));  // busy time starts once the input is here
-      cudaEventDestroy(ready);
-      cudaEventDestroy(got);
+      SP_CUDA(cudaMemcpyAsync(xs, ain_buf[b], Ls * h * 2, cudaMemcpyDeviceToDevice, comp));
+      SP_CUDA(cudaEventRecord(ev_ain_free[b], comp));
     }
     SP_CUDA(cudaMemcpyAsync(ws[0].x_in, xs, Ls * h * 2, cudaMemcpyDeviceToDevice, comp));
     if (stage < p) {
@@ -696,9 +730,9 @@ class Runtime {
       cudaEvent_t done;
       SP_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
       SP_CUDA(cudaEventRecord(done, comp));
-      SP_CUDA(cudaStreamWaitEvent(cfwd, done, 0));
-      SP_NCCL(ncclSend(out_buf[b], Ls * h, ncclBfloat16, rank + 1, nc_fwd, cfwd));
-      SP_CUDA(cudaEventRecord(ev_out_free[b], cfwd));
+      SP_CUDA(cudaStreamWaitEvent(s_act_out, done, 0));
+      SP_NCCL(ncclSend(out_buf[b], Ls * h, ncclBfloat16, 1, c_act_out, s_act_out));
+      SP_CUDA(cudaEventRecord(ev_out_free[b], s_act_out));
       cudaEventDestroy(done);
     } else {
       SP_TRY(stage_forward(k, i, x_final, px));
@@ -797,11 +831,11 @@ class Runtime {
       gb = gin_idx;
       gin_idx ^= 1;
       dx = gin_buf[gb];
-      SP_CUDA(cudaStreamWaitEvent(cbwd, ev_gin_free[gb], 0));
-      SP_NCCL(ncclRecv(dx, Ls * h, ncclBfloat16, rank + 1, nc_bwd, cbwd));
+      SP_CUDA(cudaStreamWaitEvent(s_grad_in, ev_gin_free[gb], 0));
+      SP_NCCL(ncclRecv(dx, Ls * h, ncclBfloat16, 1, c_grad_in, s_grad_in));
       cudaEvent_t got;
       SP_CUDA(cudaEventCreateWithFlags(&got, cudaEventDisableTiming));
-      SP_CUDA(cudaEventRecord(got, cbwd));
+      SP_CUDA(cudaEventRecord(got, s_grad_in));
       SP_CUDA(cudaStreamWaitEvent(comp, got, 0));
       cudaEventDestroy(got);
       SP_CUDA(cudaEventRecord(t0, comp));
@@ -835,13 +869,13 @@ class Runtime {
       cudaEvent_t done;
       SP_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
       SP_CUDA(cudaEventRecord(done, comp));
-      SP_CUDA(cudaStreamWaitEvent(cbwd, done, 0));
+      SP_CUDA(cudaStreamWaitEvent(s_grad_out, done, 0));
       cudaEventDestroy(done);
-      SP_NCCL(ncclSend(dx, Ls * h, ncclBfloat16, rank - 1, nc_bwd, cbwd));
+      SP_NCCL(ncclSend(dx, Ls * h, ncclBfloat16, 0, c_grad_out, s_grad_out));
       if (gb >= 0) {  // middle stage: dx lives in the receive buffer
-        SP_CUDA(cudaEventRecord(ev_gin_free[gb], cbwd));
+        SP_CUDA(cudaEventRecord(ev_gin_free[gb], s_grad_out));
       } else {        // last stage: dx lives in gout_buf[gout_idx]
-        SP_CUDA(cudaEventRecord(ev_gout_free[gout_idx], cbwd));
+        SP_CUDA(cudaEventRecord(ev_gout_free[gout_idx], s_grad_out));
         gout_idx ^= 1;
       }
     }
@@ -889,10 +923,10 @@ class Runtime {
     cudaEvent_t e1, e2;
     SP_CUDA(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
     SP_CUDA(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming));
-    SP_CUDA(cudaEventRecord(e1, cfwd));
-    SP_CUDA(cudaEventRecord(e2, cbwd));
-    SP_CUDA(cudaStreamWaitEvent(comp, e1, 0));
-    SP_CUDA(cudaStreamWaitEvent(comp, e2, 0));
+    for (cudaStream_t st : {s_act_in, s_act_out, s_grad_in, s_grad_out}) {
+      SP_CUDA(cudaEventRecord(e1, st));
+      SP_CUDA(cudaStreamWaitEvent(comp, e1, 0));
+    }
     for (int c = 0; c < 2; ++c)
       if (cx[c]) {
         SP_TRY(link(cx[c], comp));
