@@ -59,7 +59,7 @@ def parse():
     ap.add_argument("--seq-len", type=int, default=131072)
     ap.add_argument("--slices", type=int, default=8)
     ap.add_argument("--microbatches", type=int, default=4)
-    ap.add_argument("--exchange", choices=["off", "on", "early"], default="early",
+    ap.add_argument("--exchange", choices=["off", "on", "early"], default="off",
                     help="attention workload redistribution (reference ExchangeMode); no effect at PP=1")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
