@@ -20,10 +20,12 @@ int embed_bwd(const int32_t* tok, const void* dy, float* dtable, int64_t rows, i
 int rmsnorm_fwd(const void* x, const void* w, void* y, float* rstd, int64_t rows, int dim, float eps, cudaStream_t st);
 int rmsnorm_bwd(const void* dy, const void* x, const void* w, const float* rstd, const void* dx_in, void* dx_out,
                 float* dw, int64_t rows, int dim, cudaStream_t st);
-int rope_qkv_fwd(const void* qkv, int64_t rows, int heads, int kv_heads, int d, int64_t pos0, float theta, void* q_out,
-                 int64_t q_stride, void* k_out, void* v_out, int64_t kv_stride, cudaStream_t st);
+int rope_table(float* cs, float* sn, int64_t positions, int d, double theta, cudaStream_t st);
+int rope_qkv_fwd(const void* qkv, int64_t rows, int heads, int kv_heads, int d, int64_t pos0, const float* cs,
+                 const float* sn, void* q_out, int64_t q_stride, void* k_out, void* v_out, int64_t kv_stride,
+                 cudaStream_t st);
 int rope_qkv_bwd(const float* dq, float* dk, float* dv, int64_t kv_stride, int64_t rows, int heads, int kv_heads,
-                 int d, int64_t pos0, float theta, void* dqkv, int zero_kv, cudaStream_t st);
+                 int d, int64_t pos0, const float* cs, const float* sn, void* dqkv, int zero_kv, cudaStream_t st);
 int swiglu_fwd(const void* gu, void* act, int64_t rows, int H, cudaStream_t st);
 int swiglu_bwd(const void* dact, const void* gu, void* dgu, int64_t rows, int H, cudaStream_t st);
 int cross_entropy(const float* logits, const int32_t* tgt, int64_t rows, int V, float scale, void* dlogits,

@@ -169,74 +169,106 @@ __global__ void rmsnorm_bwd_k(const bf16* __restrict__ dy, const bf16* __restric
 }
 
 // ---- RoPE (rotate-half convention over head_dim) ---------------------------------
-// qkv row: [q (heads*d) | k (kv*d) | v (kv*d)].  Writes rotated q to q_out,
-// rotated k and v into the K/V pool rows.  pos = pos0 + row.
-__device__ __forceinline__ void rope_cs(int64_t pos, int j, int d, float theta, float& c, float& s) {
-  const float inv = exp2f(-2.f * float(j) / float(d) * log2f(theta));
-  const float ang = float(pos) * inv;
-  sincosf(ang, &s, &c);
+// cos/sin come from a table [positions][d/2] built once per run (fp64 angles),
+// so the per-slice kernels are pure streaming: each thread rotates 4
+// consecutive pairs (j..j+3, j+d/2..j+d/2+3) of one head with 8-byte accesses.
+// qkv row: [q (heads*d) | k (kv*d) | v (kv*d)]; pos = pos0 + row.
+__global__ void rope_table_k(float* __restrict__ cs, float* __restrict__ sn, int64_t positions, int half, double theta) {
+  const int64_t n = positions * half;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t pos = i / half;
+    const int j = int(i % half);
+    const double ang = double(pos) * pow(theta, -2.0 * j / (2.0 * half));
+    double sv, cv;
+    sincos(ang, &sv, &cv);
+    cs[i] = float(cv);
+    sn[i] = float(sv);
+  }
 }
 
-__global__ void rope_qkv_fwd_k(const bf16* __restrict__ qkv, int64_t rows, int heads, int kv_heads, int d,
-                               int64_t pos0, float theta, bf16* __restrict__ q_out, int64_t q_stride,
-                               bf16* __restrict__ k_out, bf16* __restrict__ v_out, int64_t kv_stride) {
+__device__ __forceinline__ void ld4(const bf16* p, float (&f)[4]) {
+  const uint2 u = *reinterpret_cast<const uint2*>(p);
+  const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+  const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+  f[0] = a.x, f[1] = a.y, f[2] = b.x, f[3] = b.y;
+}
+
+__device__ __forceinline__ void st4(bf16* p, const float (&f)[4]) {
+  *reinterpret_cast<uint2*>(p) = make_uint2(pack_bf16(f[0], f[1]), pack_bf16(f[2], f[3]));
+}
+
+__global__ void rope_qkv_fwd_k(const bf16* __restrict__ qkv, int heads, int kv_heads, int d, int64_t pos0,
+                               const float* __restrict__ cs, const float* __restrict__ sn, bf16* __restrict__ q_out,
+                               int64_t q_stride, bf16* __restrict__ k_out, bf16* __restrict__ v_out,
+                               int64_t kv_stride) {
   const int64_t r = blockIdx.x;
-  const int width = (heads + 2 * kv_heads) * d;
-  const bf16* src = qkv + r * width;
-  const int half = d / 2;
-  const int pairs = (heads + kv_heads) * half;
-  for (int idx = threadIdx.x; idx < pairs; idx += blockDim.x) {
-    const int h = idx / half, j = idx % half;
-    float c, s;
-    rope_cs(pos0 + r, j, d, theta, c, s);
-    const float x1 = __bfloat162float(src[h * d + j]), x2 = __bfloat162float(src[h * d + j + half]);
-    const float y1 = x1 * c - x2 * s, y2 = x2 * c + x1 * s;
-    if (h < heads) {
-      q_out[r * q_stride + h * d + j] = __float2bfloat16(y1);
-      q_out[r * q_stride + h * d + j + half] = __float2bfloat16(y2);
-    } else {
-      const int kh = h - heads;
-      k_out[r * kv_stride + kh * d + j] = __float2bfloat16(y1);
-      k_out[r * kv_stride + kh * d + j + half] = __float2bfloat16(y2);
+  const int half = d / 2, qpr = half / 4;  // quads per head
+  const bf16* src = qkv + r * int64_t(heads + 2 * kv_heads) * d;
+  const float* c_row = cs + (pos0 + r) * half;
+  const float* s_row = sn + (pos0 + r) * half;
+  for (int idx = threadIdx.x; idx < (heads + kv_heads) * qpr; idx += blockDim.x) {
+    const int h = idx / qpr, j = (idx % qpr) * 4;
+    float x1[4], x2[4], y1[4], y2[4];
+    ld4(src + h * d + j, x1);
+    ld4(src + h * d + j + half, x2);
+    const float4 c = *reinterpret_cast<const float4*>(c_row + j);
+    const float4 sv = *reinterpret_cast<const float4*>(s_row + j);
+    const float cc[4] = {c.x, c.y, c.z, c.w}, ss[4] = {sv.x, sv.y, sv.z, sv.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      y1[e] = x1[e] * cc[e] - x2[e] * ss[e];
+      y2[e] = x2[e] * cc[e] + x1[e] * ss[e];
     }
+    bf16* dst = h < heads ? q_out + r * q_stride + h * d : k_out + r * kv_stride + (h - heads) * d;
+    st4(dst + j, y1);
+    st4(dst + j + half, y2);
   }
-  for (int idx = threadIdx.x; idx < kv_heads * d; idx += blockDim.x)
-    v_out[r * kv_stride + idx] = src[(heads + kv_heads) * d + idx];
+  const uint4* vs = reinterpret_cast<const uint4*>(src + (heads + kv_heads) * d);
+  uint4* vd = reinterpret_cast<uint4*>(v_out + r * kv_stride);
+  for (int idx = threadIdx.x; idx < kv_heads * d / 8; idx += blockDim.x) vd[idx] = vs[idx];
 }
 
 // Inverse rotation of fp32 gradients into the bf16 d_qkv row.  dq rows come
 // from dq (q_rows x heads*d); dk/dv from the chunk accumulators (zeroed after
-// reading when `zero_kv`).
-__global__ void rope_qkv_bwd_k(const float* __restrict__ dq, float* dk, float* dv, int64_t kv_stride, int64_t rows,
-                               int heads, int kv_heads, int d, int64_t pos0, float theta, bf16* __restrict__ dqkv,
-                               int zero_kv) {
+// reading when `zero_kv`).  y1 = x1 c - x2 s, y2 = x2 c + x1 s  =>
+// dx1 = g1 c + g2 s, dx2 = g2 c - g1 s.
+__global__ void rope_qkv_bwd_k(const float* __restrict__ dq, float* dk, float* dv, int64_t kv_stride, int heads,
+                               int kv_heads, int d, int64_t pos0, const float* __restrict__ cs,
+                               const float* __restrict__ sn, bf16* __restrict__ dqkv, int zero_kv) {
   const int64_t r = blockIdx.x;
-  const int width = (heads + 2 * kv_heads) * d;
-  bf16* dst = dqkv + r * width;
-  const int half = d / 2;
-  const int pairs = (heads + kv_heads) * half;
-  for (int idx = threadIdx.x; idx < pairs; idx += blockDim.x) {
-    const int h = idx / half, j = idx % half;
-    float c, s;
-    rope_cs(pos0 + r, j, d, theta, c, s);
-    float g1, g2;
-    if (h < heads) {
-      g1 = dq[r * heads * d + h * d + j];
-      g2 = dq[r * heads * d + h * d + j + half];
-    } else {
-      float* p = dk + r * kv_stride + (h - heads) * d;
-      g1 = p[j];
-      g2 = p[j + half];
-      if (zero_kv) p[j] = p[j + half] = 0.f;
+  const int half = d / 2, qpr = half / 4;
+  bf16* dst = dqkv + r * int64_t(heads + 2 * kv_heads) * d;
+  const float* c_row = cs + (pos0 + r) * half;
+  const float* s_row = sn + (pos0 + r) * half;
+  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int idx = threadIdx.x; idx < (heads + kv_heads) * qpr; idx += blockDim.x) {
+    const int h = idx / qpr, j = (idx % qpr) * 4;
+    float* g = h < heads ? const_cast<float*>(dq) + r * int64_t(heads) * d + h * d : dk + r * kv_stride + (h - heads) * d;
+    const float4 a = *reinterpret_cast<const float4*>(g + j);
+    const float4 b = *reinterpret_cast<const float4*>(g + j + half);
+    if (h >= heads && zero_kv) {
+      *reinterpret_cast<float4*>(g + j) = zero;
+      *reinterpret_cast<float4*>(g + j + half) = zero;
     }
-    // y1 = x1 c - x2 s ; y2 = x2 c + x1 s  =>  dx1 = g1 c + g2 s ; dx2 = g2 c - g1 s
-    dst[h * d + j] = __float2bfloat16(g1 * c + g2 * s);
-    dst[h * d + j + half] = __float2bfloat16(g2 * c - g1 * s);
+    const float4 c = *reinterpret_cast<const float4*>(c_row + j);
+    const float4 sv = *reinterpret_cast<const float4*>(s_row + j);
+    const float g1[4] = {a.x, a.y, a.z, a.w}, g2[4] = {b.x, b.y, b.z, b.w};
+    const float cc[4] = {c.x, c.y, c.z, c.w}, ss[4] = {sv.x, sv.y, sv.z, sv.w};
+    float o1[4], o2[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      o1[e] = g1[e] * cc[e] + g2[e] * ss[e];
+      o2[e] = g2[e] * cc[e] - g1[e] * ss[e];
+    }
+    st4(dst + h * d + j, o1);
+    st4(dst + h * d + j + half, o2);
   }
-  for (int idx = threadIdx.x; idx < kv_heads * d; idx += blockDim.x) {
-    float* p = dv + r * kv_stride + idx;
-    dst[(heads + kv_heads) * d + idx] = __float2bfloat16(*p);
-    if (zero_kv) *p = 0.f;
+  for (int idx = threadIdx.x; idx < kv_heads * d / 4; idx += blockDim.x) {
+    float4* p = reinterpret_cast<float4*>(dv + r * kv_stride) + idx;
+    const float4 v = *p;
+    const float f[4] = {v.x, v.y, v.z, v.w};
+    st4(dst + (heads + kv_heads) * d + idx * 4, f);
+    if (zero_kv) *p = zero;
   }
 }
 
@@ -432,18 +464,26 @@ int rmsnorm_bwd(const void* dy, const void* x, const void* w, const float* rstd,
   return cuda_status(cudaGetLastError(), "rmsnorm_bwd");
 }
 
-int rope_qkv_fwd(const void* qkv, int64_t rows, int heads, int kv_heads, int d, int64_t pos0, float theta, void* q_out,
-                 int64_t q_stride, void* k_out, void* v_out, int64_t kv_stride, cudaStream_t st) {
-  rope_qkv_fwd_k<<<unsigned(rows), 256, 0, st>>>((const bf16*)qkv, rows, heads, kv_heads, d, pos0, theta, (bf16*)q_out,
+int rope_table(float* cs, float* sn, int64_t positions, int d, double theta, cudaStream_t st) {
+  rope_table_k<<<grid_for(positions * (d / 2), 256), 256, 0, st>>>(cs, sn, positions, d / 2, theta);
+  count_launch();
+  return cuda_status(cudaGetLastError(), "rope_table");
+}
+
+int rope_qkv_fwd(const void* qkv, int64_t rows, int heads, int kv_heads, int d, int64_t pos0, const float* cs,
+                 const float* sn, void* q_out, int64_t q_stride, void* k_out, void* v_out, int64_t kv_stride,
+                 cudaStream_t st) {
+  if (d % 8) return set_error(SP_ERR_UNSUPPORTED, "rope: head_dim %% 8");
+  rope_qkv_fwd_k<<<unsigned(rows), 256, 0, st>>>((const bf16*)qkv, heads, kv_heads, d, pos0, cs, sn, (bf16*)q_out,
                                                  q_stride, (bf16*)k_out, (bf16*)v_out, kv_stride);
   count_launch();
   return cuda_status(cudaGetLastError(), "rope_qkv_fwd");
 }
 
 int rope_qkv_bwd(const float* dq, float* dk, float* dv, int64_t kv_stride, int64_t rows, int heads, int kv_heads,
-                 int d, int64_t pos0, float theta, void* dqkv, int zero_kv, cudaStream_t st) {
-  rope_qkv_bwd_k<<<unsigned(rows), 256, 0, st>>>(dq, dk, dv, kv_stride, rows, heads, kv_heads, d, pos0, theta,
-                                                 (bf16*)dqkv, zero_kv);
+                 int d, int64_t pos0, const float* cs, const float* sn, void* dqkv, int zero_kv, cudaStream_t st) {
+  rope_qkv_bwd_k<<<unsigned(rows), 256, 0, st>>>(dq, dk, dv, kv_stride, heads, kv_heads, d, pos0, cs, sn, (bf16*)dqkv,
+                                                 zero_kv);
   count_launch();
   return cuda_status(cudaGetLastError(), "rope_qkv_bwd");
 }

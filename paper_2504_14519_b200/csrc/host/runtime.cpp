@@ -110,6 +110,7 @@ class Runtime {
   bf16raw* out_buf[2] = {nullptr, nullptr};  // stage outputs (send to s+1)
   bf16raw* gin_buf[2] = {nullptr, nullptr};  // gradients received from s+1
   bf16raw* gout_buf[2] = {nullptr, nullptr}; // gradients sent to s-1 (dx)
+  float *rope_cos = nullptr, *rope_sin = nullptr;  // [seq_len][d/2]
   float *dq_acc = nullptr, *delta_ws = nullptr, *logits = nullptr, *rstd_f = nullptr, *loss_dev = nullptr;
   int32_t *tokens = nullptr, *targets = nullptr;
 
@@ -592,6 +593,9 @@ class Runtime {
       SP_TRY(alloc(&gin_buf[x], Ls * h));
       SP_TRY(alloc(&gout_buf[x], Ls * h));
     }
+    SP_TRY(alloc(&rope_cos, cfg.seq_len * (cfg.head_dim / 2)));
+    SP_TRY(alloc(&rope_sin, cfg.seq_len * (cfg.head_dim / 2)));
+    SP_TRY(rope_table(rope_cos, rope_sin, cfg.seq_len, cfg.head_dim, double(cfg.rope_theta), comp));
     SP_TRY(alloc(&dq_acc, Ls * qd));
     SP_TRY(alloc(&delta_ws, 2 * int64_t(cfg.heads) * Ls));
     SP_TRY(alloc(&loss_dev, 1));
@@ -677,7 +681,7 @@ class Runtime {
     const int64_t pos0 = int64_t(i - 1) * Ls;
     SP_TRY(rmsnorm_fwd(x.x_in, W(P.attn_norm), x.xn, x.rstd1, Ls, int(h), cfg.norm_eps, comp));
     SP_TRY(gemm(false, true, Ls, qkv_w, h, x.xn, h, W(P.wqkv), h, qkv, qkv_w, false, 1.f, 0.f, comp));
-    SP_TRY(rope_qkv_fwd(qkv, Ls, cfg.heads, cfg.kv_heads, cfg.head_dim, pos0, cfg.rope_theta, x.q, qd,
+    SP_TRY(rope_qkv_fwd(qkv, Ls, cfg.heads, cfg.kv_heads, cfg.head_dim, pos0, rope_cos, rope_sin, x.q, qd,
                         k_pool[l] + int64_t(slot) * Ls * kvd, v_pool[l] + int64_t(slot) * Ls * kvd, kvd, comp));
     SP_TRY(attention_forward(l, k, i, x, px));
     SP_CUDA(cudaMemcpyAsync(x.x_mid, x.x_in, Ls * h * 2, cudaMemcpyDeviceToDevice, comp));
@@ -811,7 +815,7 @@ class Runtime {
     }
     // chunk i's dK/dV is complete: RoPE backward into d_qkv and reset the rows
     SP_TRY(rope_qkv_bwd(dq_acc, dk_acc[l] + pos0 * kvd, dv_acc[l] + pos0 * kvd, kvd, Ls, cfg.heads, cfg.kv_heads,
-                        cfg.head_dim, pos0, cfg.rope_theta, dqkv, 1, comp));
+                        cfg.head_dim, pos0, rope_cos, rope_sin, dqkv, 1, comp));
     SP_TRY(gemm(false, false, Ls, h, qkv_w, dqkv, qkv_w, W(P.wqkv), h, tmp_h, h, false, 1.f, 0.f, comp));   // dxn
     SP_TRY(gemm(true, false, qkv_w, h, Ls, dqkv, qkv_w, x.xn, h, G(P.wqkv), h, true, 1.f, 1.f, comp));      // dWqkv
     SP_TRY(rmsnorm_bwd(tmp_h, x.x_in, W(P.attn_norm), x.rstd1, dx, dx, G(P.attn_norm), Ls, int(h), comp));
