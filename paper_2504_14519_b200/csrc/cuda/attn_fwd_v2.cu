@@ -39,6 +39,8 @@ constexpr int kSlab = 128 * 64;
 struct Params {
   int q_rows, total_kv, chunk_len, group, causal;
   float scale_log2;
+  int dbg;    // diagnostics: 1 = MMA ignores P readiness, 2 = + no K/V reloads
+  int trace;  // per-tile timeline of CTA (0,0) into g_fwd_trace (diagnostics)
   __nv_bfloat16* o;
   int64_t o_stride;
   float* lse;
@@ -72,6 +74,12 @@ __device__ __forceinline__ float poly_exp2(float x) {
   return __int_as_float(__float_as_int(p) + (j << 23));
 }
 
+__device__ long long g_fwd_trace[12][1024];
+#define TRF(e, j)                                                           \
+  do {                                                                      \
+    if (tracing && (j) < 1024) g_fwd_trace[e][(j)] = clock64();            \
+  } while (0)
+
 template <int kPoly>  // every kPoly-th pair computes its second exponential on the FMA pipe (0: never)
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_d128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
@@ -85,6 +93,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int kvh = head / prm.group;
   const int row0 = tile * BM;
   const int n = prm.causal ? (prm.total_kv - prm.q_rows + row0 + BM) / BN : prm.total_kv / BN;
+  const bool tracing = prm.trace && blockIdx.x == 0 && blockIdx.y == 0;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tm_q);
@@ -137,9 +146,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       // consumption order: S(0), S(1), PV(0), S(2), PV(1), ... (K two ahead of V)
       int jk = 0;
       for (; jk < n && jk < 2; ++jk) load_k(jk);
-      for (int jv = 0; jv < n; ++jv) {
+      const int nload = (prm.dbg & 2) ? (n < NV ? n : NV) : n;
+      if (prm.dbg & 2) for (; jk < n && jk < NK; ++jk) load_k(jk);
+      for (int jv = 0; jv < nload; ++jv) {
         load_v(jv);
-        if (jk < n) load_k(jk++);
+        if (jk < n && !(prm.dbg & 2)) load_k(jk++);
       }
     }
   } else if (warp == 1) {
@@ -149,7 +160,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t q_a = smem_u32(sm.q);
       auto issue_s = [&](int j) {
         const int s = j % NK;
-        mbar_wait(&ctl.k_full[s], (j / NK) & 1);
+        if (!(prm.dbg & 2) || j < NK) mbar_wait(&ctl.k_full[s], (j / NK) & 1);
+        TRF(10, j);
         tc_fence_after();
         const uint32_t k_a = smem_u32(sm.k[s]);
 #pragma unroll
@@ -168,9 +180,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         // S(j+1) into the other buffer: softmax(j-1) finished with it (p_full
         // waited in iteration j-1) and P(j-1) is consumed by PV(j-1), issued
         // before this MMA (in-order tcgen05 pipe).
-        if (j + 1 < n) issue_s(j + 1);
-        mbar_wait(&ctl.p_full[j & 1], (j >> 1) & 1);
-        mbar_wait(&ctl.v_full[j % NV], (j / NV) & 1);
+        TRF(0, j);
+        if (j + 1 < n && !(prm.dbg & 8)) issue_s(j + 1);
+        TRF(1, j);
+        if (!(prm.dbg & 1)) mbar_wait(&ctl.p_full[j & 1], (j >> 1) & 1);
+        TRF(2, j);
+        if (!(prm.dbg & 2) || j < NV) mbar_wait(&ctl.v_full[j % NV], (j / NV) & 1);
+        TRF(3, j);
         tc_fence_after();
         const uint32_t v_a = smem_u32(sm.v[j % NV]);
         const uint32_t p_t = tmem + (j & 1) * 128;
@@ -178,11 +194,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int hf = 0; hf < 2; ++hf)
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)  // keys [64hf + 16kk, +16)
+            if (!(prm.dbg & 4))
             umma_bf16_ts(tmem + 256 + hf * 128, p_t + hf * 64 + kk * 8,
                          smem_desc_sw128(v_a + (hf * 64 + kk * 16) * 128, kSlab * 2, 1024), id_o,
                          (j > 0 || kk > 0) ? 1u : 0u);
         umma_commit(&ctl.v_empty[j % NV]);
         umma_commit(&ctl.o_ready);
+        TRF(4, j);
       }
     }
   } else {
@@ -194,10 +212,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t o_col = tmem + 256 + hf * 128 + lane_off;
     const float sl2 = prm.scale_log2;
     float m_used = -INFINITY, l = 0.f;
-    for (int j = 0; j < n; ++j) {
+    for (int j = 0; j < ((prm.dbg & 16) ? 0 : n); ++j) {
       const int b = j & 1;
       const uint32_t s_col = tmem + b * 128 + hf * 64 + lane_off;
+      const bool tl = tracing && warp == 2 && lane == 0;
+      if (tl) TRF(5, j);
       mbar_wait(&ctl.s_full[b], (j >> 1) & 1);
+      if (tl) TRF(6, j);
       tc_fence_after();
       const bool diag = prm.causal && j == n - 1;
       float sv[64];
@@ -209,9 +230,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int x = 0; x < 64; ++x)
           if (hf * 64 + x > r) sv[x] = -INFINITY;
       }
-      float mx = -INFINITY;
+      // tree reduction: 8 independent chains instead of one 64-long FMNMX chain
+      float m8[8];
 #pragma unroll
-      for (int x = 0; x < 64; ++x) mx = fmaxf(mx, sv[x]);
+      for (int x = 0; x < 8; ++x) m8[x] = fmaxf(sv[x], sv[x + 8]);
+#pragma unroll
+      for (int x = 16; x < 64; x += 8)
+#pragma unroll
+        for (int y = 0; y < 8; ++y) m8[y] = fmaxf(m8[y], sv[x + y]);
+      const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])), fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+      if (tl) TRF(7, j);
       const float cand = mx * sl2;
       const bool grow = cand > m_used + 8.0f;
       float corr = 1.f;
@@ -233,7 +261,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_st32(o_col + c * 32, ov);
         }
       }
-      float rs0 = 0.f, rs1 = 0.f;
+      float rs[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         uint32_t pk[16];
@@ -242,16 +270,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float a = fast_exp2(fmaf(sv[h * 32 + 2 * x], sl2, -msub));
           const float xc = fmaf(sv[h * 32 + 2 * x + 1], sl2, -msub);
           const float c = (kPoly > 0 && x % (kPoly > 0 ? kPoly : 1) == 0) ? poly_exp2(xc) : fast_exp2(xc);
-          rs0 += a;
-          rs1 += c;
+          rs[(2 * x) & 7] += a;
+          rs[(2 * x + 1) & 7] += c;
           pk[x] = pack_bf16(a, c);
         }
         tmem_st16(s_col + h * 16, pk);
       }
-      l = l * corr + (rs0 + rs1);
+      l = l * corr + (((rs[0] + rs[1]) + (rs[2] + rs[3])) + ((rs[4] + rs[5]) + (rs[6] + rs[7])));
+      if (tl) TRF(8, j);
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&ctl.p_full[b]);
+      if (tl) TRF(9, j);
     }
     // ---------------- epilogue: merge the two halves (reference merge_partials)
     ctl.m_half[hf][r] = m_used;
@@ -312,6 +342,8 @@ int attn_fwd_d128(const void* q, int64_t q_rows, int64_t q_stride, const void* k
   prm.group = heads / kv_heads;
   prm.causal = causal;
   prm.scale_log2 = float(1.4426950408889634 / sqrt(double(D)));
+  prm.trace = getenv("SP_FWD_TRACE") != nullptr;
+  prm.dbg = getenv("SP_FWD_DBG") ? atoi(getenv("SP_FWD_DBG")) : 0;
   prm.o = static_cast<__nv_bfloat16*>(o);
   prm.o_stride = o_stride;
   prm.lse = lse;
@@ -334,4 +366,10 @@ int attn_fwd_d128(const void* q, int64_t q_rows, int64_t q_stride, const void* k
   return cuda_status(cudaGetLastError(), "attn_fwd_d128 launch");
 }
 
+int fwd_trace_copy(long long* out) {
+  return cuda_status(cudaMemcpyFromSymbol(out, g_fwd_trace, sizeof(long long) * 12 * 1024), "trace copy");
+}
+
 }  // namespace sp
+
+extern "C" int sp_debug_fwd_trace(long long* out) { return sp::fwd_trace_copy(out); }

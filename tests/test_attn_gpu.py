@@ -87,6 +87,8 @@ def test_fwd_matches_reference_golden_fixtures():
     (128, 4, 4, 3, 256, True),
     (128, 8, 2, 4, 128, True),     # GQA 4:1
     (128, 2, 2, 2, 384, False),
+    (128, 4, 4, 2, 512, True),     # two 256-row query pairs per head
+    (128, 2, 2, 3, 640, True),     # odd 128-row tile count: last pair has no tile B
     (64, 4, 4, 4, 256, True),      # c1 head_dim
     (64, 4, 1, 2, 128, True),
 ])
