@@ -12,9 +12,11 @@
 //     kernel is bound by; dQ^T of pair j lands in its consumed dP^T columns.
 //   * two compute warpgroups (8 warps) split every pair's 64 query columns;
 //   * dQ leaves through TMA bulk reduce-add (cp.reduce.async.bulk.tensor
-//     .add.f32) from a double-buffered smem stage instead of per-thread
-//     global atomics.
-// Warps: 0 TMA producer, 1 TMEM owner + UMMA issuer, 2..9 element math.
+//     .add.f32) from an smem stage instead of per-thread global atomics; a
+//     dedicated drain warpgroup does TMEM -> smem -> TMA, so the element-math
+//     warps never wait on it (it was ~28% of their time per pair).
+// Warps: 0 TMA producer, 1 TMEM owner + UMMA issuer, 2..9 element math,
+// 10..13 dQ drain.
 #include <math.h>
 
 #include "errors.hpp"
@@ -27,8 +29,9 @@ namespace sp {
 namespace {
 
 constexpr int D = 128, BQ = 64, BK = 128, NS = 3;
-constexpr int kThreads = 320;
+constexpr int kThreads = 448;
 constexpr int kCompute = 256;
+constexpr int kDrain = 128;
 constexpr int kSlabQ = BQ * 64, kSlabK = BK * 64;  // elements per slab
 
 struct Params {
@@ -38,9 +41,11 @@ struct Params {
   const float* delta;
   float* dk;
   float* dv;
+  float* dq;  // [q_rows][heads * D] fp32 accumulator (direct-reduce drain)
   int64_t acc_stride;
   int trace;  // record a per-pair timeline of CTA (0,0) into g_bwd_trace
   int dbg;    // diagnostics only: bit0 skip the dQ stage/reduce, bit1 skip the dQ MMA
+  int dq_red; // 1: dQ by red.global.add from registers (no smem stage), 0: smem stage + TMA reduce
   int chunk_row[SP_MAX_CHUNKS];
   int acc_row[SP_MAX_CHUNKS];
 };
@@ -111,7 +116,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int b = 0; b < 2; ++b) {
       mbar_init(&ctl.sdp_full[b], 1);
       mbar_init(&ctl.dq_full[b], 1);
-      mbar_init(&ctl.dq_free[b], kCompute);
+      mbar_init(&ctl.dq_free[b], kDrain);
     }
     mbar_init(&ctl.pds_ready, kCompute);
     mbar_init(&ctl.pds_free, 1);
@@ -148,11 +153,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && n_pairs > 0) {
+    // the whole warp runs the issue loop; one elected lane issues each UMMA
+    // (sm100.cuh *_w / umma_commit_warp): a lane-0-only loop pays an
+    // ELECT/BRA.U.ANY wrapper per MMA and starves the tensor pipe
+    if (n_pairs > 0) {
       constexpr uint32_t id_s = idesc_bf16_f32(BK, BQ, false, false);  // K Q^T, V dO^T
       constexpr uint32_t id_acc = idesc_bf16_f32(BK, D, false, true);  // P^T dO, dS^T Q
       constexpr uint32_t id_dq = idesc_bf16_f32(D, BQ, true, true);    // K^T dS^T
       const uint32_t k_a = smem_u32(sm.k), v_a = smem_u32(sm.v), ds_a = smem_u32(sm.ds);
+      // descriptor bases; per-step offsets are added to the low word (address >> 4)
+      const uint64_t dk_k = smem_desc_sw128(k_a, 16, 1024), dv_k = smem_desc_sw128(v_a, 16, 1024);
+      const uint64_t dk_mn = smem_desc_sw128(k_a, kSlabK * 2, 1024), dds_mn = smem_desc_sw128(ds_a, kSlabK * 2, 1024);
       auto issue_sdp = [&](int j) {
         const int s = j % NS, b = j & 1;
         mbar_wait(&ctl.q_full[s], (j / NS) & 1);
@@ -160,17 +171,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (j >= 2) mbar_wait(&ctl.dq_free[b], ((j >> 1) - 1) & 1);  // dQ(j-2) drained from this buffer
         if (j >= 1) TR(11, j - 1);
         tc_fence_after();
-        const uint32_t q_a = smem_u32(sm.q[s]), do_a = smem_u32(sm.dout[s]);
+        const uint64_t dq_k = smem_desc_sw128(smem_u32(sm.q[s]), 16, 1024);
+        const uint64_t ddo_k = smem_desc_sw128(smem_u32(sm.dout[s]), 16, 1024);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t oa = (kk / 4) * (kSlabK * 2) + (kk % 4) * 32;
-          const uint32_t ob = (kk / 4) * (kSlabQ * 2) + (kk % 4) * 32;
-          umma_bf16_ss(tmem + b * 128, smem_desc_sw128(k_a + oa, 16, 1024), smem_desc_sw128(q_a + ob, 16, 1024),
-                       id_s, kk > 0);
-          umma_bf16_ss(tmem + b * 128 + 64, smem_desc_sw128(v_a + oa, 16, 1024),
-                       smem_desc_sw128(do_a + ob, 16, 1024), id_s, kk > 0);
+          const uint32_t oa = ((kk / 4) * (kSlabK * 2) + (kk % 4) * 32) >> 4;
+          const uint32_t ob = ((kk / 4) * (kSlabQ * 2) + (kk % 4) * 32) >> 4;
+          umma_bf16_ss_w(tmem + b * 128, dk_k + oa, dq_k + ob, id_s, kk > 0);
+          umma_bf16_ss_w(tmem + b * 128 + 64, dv_k + oa, ddo_k + ob, id_s, kk > 0);
         }
-        umma_commit(&ctl.sdp_full[b]);
+        umma_commit_warp(&ctl.sdp_full[b]);
       };
       mbar_wait(&ctl.kv_full, 0);
       issue_sdp(0);
@@ -182,34 +192,32 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&ctl.pds_ready, j & 1);
         TR(2, j);
         tc_fence_after();
-        const uint32_t q_a = smem_u32(sm.q[s]), do_a = smem_u32(sm.dout[s]);
+        const uint64_t dq_mn = smem_desc_sw128(smem_u32(sm.q[s]), kSlabQ * 2, 1024);
+        const uint64_t ddo_mn = smem_desc_sw128(smem_u32(sm.dout[s]), kSlabQ * 2, 1024);
         // dQ^T = K^T dS^T into pair j's (consumed) dP^T columns (K = 128 keys)
 #pragma unroll
         for (int kk = 0; kk < BK / 16; ++kk) {
           if (prm.dbg & 2) break;
-          const uint32_t ok = kk * 16 * 128;
-          umma_bf16_ss(tmem + b * 128 + 64, smem_desc_sw128(k_a + ok, kSlabK * 2, 1024),
-                       smem_desc_sw128(ds_a + ok, kSlabK * 2, 1024), id_dq, kk > 0);
+          const uint32_t ok = (kk * 16 * 128) >> 4;
+          umma_bf16_ss_w(tmem + b * 128 + 64, dk_mn + ok, dds_mn + ok, id_dq, kk > 0);
         }
-        umma_commit(&ctl.dq_full[b]);
+        umma_commit_warp(&ctl.dq_full[b]);
         // dV += P^T dO ; dK += dS^T Q   (K = BQ queries), A operands from TMEM:
         // WG w left P^T (packed bf16) at cols 32w+[0,16), dS^T at 32w+[16,32)
 #pragma unroll
         for (int kk = 0; kk < BQ / 16; ++kk) {
           const uint32_t pcol = tmem + b * 128 + (kk >> 1) * 32 + (kk & 1) * 8;
-          const uint32_t ob = kk * 16 * 128;
-          umma_bf16_ts(tmem + kDV, pcol, smem_desc_sw128(do_a + ob, kSlabQ * 2, 1024), id_acc,
-                       (j > 0 || kk > 0) ? 1u : 0u);
-          umma_bf16_ts(tmem + kDK, pcol + 16, smem_desc_sw128(q_a + ob, kSlabQ * 2, 1024), id_acc,
-                       (j > 0 || kk > 0) ? 1u : 0u);
+          const uint32_t ob = (kk * 16 * 128) >> 4;
+          umma_bf16_ts_w(tmem + kDV, pcol, ddo_mn + ob, id_acc, (j > 0 || kk > 0) ? 1u : 0u);
+          umma_bf16_ts_w(tmem + kDK, pcol + 16, dq_mn + ob, id_acc, (j > 0 || kk > 0) ? 1u : 0u);
         }
-        umma_commit(&ctl.q_empty[s]);
-        umma_commit(&ctl.pds_free);
+        umma_commit_warp(&ctl.q_empty[s]);
+        umma_commit_warp(&ctl.pds_free);
         TR(3, j);
       }
-      umma_commit(&ctl.acc_done);
+      umma_commit_warp(&ctl.acc_done);
     }
-  } else {
+  } else if (warp < 10) {
     // ------------------------------------------------ element math (2 WGs)
     const int cw = warp - 2;         // 0..7
     const int wg = cw >> 2;          // column half of every pair
@@ -221,41 +229,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int key_rel = key0 - off + r;
     const int c0 = wg * 32;
 
-    // dQ of pair jj: (1) TMEM -> registers, freeing its TMEM columns for the
-    // S/dP of pair jj+2 as early as possible; (2) registers -> smem stage ->
-    // TMA reduce-add into dq_acc.
-    float dq[32];
-    auto drain_load = [&](int jj) {
-      const int bb = jj & 1;
-      mbar_wait(&ctl.dq_full[bb], (jj >> 1) & 1);
-      tc_fence_after();
-      tmem_ld32(tmem + lane_off + bb * 128 + 64 + c0, dq);  // lane r = d, columns = queries c0..c0+31
-      tmem_wait_ld();
-      tc_fence_before();
-      mbar_arrive(&ctl.dq_free[bb]);
-    };
-    auto drain_store = [&](int jj) {
-      const int bb = jj & 1;
-      if (prm.dbg & 1) return;
-      // stage buffer bb is free once the reduce issued two drains ago has read it
-      if (ctid == 0) bulk_wait_read<0>();
-      named_bar_sync(1, kCompute);
-      const uint32_t st = smem_u32(sm.stage[0]) + uint32_t(c0 * D + r) * 4u;
-#pragma unroll
-      for (int x = 0; x < 32; ++x) asm volatile("st.shared.f32 [%0], %1;" ::"r"(st + x * D * 4), "f"(dq[x]) : "memory");
-      fence_async_smem();
-      named_bar_sync(2, kCompute);
-      if (ctid == 0) {
-        tma_reduce_add_2d(&tm_dq, sm.stage[0], pair_head(jj) * D, pair_row(jj));
-        bulk_commit();
-      }
-    };
-
     for (int j = 0; j < n_pairs; ++j) {
       const int s = j % NS, b = j & 1;
       const bool tl = ctid == 0;
-      if (j > 0) drain_load(j - 1);
-      if (tl) TR(4, j);
+
       const int qrow0 = pair_row(j);
       const bool need_mask = prm.causal && (key0 + BK - 1 - off > qrow0);
       mbar_wait(&ctl.q_full[s], (j / NS) & 1);
@@ -266,20 +243,40 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_ld32(tmem + lane_off + b * 128 + c0, sv);
       tmem_ld32(tmem + lane_off + b * 128 + 64 + c0, dp);
       tmem_wait_ld();
+      // P = exp2(S*scale*log2e - lse2), dS = P * (dP - delta) * scale on
+      // packed fp32x2 (FFMA2/FMUL2); statistics come from smem 8 columns at a
+      // time with 128-bit loads (they are uniform across the warp)
       uint32_t pk[16], dk[16];
+      const float* lse_s = ctl.lse2[s] + c0;
+      const float* del_s = ctl.delta[s] + c0;
+      const float2 sl2x2 = make_float2(prm.scale_log2, prm.scale_log2);
+      const float2 scx2 = make_float2(prm.scale, prm.scale);
+      const float2 nscx2 = make_float2(-prm.scale, -prm.scale);
+      const float2 neg1 = make_float2(-1.f, -1.f);
 #pragma unroll
-      for (int x = 0; x < 32; x += 2) {
-        float pp[2], dd[2];
+      for (int g = 0; g < 4; ++g) {
+        const float4 la = *reinterpret_cast<const float4*>(lse_s + 8 * g);
+        const float4 lb = *reinterpret_cast<const float4*>(lse_s + 8 * g + 4);
+        const float4 da = *reinterpret_cast<const float4*>(del_s + 8 * g);
+        const float4 db = *reinterpret_cast<const float4*>(del_s + 8 * g + 4);
+        const float2 nl[4] = {fmul2(make_float2(la.x, la.y), neg1), fmul2(make_float2(la.z, la.w), neg1),
+                              fmul2(make_float2(lb.x, lb.y), neg1), fmul2(make_float2(lb.z, lb.w), neg1)};
+        const float2 nd[4] = {fmul2(make_float2(da.x, da.y), nscx2), fmul2(make_float2(da.z, da.w), nscx2),
+                              fmul2(make_float2(db.x, db.y), nscx2), fmul2(make_float2(db.z, db.w), nscx2)};
 #pragma unroll
-        for (int y = 0; y < 2; ++y) {
-          const int c = c0 + x + y;
-          float pv = fast_exp2(fmaf(sv[x + y], prm.scale_log2, -ctl.lse2[s][c]));
-          if (need_mask && key_rel > qrow0 + c) pv = 0.f;
-          pp[y] = pv;
-          dd[y] = pv * (dp[x + y] - ctl.delta[s][c]) * prm.scale;
+        for (int e = 0; e < 4; ++e) {
+          const int x = 8 * g + 2 * e;
+          const float2 t = ffma2(make_float2(sv[x], sv[x + 1]), sl2x2, nl[e]);
+          float p0 = fast_exp2(t.x), p1 = fast_exp2(t.y);
+          if (need_mask) {
+            if (key_rel > qrow0 + c0 + x) p0 = 0.f;
+            if (key_rel > qrow0 + c0 + x + 1) p1 = 0.f;
+          }
+          const float2 u = ffma2(make_float2(dp[x], dp[x + 1]), scx2, nd[e]);
+          const float2 dd = fmul2(u, make_float2(p0, p1));
+          pk[x / 2] = pack_bf16(p0, p1);
+          dk[x / 2] = pack_bf16(dd.x, dd.y);
         }
-        pk[x / 2] = pack_bf16(pp[0], pp[1]);
-        dk[x / 2] = pack_bf16(dd[0], dd[1]);
       }
       if (tl) TR(6, j);
       if (j > 0) mbar_wait(&ctl.pds_free, (j - 1) & 1);
@@ -296,12 +293,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       mbar_arrive(&ctl.pds_ready);
       if (tl) TR(8, j);
-      if (j > 0) drain_store(j - 1);
-      if (tl) TR(9, j);
+
     }
     if (n_pairs > 0) {
-      drain_load(n_pairs - 1);
-      drain_store(n_pairs - 1);
       // dK / dV (lane r = key, 128 cols each) += into the fp32 chunk accumulators
       mbar_wait(&ctl.acc_done, 0);
       tc_fence_after();
@@ -320,8 +314,60 @@ __global__ void __launch_bounds__(kThreads, 1)
           g4[x] = make_float4(o.x + a[4 * x], o.y + a[4 * x + 1], o.z + a[4 * x + 2], o.w + a[4 * x + 3]);
         }
       }
-      if (ctid == 0) bulk_wait<0>();
     }
+    tc_fence_before();
+  } else {
+    // --------------------------------------------- dQ drain (one warpgroup)
+    // dQ^T of pair jj sits in its consumed dP^T columns (lane = head dim d,
+    // columns = the pair's 64 queries): TMEM -> registers (frees the columns
+    // for the S/dP of pair jj+2) -> smem stage [q][d] -> TMA reduce-add.
+    const int quarter = warp & 3;
+    const int d = quarter * 32 + lane;
+    const int dtid = (warp - 10) * 32 + lane;
+    const uint32_t lane_off = uint32_t(quarter * 32) << 16;
+    for (int jj = 0; jj < n_pairs; ++jj) {
+      const int bb = jj & 1;
+      const bool tl = tracing && dtid == 0;
+      mbar_wait(&ctl.dq_full[bb], (jj >> 1) & 1);
+      if (tl) TR(4, jj);
+      tc_fence_after();
+      float a0[32], a1[32];
+      tmem_ld32(tmem + lane_off + bb * 128 + 64, a0);
+      tmem_ld32(tmem + lane_off + bb * 128 + 96, a1);
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(&ctl.dq_free[bb]);
+      if (prm.dbg & 1) continue;
+      if (prm.dq_red) {
+        // lanes of a warp hold 32 consecutive head dims of one query row:
+        // every red.global is one coalesced 128-byte L2 reduction
+        float* g = prm.dq + int64_t(pair_row(jj)) * (int64_t(prm.group) * prm.acc_stride) + pair_head(jj) * D + d;
+        const int64_t rs = int64_t(prm.group) * prm.acc_stride;
+#pragma unroll
+        for (int x = 0; x < 32; ++x) {
+          asm volatile("red.global.add.f32 [%0], %1;" ::"l"(g + x * rs), "f"(a0[x]) : "memory");
+          asm volatile("red.global.add.f32 [%0], %1;" ::"l"(g + (32 + x) * rs), "f"(a1[x]) : "memory");
+        }
+        if (tl) TR(9, jj);
+        continue;
+      }
+      if (dtid == 0) bulk_wait_read<0>();  // the previous reduce has read the stage
+      named_bar_sync(1, kDrain);
+      const uint32_t st = smem_u32(sm.stage[0]) + uint32_t(d) * 4u;
+#pragma unroll
+      for (int x = 0; x < 32; ++x) {
+        asm volatile("st.shared.f32 [%0], %1;" ::"r"(st + x * D * 4), "f"(a0[x]) : "memory");
+        asm volatile("st.shared.f32 [%0], %1;" ::"r"(st + (32 + x) * D * 4), "f"(a1[x]) : "memory");
+      }
+      fence_async_smem();
+      named_bar_sync(2, kDrain);
+      if (tl) TR(9, jj);
+      if (dtid == 0) {
+        tma_reduce_add_2d(&tm_dq, sm.stage[0], pair_head(jj) * D, pair_row(jj));
+        bulk_commit();
+      }
+    }
+    if (dtid == 0) bulk_wait<0>();
     tc_fence_before();
   }
   __syncthreads();
@@ -352,6 +398,8 @@ int attn_bwd_d128(const void* q, int64_t q_rows, int64_t q_stride, const void* k
   prm.delta = delta;
   prm.dk = dk_acc;
   prm.dv = dv_acc;
+  prm.dq = dq_acc;
+  prm.dq_red = getenv("SP_BWD_DQ_RED") ? 1 : 0;  // measured slower: L2 atomics at 64 per thread per pair
   prm.acc_stride = int64_t(kv_heads) * D;
   prm.trace = getenv("SP_BWD_TRACE") != nullptr;
   prm.dbg = getenv("SP_BWD_DBG") ? atoi(getenv("SP_BWD_DBG")) : 0;

@@ -20,7 +20,7 @@ lib = native.lib()
 lib.sp_debug_bwd_trace(buf)
 t = np.array(buf[:], dtype=np.int64).reshape(12, 512)
 t = t - t[0, 0]
-names = ["mma_top", "sdp_issued", "pds_ready_ok", "mma_done", "drain_ld_ok", "sdp_full_ok", "compute_done", "pds_free_ok", "pds_ready_arr", "drain_st_done", "qfull_ok", "dqfree_ok"]
+names = ["mma_top", "sdp_issued", "pds_ready_ok", "mma_done", "drain_dqfull_ok(j)", "sdp_full_ok", "compute_done", "pds_free_ok", "pds_ready_arr", "drain_staged(j)", "qfull_ok", "dqfree_ok"]
 for j in [1, 2, 3, 50, 51, 52, 100, 101, 200]:
     print(j, " ".join(f"{names[e]}={t[e, j]}" for e in range(12)))
 per = np.diff(t[0, 10:250])
