@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--seq-len", type=int, default=131072)
     ap.add_argument("--slices", type=int, default=8)
     ap.add_argument("--microbatches", type=int, default=4)
+    ap.add_argument("--recompute", choices=["selective", "full"], default="selective",
+                    help="selective: the forward stashes attention O/LSE, the backward recomputes the rest")
     ap.add_argument("--exchange", choices=["off", "on", "early"], default="off",
                     help="attention workload redistribution (reference ExchangeMode); no effect at PP=1")
     ap.add_argument("--no-e2e", action="store_true")
@@ -70,12 +72,13 @@ def parse():
 def make_cfg(args, world):
     from paper_2504_14519_b200.runtime import StepConfig
     return StepConfig.c2(layers=args.layers, seq_len=args.seq_len, slices=args.slices,
-                         microbatches=args.microbatches, pp=world, exchange=args.exchange)
+                         microbatches=args.microbatches, pp=world, exchange=args.exchange,
+                         recompute=args.recompute)
 
 
 def workload_name(cfg):
     return (f"c2 Llama-7B layer shapes x{cfg.layers} layers, {cfg.seq_len // 1024}K ctx, n={cfg.slices} slices, "
-            f"m={cfg.microbatches}, PP={cfg.pp}, exchange={cfg.exchange}")
+            f"m={cfg.microbatches}, PP={cfg.pp}, exchange={cfg.exchange}, recompute={cfg.recompute}")
 
 
 # ----------------------------------------------------------------- clocks
@@ -344,7 +347,7 @@ def main():
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic tokens, random-init weights",
             "config": {"workload": workload_name(cfg), "model": "llama-7b-shapes", "layers": cfg.layers,
                        "global_batch": cfg.microbatches, "seq_len": cfg.seq_len, "slices": cfg.slices,
-                       "parallelism": f"pp{world}", "exchange": cfg.exchange,
+                       "parallelism": f"pp{world}", "exchange": cfg.exchange, "recompute": cfg.recompute,
                        "l2": "inputs larger than L2 (per-step working set tens of GB)"},
             "mfu": mfu, "mfu_nominal": mfu_nominal, "mfu_peak_tflops": peak_tf,
             "bubble_fraction": bubble,

@@ -136,13 +136,20 @@ int sp_attn_merge(const void* o_a, const float* lse_a, const void* o_b, const fl
  * embedding on stage 1, final norm + LM head + cross entropy on stage pp).
  * Weights are bf16 (fp32 master + AdamW), random-initialised N(0, 0.02)
  * from `seed`.  The slot arena holds ledger-peak slots of (stage input +
- * per-layer K/V) — reference simulator.cpp:311-346. */
+ * per-layer K/V [+ per-layer attention O/LSE when recompute = 0]) —
+ * reference simulator.cpp:311-346. */
 typedef struct {
   int32_t layers, hidden, ffn_hidden, heads, kv_heads, head_dim, vocab;
   int32_t microbatches, slices, pp, rank, exchange_mode;
   int64_t seq_len;
   float rope_theta, norm_eps, lr;
   uint64_t seed;
+  /* 0 = selective (default): the forward pass stashes each layer's attention
+   * output O and LSE in the slot, the backward pass recomputes everything
+   * else (norms, GEMMs, RoPE, SwiGLU) but not K1;  1 = full: only the stage
+   * input is stashed and K1 runs again in the backward (reference Full
+   * checkpointing, workload.cpp:100-104). */
+  int32_t recompute;
 } sp_model_config;
 
 #define SP_STEP_NO_OPTIMIZER 1

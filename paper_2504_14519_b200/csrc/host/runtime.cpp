@@ -9,8 +9,10 @@
 //              rows of the layer's KV pool) -> K1 sliced attention over the
 //              slots of slices 1..i -> O GEMM + residual -> RMSNorm -> gate/up
 //              GEMM -> SwiGLU -> down GEMM + residual; send to s+1.
-//   BW(k,i,s): full recompute of the stage from the stashed input (Full
-//              checkpointing, reference workload.cpp:100-104), then the layer
+//   BW(k,i,s): recompute of the stage from the stashed input — every op but
+//              K1, whose O/LSE the forward stashed in the slot (selective;
+//              cfg.recompute = 1: full, K1 again, reference Full
+//              checkpointing workload.cpp:100-104), then the layer
 //              backward in reverse with K2 accumulating dK/dV of chunks 1..i
 //              into fp32 chunk accumulators (complete for chunk i now, since
 //              slices n..i+1 ran before: schedule.cpp:125-126), LM head + loss
@@ -63,6 +65,8 @@ struct LayerParams {
 struct LayerWs {
   bf16raw *x_in, *xn, *q, *o, *x_mid, *xn2, *gu, *act;
   float *lse, *rstd1, *rstd2;
+  bf16raw* o_ws;  // workspace O/LSE (full recompute); o/lse point at the slot's stash otherwise
+  float* lse_ws;
 };
 
 struct PassTime {
@@ -97,6 +101,9 @@ class Runtime {
   int slots = 0;
   bf16raw* x_pool = nullptr;
   std::vector<bf16raw*> k_pool, v_pool;
+  bool stash = true;                // selective recompute: attention O/LSE live in the slot
+  std::vector<bf16raw*> o_pool;     // [slots*Ls][qd] per layer
+  std::vector<float*> lse_pool;     // [slots][heads][Ls] per layer
   std::vector<int> free_slots;
   std::map<std::pair<int, int>, int> slot_of;
   int slots_in_use = 0, slots_high_water = 0;
@@ -208,6 +215,8 @@ class Runtime {
     if (c.hidden != c.heads * c.head_dim) return set_error(SP_ERR_INVALID, "hidden != heads * head_dim");
     Lps = c.layers / p;
     Ls = c.seq_len / c.slices;
+    if (c.recompute != 0 && c.recompute != 1) return set_error(SP_ERR_INVALID, "recompute must be 0 or 1");
+    stash = c.recompute == 0;
     h = c.hidden;
     H = c.ffn_hidden;
     qd = int64_t(c.heads) * c.head_dim;
@@ -486,7 +495,10 @@ class Runtime {
       }
       return SP_OK;
     };
-    for (int l = 0; l < Lps; ++l) SP_TRY(fwd_layer());
+    // backward ticks: the peer's recompute needs the forward partials again
+    // only under full recompute (selective reuses its stashed O/LSE)
+    if (c == 0 || !stash)
+      for (int l = 0; l < Lps; ++l) SP_TRY(fwd_layer());
     if (c == 1)
       for (int l = Lps - 1; l >= 0; --l) SP_TRY(bwd_layer());
     return SP_OK;
@@ -547,6 +559,14 @@ class Runtime {
   int alloc_arena() {
     const int64_t rows = int64_t(slots) * Ls;
     SP_TRY(alloc(&x_pool, rows * h));
+    if (stash) {
+      o_pool.assign(Lps, nullptr);
+      lse_pool.assign(Lps, nullptr);
+      for (int l = 0; l < Lps; ++l) {
+        SP_TRY(alloc(&o_pool[l], rows * qd));
+        SP_TRY(alloc(&lse_pool[l], rows * cfg.heads));
+      }
+    }
     k_pool.assign(Lps, nullptr);
     v_pool.assign(Lps, nullptr);
     dk_acc.assign(Lps, nullptr);
@@ -572,12 +592,14 @@ class Runtime {
       SP_TRY(alloc(&x.x_in, Ls * h));
       SP_TRY(alloc(&x.xn, Ls * h));
       SP_TRY(alloc(&x.q, Ls * qd));
-      SP_TRY(alloc(&x.o, Ls * qd));
+      SP_TRY(alloc(&x.o_ws, Ls * qd));
+      x.o = x.o_ws;
       SP_TRY(alloc(&x.x_mid, Ls * h));
       SP_TRY(alloc(&x.xn2, Ls * h));
       SP_TRY(alloc(&x.gu, Ls * 2 * H));
       SP_TRY(alloc(&x.act, Ls * H));
-      SP_TRY(alloc(&x.lse, int64_t(cfg.heads) * Ls));
+      SP_TRY(alloc(&x.lse_ws, int64_t(cfg.heads) * Ls));
+      x.lse = x.lse_ws;
       SP_TRY(alloc(&x.rstd1, Ls));
       SP_TRY(alloc(&x.rstd2, Ls));
     }
@@ -674,16 +696,24 @@ class Runtime {
     return SP_OK;
   }
 
-  int layer_forward(int l, int k, int i, bf16raw* x_out, const PassX* px) {
+  // attention output of layer l for slice (k, i): the slot's stash or the workspace
+  void bind_attn_out(int l, int slot) {
+    LayerWs& x = ws[l];
+    x.o = stash ? o_pool[l] + int64_t(slot) * Ls * qd : x.o_ws;
+    x.lse = stash ? lse_pool[l] + int64_t(slot) * cfg.heads * Ls : x.lse_ws;
+  }
+
+  int layer_forward(int l, int k, int i, bf16raw* x_out, const PassX* px, bool recompute) {
     LayerWs& x = ws[l];
     const LayerParams& P = lp[l];
     const int slot = slot_of.at({k, i});
+    bind_attn_out(l, slot);
     const int64_t pos0 = int64_t(i - 1) * Ls;
     SP_TRY(rmsnorm_fwd(x.x_in, W(P.attn_norm), x.xn, x.rstd1, Ls, int(h), cfg.norm_eps, comp));
     SP_TRY(gemm(false, true, Ls, qkv_w, h, x.xn, h, W(P.wqkv), h, qkv, qkv_w, false, 1.f, 0.f, comp));
     SP_TRY(rope_qkv_fwd(qkv, Ls, cfg.heads, cfg.kv_heads, cfg.head_dim, pos0, rope_cos, rope_sin, x.q, qd,
                         k_pool[l] + int64_t(slot) * Ls * kvd, v_pool[l] + int64_t(slot) * Ls * kvd, kvd, comp));
-    SP_TRY(attention_forward(l, k, i, x, px));
+    if (!(recompute && stash)) SP_TRY(attention_forward(l, k, i, x, px));
     SP_CUDA(cudaMemcpyAsync(x.x_mid, x.x_in, Ls * h * 2, cudaMemcpyDeviceToDevice, comp));
     SP_TRY(gemm(false, true, Ls, h, qd, x.o, qd, W(P.wo), qd, x.x_mid, h, false, 1.f, 1.f, comp));
     SP_TRY(rmsnorm_fwd(x.x_mid, W(P.mlp_norm), x.xn2, x.rstd2, Ls, int(h), cfg.norm_eps, comp));
@@ -695,8 +725,8 @@ class Runtime {
   }
 
   // Stage forward of slice (k,i) from ws[0].x_in; final output to `out`.
-  int stage_forward(int k, int i, bf16raw* out, const PassX* px) {
-    for (int l = 0; l < Lps; ++l) SP_TRY(layer_forward(l, k, i, l + 1 < Lps ? ws[l + 1].x_in : out, px));
+  int stage_forward(int k, int i, bf16raw* out, const PassX* px, bool recompute) {
+    for (int l = 0; l < Lps; ++l) SP_TRY(layer_forward(l, k, i, l + 1 < Lps ? ws[l + 1].x_in : out, px, recompute));
     return SP_OK;
   }
 
@@ -730,7 +760,7 @@ class Runtime {
       const int b = out_idx;
       out_idx ^= 1;
       SP_CUDA(cudaStreamWaitEvent(comp, ev_out_free[b], 0));
-      SP_TRY(stage_forward(k, i, out_buf[b], px));
+      SP_TRY(stage_forward(k, i, out_buf[b], px, false));
       cudaEvent_t done;
       SP_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
       SP_CUDA(cudaEventRecord(done, comp));
@@ -739,12 +769,13 @@ class Runtime {
       SP_CUDA(cudaEventRecord(ev_out_free[b], s_act_out));
       cudaEventDestroy(done);
     } else {
-      SP_TRY(stage_forward(k, i, x_final, px));
+      SP_TRY(stage_forward(k, i, x_final, px, false));
     }
     return SP_OK;
   }
 
   int layer_backward(int l, int k, int i, bf16raw* dx, const PassX* px) {
+    bind_attn_out(l, slot_of.at({k, i}));
     LayerWs& x = ws[l];
     const LayerParams& P = lp[l];
     const int64_t pos0 = int64_t(i - 1) * Ls;
@@ -852,7 +883,7 @@ class Runtime {
     bf16raw* top = stage < p ? tmp_h : x_final;
     if (stage == p) {
       SP_CUDA(cudaStreamWaitEvent(comp, ev_gout_free[gout_idx], 0));
-      SP_TRY(stage_forward(k, i, x_final, px));
+      SP_TRY(stage_forward(k, i, x_final, px, true));
       // LM head + cross entropy
       const int64_t V = cfg.vocab;
       SP_TRY(rmsnorm_fwd(x_final, W(final_norm), xf, rstd_f, Ls, int(h), cfg.norm_eps, comp));
@@ -863,7 +894,7 @@ class Runtime {
       SP_TRY(gemm(true, false, V, h, Ls, dlogits, V, xf, h, G(head), h, true, 1.f, 1.f, comp));        // dWhead
       SP_TRY(rmsnorm_bwd(tmp_h, x_final, W(final_norm), rstd_f, nullptr, dx, G(final_norm), Ls, int(h), comp));
     } else {
-      SP_TRY(stage_forward(k, i, top, px));
+      SP_TRY(stage_forward(k, i, top, px, true));
     }
     for (int l = Lps - 1; l >= 0; --l) SP_TRY(layer_backward(l, k, i, dx, px));
     if (stage == 1) {
@@ -1044,7 +1075,8 @@ int sp_runtime_memory(void* handle, int64_t* out7) {
   Runtime* rt = static_cast<Runtime*>(handle);
   out7[0] = rt->slots;
   out7[1] = rt->slots_high_water;
-  out7[2] = rt->Ls * rt->h * 2 + int64_t(rt->Lps) * 2 * rt->Ls * rt->kvd * 2;
+  out7[2] = rt->Ls * rt->h * 2 + int64_t(rt->Lps) * 2 * rt->Ls * rt->kvd * 2 +
+            (rt->stash ? int64_t(rt->Lps) * rt->Ls * (rt->qd * 2 + int64_t(rt->cfg.heads) * 4) : 0);
   out7[3] = rt->ledger.per_device[rt->rank].peak_activation_units;
   out7[4] = int64_t(rt->bytes_allocated);
   out7[5] = rt->n_params;

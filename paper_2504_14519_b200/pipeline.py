@@ -64,9 +64,12 @@ def exchange_plan(sched: dict, ann: dict, rank: int) -> dict[int, dict]:
     return plan
 
 
-def exchange_messages(sched: dict, ann: dict, rank: int, layers: int) -> dict[int, list[tuple]]:
+def exchange_messages(sched: dict, ann: dict, rank: int, layers: int,
+                      recompute: str = "selective") -> dict[int, list[tuple]]:
     """Ordered (op, peer, tag) per exchange communicator (class 0: forward
-    ticks, 1: backward ticks) in the order this rank posts them."""
+    ticks, 1: backward ticks) in the order this rank posts them.  Backward
+    ticks carry the recompute's forward partials only under full recompute
+    (selective recompute reuses the stashed attention output)."""
     xp = exchange_plan(sched, ann, rank)
     msgs: dict[int, list[tuple]] = {0: [], 1: []}
     for ps in device_passes(sched, rank):
@@ -74,7 +77,9 @@ def exchange_messages(sched: dict, ann: dict, rank: int, layers: int) -> dict[in
         if e is None:
             continue
         c = e["cls"]
-        phases = [("fwd", l) for l in range(layers)] + ([("bwd", l) for l in reversed(range(layers))] if c else [])
+        fwd = c == 0 or recompute == "full"
+        phases = ([("fwd", l) for l in range(layers)] if fwd else []) + \
+            ([("bwd", l) for l in reversed(range(layers))] if c else [])
         if e["in"]:  # receiver: posted at pass start, per layer and transfer: recv -> partial -> send back
             for phase, l in phases:
                 for peer, _i_src, chunks in e["in"]:

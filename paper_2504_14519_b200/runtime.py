@@ -24,7 +24,10 @@ class _Cfg(C.Structure):
     _fields_ = [(n, C.c_int32) for n in ("layers", "hidden", "ffn_hidden", "heads", "kv_heads", "head_dim", "vocab",
                                          "microbatches", "slices", "pp", "rank", "exchange_mode")] + [
         ("seq_len", C.c_int64), ("rope_theta", C.c_float), ("norm_eps", C.c_float), ("lr", C.c_float),
-        ("seed", C.c_uint64)]
+        ("seed", C.c_uint64), ("recompute", C.c_int32)]
+
+
+RECOMPUTE = {"selective": 0, "full": 1}
 
 
 @dataclass(frozen=True)
@@ -40,6 +43,7 @@ class StepConfig:
     microbatches: int
     pp: int = 1
     exchange: str = "off"
+    recompute: str = "selective"  # "selective": stash attention O/LSE, "full": K1 again in the backward
     rope_theta: float = 10000.0
     norm_eps: float = 1e-5
     lr: float = 1e-4
@@ -77,7 +81,7 @@ class StepConfig:
     def to_c(self, rank: int) -> _Cfg:
         return _Cfg(self.layers, self.hidden, self.ffn_hidden, self.heads, self.kv_heads, self.head_dim, self.vocab,
                     self.microbatches, self.slices, self.pp, rank, N.MODES[self.exchange], self.seq_len,
-                    self.rope_theta, self.norm_eps, self.lr, self.seed)
+                    self.rope_theta, self.norm_eps, self.lr, self.seed, RECOMPUTE[self.recompute])
 
     # ---- accounting ----
     def linear_params_per_layer(self) -> int:

@@ -12,14 +12,18 @@ pytestmark = pytest.mark.gpu
 ROOT = Path(__file__).resolve().parents[1]
 
 
-@pytest.mark.parametrize("pp,m,n,x", [(2, 2, 4, "off"), (2, 1, 2, "off"), (2, 2, 4, "on"), (2, 2, 8, "early"),
-                                      (2, 3, 4, "on"), (4, 2, 4, "off"), (4, 2, 8, "on"), (4, 2, 8, "early")])
-def test_pipeline_parallel_step_matches_oracle(pp, m, n, x):
+@pytest.mark.parametrize("pp,m,n,x,rc", [(2, 2, 4, "off", "selective"), (2, 1, 2, "off", "full"),
+                                         (2, 2, 4, "on", "selective"), (2, 2, 4, "on", "full"),
+                                         (2, 2, 8, "early", "selective"), (2, 3, 4, "on", "selective"),
+                                         (4, 2, 4, "off", "selective"), (4, 2, 8, "on", "selective"),
+                                         (4, 2, 8, "early", "full")])
+def test_pipeline_parallel_step_matches_oracle(pp, m, n, x, rc):
     if not torch.cuda.is_available() or torch.cuda.device_count() < pp:
         pytest.skip(f"needs {pp} GPUs")
-    env = dict(os.environ, SP_M=str(m), SP_N=str(n), SP_X=x)
+    env = dict(os.environ, SP_M=str(m), SP_N=str(n), SP_X=x, SP_RC=rc)
+    port = 29500 + pp * 100 + m * 10 + n + len(x) + (50 if rc == "full" else 0)
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={pp}",
-                        "--master-addr", "127.0.0.1", "--master-port", str(29500 + pp * 100 + m * 10 + n + len(x)),
+                        "--master-addr", "127.0.0.1", "--master-port", str(port),
                         str(ROOT / "tests" / "mp_step_check.py")], env=env, capture_output=True, text=True,
                        timeout=600)
     print(r.stdout[-3000:], r.stderr[-3000:])

@@ -31,7 +31,8 @@ def _worker(rank, world, port, cases, q):
         results = []
         for (m, n, mode, layers) in cases:
             sched, ann = PL.schedule_and_annotation(world, m, n, mode)
-            mine = {"stage": PL.stage_messages(sched, rank), "x": PL.exchange_messages(sched, ann, rank, layers)}
+            rc = "full" if (m + n) % 2 else "selective"  # both recompute policies' exchange programs
+            mine = {"stage": PL.stage_messages(sched, rank), "x": PL.exchange_messages(sched, ann, rank, layers, rc)}
             allv = [None] * world
             dist.all_gather_object(allv, mine)
             if rank == 0:

@@ -53,12 +53,12 @@ def _pull(step, cfg):
     return W
 
 
-@pytest.mark.parametrize("m,n", [(2, 4), (1, 2)])
-def test_c1_step_matches_oracle(m, n):
+@pytest.mark.parametrize("m,n,rc", [(2, 4, "selective"), (1, 2, "selective"), (2, 4, "full")])
+def test_c1_step_matches_oracle(m, n, rc):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     from paper_2504_14519_b200.runtime import SlimPipeStep, StepConfig
-    cfg = StepConfig.c1(microbatches=m, slices=n)
+    cfg = StepConfig.c1(microbatches=m, slices=n, recompute=rc)
     step = SlimPipeStep(cfg, rank=0, world=1)
     tok, tgt = _data(cfg)
     loss = step.step(tok, tgt, optimizer=False)
