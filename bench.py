@@ -55,10 +55,12 @@ def parse():
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--layers", type=int, default=8)
-    ap.add_argument("--seq-len", type=int, default=131072)
-    ap.add_argument("--slices", type=int, default=8)
-    ap.add_argument("--microbatches", type=int, default=4)
+    ap.add_argument("--model", choices=["c2", "c3", "c4"], default="c2",
+                    help="BASELINE.json layer shapes: c2 Llama-7B, c3 Llama-13B, c4 Llama-70B (GQA 64/8)")
+    ap.add_argument("--layers", type=int, default=None, help="default: c2 8, c3 8, c4 2")
+    ap.add_argument("--seq-len", type=int, default=None, help="default: c2 128K, c3 256K, c4 1M")
+    ap.add_argument("--slices", type=int, default=None, help="default: c2 8, c3 16, c4 32")
+    ap.add_argument("--microbatches", type=int, default=None, help="default: c2 4, c3 4, c4 1")
     ap.add_argument("--recompute", choices=["selective", "full"], default="selective",
                     help="selective: the forward stashes attention O/LSE, the backward recomputes the rest")
     ap.add_argument("--exchange", choices=["off", "on", "early"], default="off",
@@ -69,15 +71,22 @@ def parse():
     return ap.parse_args()
 
 
+MODEL_NAMES = {"c2": ("c2 Llama-7B", "llama-7b-shapes"), "c3": ("c3 Llama-13B", "llama-13b-shapes"),
+               "c4": ("c4 Llama-70B GQA", "llama-70b-shapes")}
+DEPTH = {"c2": 8, "c3": 8, "c4": 2}  # reduced depth (BASELINE.json: "reduced depth")
+
+
 def make_cfg(args, world):
     from paper_2504_14519_b200.runtime import StepConfig
-    return StepConfig.c2(layers=args.layers, seq_len=args.seq_len, slices=args.slices,
-                         microbatches=args.microbatches, pp=world, exchange=args.exchange,
-                         recompute=args.recompute)
+    base = getattr(StepConfig, args.model)()
+    kw = {k: v for k, v in (("layers", args.layers or DEPTH[args.model]), ("seq_len", args.seq_len),
+                            ("slices", args.slices), ("microbatches", args.microbatches)) if v is not None}
+    return base.__class__(**{**base.__dict__, **kw, "pp": world, "exchange": args.exchange,
+                             "recompute": args.recompute})
 
 
-def workload_name(cfg):
-    return (f"c2 Llama-7B layer shapes x{cfg.layers} layers, {cfg.seq_len // 1024}K ctx, n={cfg.slices} slices, "
+def workload_name(cfg, model="c2"):
+    return (f"{MODEL_NAMES[model][0]} layer shapes x{cfg.layers} layers, {cfg.seq_len // 1024}K ctx, n={cfg.slices} slices, "
             f"m={cfg.microbatches}, PP={cfg.pp}, exchange={cfg.exchange}, recompute={cfg.recompute}")
 
 
@@ -191,7 +200,7 @@ def run_reference(args):
     line = {"metric": "tokens/s", "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": workload_name(cfg), "global_batch": cfg.microbatches, "seq_len": cfg.seq_len,
+            "config": {"workload": workload_name(cfg, args.model), "global_batch": cfg.microbatches, "seq_len": cfg.seq_len,
                        "parallelism": f"pp{cfg.pp}"},
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": base["cores"], "kind": base["kind"],
                              "sample": base["sample"]},
@@ -345,7 +354,7 @@ def main():
             "metric": "tokens/s", "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic tokens, random-init weights",
-            "config": {"workload": workload_name(cfg), "model": "llama-7b-shapes", "layers": cfg.layers,
+            "config": {"workload": workload_name(cfg, args.model), "model": MODEL_NAMES[args.model][1], "layers": cfg.layers,
                        "global_batch": cfg.microbatches, "seq_len": cfg.seq_len, "slices": cfg.slices,
                        "parallelism": f"pp{world}", "exchange": cfg.exchange, "recompute": cfg.recompute,
                        "l2": "inputs larger than L2 (per-step working set tens of GB)"},
