@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "pipelab/attention.hpp"
+#include "pipelab/analytics.hpp"
 #include "pipelab/exchange.hpp"
 #include "pipelab/schedule.hpp"
 #include "pipelab/simulator.hpp"
@@ -198,6 +199,28 @@ char* ref_activation_json(const int64_t* model, const int64_t* par, const int64_
        << ",\"logits_slice\":" << rat(mm.logits_slice_bytes)
        << ",\"exchange_slice\":" << rat(mm.exchange_slice_bytes) << "}";
     return dup(os.str());
+  } catch (const std::exception& e) {
+    return error_json("invalid_argument", e);
+  }
+}
+
+// The reference's closed forms (analytics.cpp:11-112), same JSON layout as
+// sp_plan_analytics_json.
+char* ref_analytics_json(int scheme, int64_t p, int64_t m, int64_t n, int64_t v, int64_t ma_num, int64_t ma_den) {
+  try {
+    const Scheme sc = Scheme(scheme);
+    std::string j = "{\"accepts\":" + std::string(scheme_accepts(sc, p, m, n, v) ? "true" : "false");
+    j += ",\"form_valid\":" + std::string(memory_form_valid(sc, p, m, n, v) ? "true" : "false");
+    j += ",\"memory\":" + rat(memory_multiplier(sc, p, m, n, v));
+    const BubbleBound b = bubble_bounds(sc, p, m, n, v);
+    if (b.exact) j += ",\"bubble\":" + rat(*b.exact);
+    if (b.interval) j += ",\"bubble_lo\":" + rat(b.interval->first) + ",\"bubble_hi\":" + rat(b.interval->second);
+    j += ",\"upper_only\":" + std::string(b.upper_bound_only ? "true" : "false");
+    if (sc == Scheme::SlimPipe) {
+      j += ",\"attention_bubble\":" + rat(slim_attention_bubble(p, m, n, v));
+      if (n >= p) j += ",\"acc_memory\":" + rat(slim_acc_memory(p, n, Rat(ma_num, ma_den)));
+    }
+    return dup(j + "}");
   } catch (const std::exception& e) {
     return error_json("invalid_argument", e);
   }

@@ -9,6 +9,7 @@
 #include <sstream>
 #include <string>
 
+#include "pipelab/analytics.hpp"
 #include "pipelab/exchange.hpp"
 #include "pipelab/schedule.hpp"
 #include "pipelab/simulator.hpp"
@@ -201,6 +202,27 @@ int sp_plan_activation_json(const int64_t* model, const int64_t* par, const int6
        << ",\"logits_slice\":" << q(mm.logits_slice_bytes) << ",\"exchange_slice\":" << q(mm.exchange_slice_bytes)
        << "}";
     return os.str();
+  });
+}
+
+// Closed forms of analytics.hpp for one (scheme, p, m, n, v): JSON with the
+// rationals as "num/den" strings.
+int sp_plan_analytics_json(int scheme, int64_t p, int64_t m, int64_t n, int64_t v, int64_t ma_num, int64_t ma_den,
+                           char** out) {
+  return guarded(out, [&] {
+    const Scheme sc = Scheme(scheme);
+    std::string j = "{\"accepts\":" + std::string(scheme_accepts(sc, p, m, n, v) ? "true" : "false");
+    j += ",\"form_valid\":" + std::string(memory_form_valid(sc, p, m, n, v) ? "true" : "false");
+    j += ",\"memory\":" + q(memory_multiplier(sc, p, m, n, v));
+    const BubbleBound b = bubble_bounds(sc, p, m, n, v);
+    if (b.exact) j += ",\"bubble\":" + q(*b.exact);
+    if (b.interval) j += ",\"bubble_lo\":" + q(b.interval->first) + ",\"bubble_hi\":" + q(b.interval->second);
+    j += ",\"upper_only\":" + std::string(b.upper_bound_only ? "true" : "false");
+    if (sc == Scheme::SlimPipe) {
+      j += ",\"attention_bubble\":" + q(slim_attention_bubble(p, m, n, v));
+      if (n >= p) j += ",\"acc_memory\":" + q(slim_acc_memory(p, n, Rat(ma_num, ma_den)));
+    }
+    return j + "}";
   });
 }
 

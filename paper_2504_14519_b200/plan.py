@@ -88,6 +88,18 @@ def exchange_volume(p: int, n: int, layers: int, mh: Fraction) -> dict[str, Frac
     return {k: Fraction(v) for k, v in d.items()}
 
 
+SCHEMES = {"gpipe": 0, "terapipe": 1, "1f1b": 2, "interleaved": 3, "zbv": 4, "vhalf": 5, "slimpipe": 6}
+
+
+def analytics(scheme: str, p: int, m: int, n: int, v: int, ma: Fraction = Fraction(1)) -> dict:
+    """Closed forms of analytics.hpp (reference analytics.cpp:11-112): memory
+    multiplier, bubble bound, validity domain, SlimPipe attention asymptote and
+    accumulated memory (for M_a = ma)."""
+    ma = Fraction(ma)
+    d = json.loads(N._json_call("sp_plan_analytics_json", SCHEMES[scheme], p, m, n, v, ma.numerator, ma.denominator))
+    return {k: (Fraction(x) if isinstance(x, str) else x) for k, x in d.items()}
+
+
 def simulate_text(p: int, v: int, m: int, n: int, mode: str = "off", cost=(1.0, 0.0, 2.0, 1.0), comm=(0.0, 0.0),
                   seq_len: int | None = None, mem_rats=None) -> str:
     seq_len = n if seq_len is None else seq_len

@@ -154,6 +154,26 @@ def test_activation_and_volume_match_live_reference():
         assert mine == ref
 
 
+@needs_ref
+def test_analytics_closed_forms_match_live_reference():
+    """memory_multiplier / slim_acc_memory / memory_form_valid
+    (+ bubble bounds) byte-identical to the compiled reference over a grid."""
+    n_checked = 0
+    for scheme, sid in P.SCHEMES.items():
+        for p in (1, 2, 3, 4, 8):
+            for m in (1, 2, 3, 4, 8, 16):
+                for n in (1, 2, 4, 8, 16, 32):
+                    for v in (1, 2, 3):
+                        ref = O.ref_text("ref_analytics_json", sid, p, m, n, v, 1 << 30, 7)
+                        mine = N._json_call("sp_plan_analytics_json", sid, p, m, n, v, 1 << 30, 7)
+                        assert mine == ref, (scheme, p, m, n, v, mine, ref)
+                        n_checked += 1
+    assert n_checked > 3000
+    # the arena sizing the executor relies on: SlimPipe peak = 1/p + 2(p-1)/(n v p)
+    a = P.analytics("slimpipe", 8, 4, 16, 1)
+    assert a["memory"] == Fraction(1, 8) + Fraction(14, 128) and a["form_valid"]
+
+
 # ---- the reference's own pinned values --------------------------------------
 
 def _trace(sched, d):
