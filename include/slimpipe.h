@@ -129,6 +129,15 @@ int sp_attn_bwd_core(const void* q, int64_t q_rows, int64_t q_stride, const void
 int sp_attn_merge(const void* o_a, const float* lse_a, const void* o_b, const float* lse_b, int64_t rows,
                   int heads, int head_dim, int64_t o_stride, void* o_out, float* lse_out, sp_stream_t stream);
 
+/* Host fp64 entry of the pipelab attention API (include/pipelab/attention.hpp,
+ * reference attention.hpp:41-61) for one head: q [rows][d], k/v the chunks'
+ * rows concatenated, chunk_lens[n_chunks].  streamed = 0: chunk_attention;
+ * 1: accumulate_chunk per chunk + finalize.  Runs K1 on the current device.
+ * out [rows][d]; row_max / row_sumexp [rows] = the returned state. */
+int sp_host_chunk_attention(const double* q, int rows, int d, const double* k, const double* v,
+                            const int* chunk_lens, int n_chunks, int causal, int streamed, double* out,
+                            double* row_max, double* row_sumexp);
+
 /* ---------------------------------------------------------- step executor
  * One process (rank) per GPU; rank r runs pipeline stage r+1 of
  * gen_slimpipe(p=pp, v=1, m=microbatches, n=slices) (the drop-in planning

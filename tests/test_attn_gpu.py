@@ -150,3 +150,41 @@ def test_merge_matches_reference_merge_partials():
     torch.cuda.synchronize()
     assert torch.allclose(oi.float(), oa.float(), atol=1e-2)
     assert torch.equal(li, la)
+
+
+@pytest.mark.parametrize("d,rows,chunks,causal,streamed", [
+    (128, 256, [256, 256], True, False),      # slice 2 of a sliced sequence
+    (128, 256, [256, 256], True, True),       # same through accumulate_chunk + merge_partials + finalize
+    (128, 128, [128, 256, 128], True, False),  # unequal chunks (128-row pieces)
+    (64, 256, [256, 256, 256], True, True),
+    (128, 256, [256, 256], False, False),
+])
+def test_pipelab_attention_api_matches_oracle(d, rows, chunks, causal, streamed):
+    """include/pipelab/attention.hpp drop-in (fp64 host types, K1 underneath)
+    against the C restatement of chunk_attention (attention.cpp:94-111)."""
+    _need_gpu()
+    import ctypes as C
+    from paper_2504_14519_b200 import native as N
+    rng = np.random.default_rng(rows + d + len(chunks))
+    total = sum(chunks)
+    q = bf16_round(rng.uniform(-1, 1, (rows, d)))
+    k = bf16_round(rng.uniform(-1, 1, (total, d)))
+    v = bf16_round(rng.uniform(-1, 1, (total, d)))
+    ref_o, ref_lse, _, _ = O.port_chunk_attention(q, k, v, chunks, causal)
+    out = np.zeros((rows, d))
+    mx = np.zeros(rows)
+    sm = np.zeros(rows)
+    dp = C.POINTER(C.c_double)
+    f = N.lib().sp_host_chunk_attention
+    f.argtypes = [dp, C.c_int, C.c_int, dp, dp, C.POINTER(C.c_int), C.c_int, C.c_int, C.c_int, dp, dp, dp]
+    arr = lambda a: np.ascontiguousarray(a, dtype=np.float64).ctypes.data_as(dp)
+    rc = f(arr(q), rows, d, arr(k), arr(v), (C.c_int * len(chunks))(*chunks), len(chunks), int(causal), int(streamed),
+           out.ctypes.data_as(dp), mx.ctypes.data_as(dp), sm.ctypes.data_as(dp))
+    assert rc == 0, N.lib().sp_last_error()
+    assert max_rel_err(out, ref_o) < TOL_BF16
+    lse = mx + np.log(sm)  # the state's log-sum-exp, whatever stabiliser it carries
+    assert np.max(np.abs(lse - ref_lse)) < TOL_LSE
+    # unsupported shapes fail loudly (no CPU fallback)
+    rc = f(arr(q[:100]), 100, d, arr(k), arr(v), (C.c_int * len(chunks))(*chunks), len(chunks), int(causal), 0,
+           out.ctypes.data_as(dp), mx.ctypes.data_as(dp), sm.ctypes.data_as(dp))
+    assert rc == 1
