@@ -24,7 +24,7 @@
 // accumulator and each half rescales / finalises its own 64 O columns.
 //   TMEM: S_A [0,128) S_B [128,256) O_A [256,384) O_B [384,512) (fp32 cols);
 //         P_X (bf16, packed 2/col): half h writes keys [64h, 64h+64) over its
-//         own S columns [64h+32, 64h+64); PV_X reads both halves.
+//         own S columns [64h, 64h+32); PV_X reads both halves.
 //   UMMA order: S_A(0) S_B(0) | PV_A(0) S_A(1) | PV_B(0) S_B(1) | PV_A(1) ...
 //   The s_full commit after S_X(j+1) also covers PV_X(j) (in-order pipe), so
 //   when softmax X sees S_X(j+1) its O_X is stable and it may rescale it
@@ -33,7 +33,7 @@
 //   The two tiles take strict turns for their exponentials (named barriers),
 //   so MUFU serves one tile at a time while the tensor core runs the other.
 // Warps: 0-7 tile A (0-3 half 0, 4-7 half 1), 8-15 tile B, 16 TMA producer,
-// 17 TMEM owner + UMMA issuer.
+// 17 TMEM owner + UMMA issuer, 18-19 idle (complete the register warpgroup).
 #include <math.h>
 
 #include <cstdlib>
@@ -46,8 +46,14 @@ namespace sp {
 namespace {
 
 constexpr int D = 128, BM = 128, BN = 128, NK = 2, NV = 2;
-constexpr int kThreads = 576;
+constexpr int kThreads = 640;  // 16 softmax warps + warpgroup 4 (producer, UMMA, 2 idle)
 constexpr int kProducerWarp = 16, kMmaWarp = 17;
+// registers: 96/thread at launch (640 threads); warpgroup 4 shrinks to 32 and
+// the four softmax warpgroups grow to 112, enough to keep a 64-column S row
+// half in registers across the max exchange (one TMEM read of S per tile).
+// setmaxnreg sits at the top of each role's branch so ptxas never sees the
+// softmax code reachable under the small budget.
+constexpr int kRegsSide = 32, kRegsSoftmax = 112;
 constexpr int kSlab = 128 * 64;  // elements of one [128 rows][64] SW128 slab
 
 struct Params {
@@ -145,6 +151,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     return prm.chunk_row[key / prm.chunk_len] + key % prm.chunk_len;
   };
 
+  if (warp >= 16) {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kRegsSide));
   if (warp == kProducerWarp) {
     if (lane == 0) {
       mbar_arrive_expect_tx(&ctl.q_full, (has_b ? 2 : 1) * BM * D * 2);
@@ -187,8 +195,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       };
       auto issue_pv = [&](int x, int j) {
         const int v = j % NV;
-        // keys [16kk, +16): P of half kk/4 at S cols 64(kk/4) + 32 + 8(kk%4)
-        umma_bf16_ts_k128(tmem + 256 + x * 128, tmem + x * 128 + 32, 64, smem_desc_sw128(smem_u32(sm.v[v]), kSlab * 2, 1024),
+        // keys [16kk, +16): P of half kk/4 at S cols 64(kk/4) + 8(kk%4)
+        umma_bf16_ts_k128(tmem + 256 + x * 128, tmem + x * 128, 64, smem_desc_sw128(smem_u32(sm.v[v]), kSlab * 2, 1024),
                           id_o, j > 0 ? 1u : 0u);
         if (x == 1 || j >= n_b) umma_commit_warp(&ctl.v_empty[v]);
         if (j == nx[x] - 1) umma_commit_warp(&ctl.o_done[x]);
@@ -224,7 +232,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
+  }
   } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kRegsSoftmax));
     // ------------------------------- softmax: tile x, key half h, query row r
     const int x = warp >> 3;
     const int h = (warp >> 2) & 1;
@@ -242,26 +252,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       TRP(8 + 4 * x, j);
       tc_fence_after();
       const bool diag = prm.causal && j == nt - 1;  // key column c visible iff c <= r
-      // pass 1: partial row max over the own 64 columns, 32 at a time (the
-      // 96-register budget of 18 warps does not hold a 64-column row twice)
+      // S row half -> registers once (both loads in flight together)
+      float sv[64];
+      tmem_ld32(s_col, *reinterpret_cast<float(*)[32]>(&sv[0]));
+      tmem_ld32(s_col + 32, *reinterpret_cast<float(*)[32]>(&sv[32]));
+      tmem_wait_ld();
+      if (diag) {
+#pragma unroll
+        for (int e = 0; e < 64; ++e)
+          if (h * 64 + e > r) sv[e] = -INFINITY;
+      }
       float m8[8];
 #pragma unroll
-      for (int y = 0; y < 8; ++y) m8[y] = -INFINITY;
+      for (int y = 0; y < 8; ++y) m8[y] = fmaxf(sv[y], sv[y + 8]);
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        float sv[32];
-        tmem_ld32(s_col + c * 32, sv);
-        tmem_wait_ld();
-        if (diag) {
+      for (int e = 16; e < 64; e += 8)
 #pragma unroll
-          for (int e = 0; e < 32; ++e)
-            if (h * 64 + c * 32 + e > r) sv[e] = -INFINITY;
-        }
-#pragma unroll
-        for (int e = 0; e < 32; e += 8)
-#pragma unroll
-          for (int y = 0; y < 8; ++y) m8[y] = fmaxf(m8[y], sv[e + y]);
-      }
+        for (int y = 0; y < 8; ++y) m8[y] = fmaxf(m8[y], sv[e + y]);
       const float mh =
           fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])), fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
       // row max shared by the two halves (slot parity j&1: the partner reads
@@ -301,29 +308,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (x == 0 ? (j >= 1 && j - 1 < n_b) : (j < n_a)) named_bar_sync(3 + x, 512);
       float2 rs[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
       const float2 sl2x2 = make_float2(sl2, sl2), nmx2 = make_float2(-msub, -msub);
-      // pass 2: re-read each 32-column chunk, exponentials, bf16 P into the
-      // columns of chunk 1 ([64h+32, 64h+64): chunk c's P at [64h+32+16c, +16)),
-      // which chunk 1's own read has already consumed when chunk 0 is stored
+      // exponentials from registers; bf16 P over the own S columns
+      // [64h, 64h+32) (keys [64h+16q, +16) -> columns [64h+8q, +8))
 #pragma unroll
-      for (int c = 1; c >= 0; --c) {
-        float sv[32];
-        tmem_ld32(s_col + c * 32, sv);
-        tmem_wait_ld();
-        if (diag) {
+      for (int q = 0; q < 4; ++q) {
+        uint32_t pk[8];
 #pragma unroll
-          for (int e = 0; e < 32; ++e)
-            if (h * 64 + c * 32 + e > r) sv[e] = -INFINITY;
-        }
-        uint32_t pk[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const float2 xx = ffma2(make_float2(sv[2 * e], sv[2 * e + 1]), sl2x2, nmx2);
-          const float a = ((kPolyMask >> ((2 * e) & 7)) & 1) ? poly_exp2(xx.x) : fast_exp2(xx.x);
-          const float b = ((kPolyMask >> ((2 * e + 1) & 7)) & 1) ? poly_exp2(xx.y) : fast_exp2(xx.y);
+        for (int e = 0; e < 8; ++e) {
+          const int i = q * 16 + 2 * e;
+          const float2 xx = ffma2(make_float2(sv[i], sv[i + 1]), sl2x2, nmx2);
+          const float a = ((kPolyMask >> (i & 7)) & 1) ? poly_exp2(xx.x) : fast_exp2(xx.x);
+          const float b = ((kPolyMask >> ((i + 1) & 7)) & 1) ? poly_exp2(xx.y) : fast_exp2(xx.y);
           rs[e & 3] = fadd2(rs[e & 3], make_float2(a, b));
           pk[e] = pack_bf16(a, b);
         }
-        tmem_st16(s_col + 32 + c * 16, pk);
+        tmem_st8(s_col + q * 8, pk);
       }
       if (x == 0 ? (j < n_b) : (j + 1 < n_a)) named_bar_arrive(4 - x, 512);
       TRP(10 + 4 * x, j);
@@ -400,11 +399,8 @@ int attn_fwd_d128_pp(const void* q, int64_t q_rows, int64_t q_stride, const void
       !make_tmap_bf16(&tv, v_pool, uint64_t(kv_stride), uint64_t(pool_rows), uint64_t(kv_stride), BN))
     return set_error(SP_ERR_CUDA, "attn_fwd_d128_pp: cuTensorMapEncodeTiled failed (alignment?)");
   const size_t smem = sizeof(Smem) + 1024;
-  static const int poly = getenv("SP_FWD_POLY") ? atoi(getenv("SP_FWD_POLY")) : 0;
-  auto kern = poly == 1   ? attn_fwd_pp_kernel<0x80>   // 1/8 of the exponentials on the FMA pipe
-              : poly == 2 ? attn_fwd_pp_kernel<0x88>   // 1/4
-              : poly == 3 ? attn_fwd_pp_kernel<0x92>   // 3/8
-                          : attn_fwd_pp_kernel<0>;
+  // kPolyMask > 0 (some exponentials on the FMA pipe) measured slower on B200
+  auto kern = attn_fwd_pp_kernel<0>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return cuda_status(e, "attn_fwd_d128_pp: set smem");
   const unsigned pairs = unsigned((q_rows + 2 * BM - 1) / (2 * BM));
