@@ -327,6 +327,10 @@ extern "C" int sp_attn_fwd(const void* q, int64_t q_rows, int64_t q_stride, cons
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int q_tiles = int(q_rows / 128);
   static const bool v2 = getenv("SP_ATTN_FWD_V2") != nullptr;
+  static const bool v3 = getenv("SP_ATTN_FWD_V3") != nullptr;
+  if (head_dim == 128 && !getenv("SP_ATTN_FWD_V1") && !v2 && !v3)
+    return attn_fwd_d128_ps(q, q_rows, q_stride, k_pool, v_pool, pool_rows, kv_stride, chunk_row, n_chunks, chunk_len,
+                            heads, kv_heads, causal, o, o_stride, lse, st);
   if (head_dim == 128 && !getenv("SP_ATTN_FWD_V1") && !v2)
     return attn_fwd_d128_pp(q, q_rows, q_stride, k_pool, v_pool, pool_rows, kv_stride, chunk_row, n_chunks, chunk_len,
                             heads, kv_heads, causal, o, o_stride, lse, st);

@@ -44,6 +44,9 @@ int attn_fwd_d128(const void* q, int64_t q_rows, int64_t q_stride, const void* k
 int attn_fwd_d128_pp(const void* q, int64_t q_rows, int64_t q_stride, const void* k_pool, const void* v_pool,
                   int64_t pool_rows, int64_t kv_stride, const int32_t* chunk_row, int n_chunks, int chunk_len,
                   int heads, int kv_heads, int causal, void* o, int64_t o_stride, float* lse, cudaStream_t st);
+int attn_fwd_d128_ps(const void* q, int64_t q_rows, int64_t q_stride, const void* k_pool, const void* v_pool,
+                  int64_t pool_rows, int64_t kv_stride, const int32_t* chunk_row, int n_chunks, int chunk_len,
+                  int heads, int kv_heads, int causal, void* o, int64_t o_stride, float* lse, cudaStream_t st);
 
 // attn_bwd_v2.cu — pipelined d=128 backward (lse2/delta prepared by the caller)
 int attn_bwd_d128(const void* q, int64_t q_rows, int64_t q_stride, const void* k_pool, const void* v_pool,
