@@ -15,8 +15,8 @@
 //     .add.f32) from an smem stage instead of per-thread global atomics; a
 //     dedicated drain warpgroup does TMEM -> smem -> TMA, so the element-math
 //     warps never wait on it (it was ~28% of their time per pair).
-// Warps: 0 TMA producer, 1 TMEM owner + UMMA issuer, 2..9 element math,
-// 10..13 dQ drain.
+// Warps: 0 TMA producer, 1 TMEM owner + S/dP issuer, 2..9 element math,
+// 10..13 dQ drain, 14 dQ/dV/dK issuer.
 #include <math.h>
 
 #include "errors.hpp"
@@ -29,7 +29,7 @@ namespace sp {
 namespace {
 
 constexpr int D = 128, BQ = 64, BK = 128, NS = 3;
-constexpr int kThreads = 448;
+constexpr int kThreads = 480;
 constexpr int kCompute = 256;
 constexpr int kDrain = 128;
 constexpr int kSlabQ = BQ * 64, kSlabK = BK * 64;  // elements per slab
@@ -63,7 +63,8 @@ static_assert(sizeof(Smem) % 1024 == 0, "operand tiles stay 1024-aligned");
 struct Ctl {  // static shared memory: statistics and barriers
   float lse2[NS][BQ];
   float delta[NS][BQ];
-  uint64_t kv_full, q_full[NS], q_empty[NS], sdp_full[2], pds_ready, pds_free, dq_full[2], dq_free[2], acc_done;
+  uint64_t kv_full, q_full[NS], q_empty[NS], sdp_full[2], pds_ready, pds_free, dq_full[2], dq_free[2], acc_free[2],
+      acc_done;
   uint32_t tmem_base;
 };
 
@@ -117,6 +118,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&ctl.sdp_full[b], 1);
       mbar_init(&ctl.dq_full[b], 1);
       mbar_init(&ctl.dq_free[b], kDrain);
+      mbar_init(&ctl.acc_free[b], 1);
     }
     mbar_init(&ctl.pds_ready, kCompute);
     mbar_init(&ctl.pds_free, 1);
@@ -152,10 +154,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         bulk_load(ctl.delta[s], prm.delta + int64_t(h) * prm.q_rows + qrow, BQ * 4, &ctl.q_full[s]);
       }
     }
-  } else if (warp == 1) {
-    // the whole warp runs the issue loop; one elected lane issues each UMMA
-    // (sm100.cuh *_w / umma_commit_warp): a lane-0-only loop pays an
-    // ELECT/BRA.U.ANY wrapper per MMA and starves the tensor pipe
+  } else if (warp == 1 || warp == 14) {
+    // Two issuing warps, each a whole warp with one elected lane per UMMA
+    // (sm100.cuh *_w / umma_commit_warp): warp 1 issues S^T/dP^T, warp 14
+    // dQ^T, dV, dK.  tcgen05 issue blocks for about the duration of the group
+    // issued, so one issuer serialises the two streams; with two, S/dP of
+    // pair j+1 runs while the accumulation MMAs of pair j wait for P/dS.
+    // Commits cover the issuing warp's own MMAs.
     if (n_pairs > 0) {
       constexpr uint32_t id_s = idesc_bf16_f32(BK, BQ, false, false);  // K Q^T, V dO^T
       constexpr uint32_t id_acc = idesc_bf16_f32(BK, D, false, true);  // P^T dO, dS^T Q
@@ -164,58 +169,62 @@ __global__ void __launch_bounds__(kThreads, 1)
       // descriptor bases; per-step offsets are added to the low word (address >> 4)
       const uint64_t dk_k = smem_desc_sw128(k_a, 16, 1024), dv_k = smem_desc_sw128(v_a, 16, 1024);
       const uint64_t dk_mn = smem_desc_sw128(k_a, kSlabK * 2, 1024), dds_mn = smem_desc_sw128(ds_a, kSlabK * 2, 1024);
-      auto issue_sdp = [&](int j) {
-        const int s = j % NS, b = j & 1;
-        mbar_wait(&ctl.q_full[s], (j / NS) & 1);
-        if (j >= 1) TR(10, j - 1);
-        if (j >= 2) mbar_wait(&ctl.dq_free[b], ((j >> 1) - 1) & 1);  // dQ(j-2) drained from this buffer
-        if (j >= 1) TR(11, j - 1);
-        tc_fence_after();
-        const uint64_t dq_k = smem_desc_sw128(smem_u32(sm.q[s]), 16, 1024);
-        const uint64_t ddo_k = smem_desc_sw128(smem_u32(sm.dout[s]), 16, 1024);
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t oa = ((kk / 4) * (kSlabK * 2) + (kk % 4) * 32) >> 4;
-          const uint32_t ob = ((kk / 4) * (kSlabQ * 2) + (kk % 4) * 32) >> 4;
-          umma_bf16_ss_w(tmem + b * 128, dk_k + oa, dq_k + ob, id_s, kk > 0);
-          umma_bf16_ss_w(tmem + b * 128 + 64, dv_k + oa, ddo_k + ob, id_s, kk > 0);
-        }
-        umma_commit_warp(&ctl.sdp_full[b]);
-      };
       mbar_wait(&ctl.kv_full, 0);
-      issue_sdp(0);
-      for (int j = 0; j < n_pairs; ++j) {
-        const int s = j % NS, b = j & 1;
-        TR(0, j);
-        if (j + 1 < n_pairs) issue_sdp(j + 1);
-        TR(1, j);
-        mbar_wait(&ctl.pds_ready, j & 1);
-        TR(2, j);
-        tc_fence_after();
-        const uint64_t dq_mn = smem_desc_sw128(smem_u32(sm.q[s]), kSlabQ * 2, 1024);
-        const uint64_t ddo_mn = smem_desc_sw128(smem_u32(sm.dout[s]), kSlabQ * 2, 1024);
-        // dQ^T = K^T dS^T into pair j's (consumed) dP^T columns (K = 128 keys)
+      if (warp == 1) {
+        for (int j = 0; j < n_pairs; ++j) {
+          const int s = j % NS, b = j & 1;
+          TR(0, j);
+          mbar_wait(&ctl.q_full[s], (j / NS) & 1);
+          if (j >= 2) {  // buffer b: dQ(j-2) drained, dV/dK(j-2) done reading P/dS
+            mbar_wait(&ctl.dq_free[b], ((j >> 1) - 1) & 1);
+            mbar_wait(&ctl.acc_free[b], ((j >> 1) - 1) & 1);
+          }
+          TR(10, j);
+          tc_fence_after();
+          const uint64_t dq_k = smem_desc_sw128(smem_u32(sm.q[s]), 16, 1024);
+          const uint64_t ddo_k = smem_desc_sw128(smem_u32(sm.dout[s]), 16, 1024);
 #pragma unroll
-        for (int kk = 0; kk < BK / 16; ++kk) {
-          if (prm.dbg & 2) break;
-          const uint32_t ok = (kk * 16 * 128) >> 4;
-          umma_bf16_ss_w(tmem + b * 128 + 64, dk_mn + ok, dds_mn + ok, id_dq, kk > 0);
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t oa = ((kk / 4) * (kSlabK * 2) + (kk % 4) * 32) >> 4;
+            const uint32_t ob = ((kk / 4) * (kSlabQ * 2) + (kk % 4) * 32) >> 4;
+            umma_bf16_ss_w(tmem + b * 128, dk_k + oa, dq_k + ob, id_s, kk > 0);
+            umma_bf16_ss_w(tmem + b * 128 + 64, dv_k + oa, ddo_k + ob, id_s, kk > 0);
+          }
+          umma_commit_warp(&ctl.sdp_full[b]);
+          TR(1, j);
         }
-        umma_commit_warp(&ctl.dq_full[b]);
-        // dV += P^T dO ; dK += dS^T Q   (K = BQ queries), A operands from TMEM:
-        // WG w left P^T (packed bf16) at cols 32w+[0,16), dS^T at 32w+[16,32)
+      } else {
+        for (int j = 0; j < n_pairs; ++j) {
+          const int s = j % NS, b = j & 1;
+          mbar_wait(&ctl.pds_ready, j & 1);
+          TR(2, j);
+          tc_fence_after();
+          const uint64_t dq_mn = smem_desc_sw128(smem_u32(sm.q[s]), kSlabQ * 2, 1024);
+          const uint64_t ddo_mn = smem_desc_sw128(smem_u32(sm.dout[s]), kSlabQ * 2, 1024);
+          // dQ^T = K^T dS^T into pair j's (consumed) dP^T columns (K = 128 keys)
 #pragma unroll
-        for (int kk = 0; kk < BQ / 16; ++kk) {
-          const uint32_t pcol = tmem + b * 128 + (kk >> 1) * 32 + (kk & 1) * 8;
-          const uint32_t ob = (kk * 16 * 128) >> 4;
-          umma_bf16_ts_w(tmem + kDV, pcol, ddo_mn + ob, id_acc, (j > 0 || kk > 0) ? 1u : 0u);
-          umma_bf16_ts_w(tmem + kDK, pcol + 16, dq_mn + ob, id_acc, (j > 0 || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            if (prm.dbg & 2) break;
+            const uint32_t ok = (kk * 16 * 128) >> 4;
+            umma_bf16_ss_w(tmem + b * 128 + 64, dk_mn + ok, dds_mn + ok, id_dq, kk > 0);
+          }
+          umma_commit_warp(&ctl.dq_full[b]);
+          // dV += P^T dO ; dK += dS^T Q   (K = BQ queries), A operands from TMEM:
+          // WG w left P^T (packed bf16) at cols 32w+[0,16), dS^T at 32w+[16,32)
+#pragma unroll
+          for (int kk = 0; kk < BQ / 16; ++kk) {
+            const uint32_t pcol = tmem + b * 128 + (kk >> 1) * 32 + (kk & 1) * 8;
+            const uint32_t ob = (kk * 16 * 128) >> 4;
+            umma_bf16_ts_w(tmem + kDV, pcol, ddo_mn + ob, id_acc, (j > 0 || kk > 0) ? 1u : 0u);
+            umma_bf16_ts_w(tmem + kDK, pcol + 16, dq_mn + ob, id_acc, (j > 0 || kk > 0) ? 1u : 0u);
+          }
+          umma_commit_warp(&ctl.q_empty[s]);  // S/dP(j) of warp 1 completed before pds_ready(j)
+          umma_commit_warp(&ctl.pds_free);
+          umma_commit_warp(&ctl.acc_free[b]);
+          TR(3, j);
         }
-        umma_commit_warp(&ctl.q_empty[s]);
-        umma_commit_warp(&ctl.pds_free);
-        TR(3, j);
+        umma_commit_warp(&ctl.acc_done);
       }
-      umma_commit_warp(&ctl.acc_done);
     }
   } else if (warp < 10) {
     // ------------------------------------------------ element math (2 WGs)
@@ -316,7 +325,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     tc_fence_before();
-  } else {
+  } else if (warp < 14) {
     // --------------------------------------------- dQ drain (one warpgroup)
     // dQ^T of pair jj sits in its consumed dP^T columns (lane = head dim d,
     // columns = the pair's 64 queries): TMEM -> registers (frees the columns

@@ -14,7 +14,7 @@ import os
 from pathlib import Path
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "lib" / "libslimpipe.so"
+LIB_PATH = Path(os.environ["SP_LIB"]) if os.environ.get("SP_LIB") else _PKG / "lib" / "libslimpipe.so"  # SP_LIB: A/B builds
 _lib: C.CDLL | None = None
 
 SP_OK, SP_ERR_INVALID, SP_ERR_RUNTIME, SP_ERR_CUDA, SP_ERR_NCCL, SP_ERR_UNSUPPORTED, SP_ERR_NO_DEVICE = range(7)
