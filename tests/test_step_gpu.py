@@ -53,12 +53,16 @@ def _pull(step, cfg):
     return W
 
 
-@pytest.mark.parametrize("m,n,rc", [(2, 4, "selective"), (1, 2, "selective"), (2, 4, "full")])
-def test_c1_step_matches_oracle(m, n, rc):
+@pytest.mark.parametrize("m,n,rc,shape", [(2, 4, "selective", {}), (1, 2, "selective", {}), (2, 4, "full", {}),
+                                          # GQA 4:2 on the d=64 kernels, and d=128 (production K1/K2) with GQA
+                                          (2, 4, "selective", {"kv_heads": 2}),
+                                          (2, 4, "selective", {"hidden": 512, "kv_heads": 2, "ffn_hidden": 1024}),
+                                          (1, 4, "full", {"hidden": 512, "kv_heads": 4, "ffn_hidden": 1024})])
+def test_c1_step_matches_oracle(m, n, rc, shape):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     from paper_2504_14519_b200.runtime import SlimPipeStep, StepConfig
-    cfg = StepConfig.c1(microbatches=m, slices=n, recompute=rc)
+    cfg = StepConfig.c1(microbatches=m, slices=n, recompute=rc, **shape)
     step = SlimPipeStep(cfg, rank=0, world=1)
     tok, tgt = _data(cfg)
     loss = step.step(tok, tgt, optimizer=False)
