@@ -71,6 +71,8 @@ def _worker(rank, world, port, cases, q):
 @pytest.mark.parametrize("world,cases", [
     (2, [(2, 4, "off", 2), (2, 4, "on", 2), (3, 8, "early", 2), (1, 2, "on", 1)]),
     (4, [(4, 8, "on", 1), (4, 8, "early", 2), (2, 4, "on", 1), (1, 8, "early", 1)]),
+    # the driver's PP=8 scaling run (bench default: m=4, n=8, exchange off) and the exchange plans at p=8
+    (8, [(4, 8, "off", 1), (4, 8, "on", 1), (1, 8, "early", 1), (2, 16, "on", 1)]),
 ])
 def test_protocol_consistent_and_deadlock_free(world, cases):
     ctx = mp.get_context("spawn")
