@@ -41,11 +41,9 @@ struct Params {
   const float* delta;
   float* dk;
   float* dv;
-  float* dq;  // [q_rows][heads * D] fp32 accumulator (direct-reduce drain)
   int64_t acc_stride;
   int trace;  // record a per-pair timeline of CTA (0,0) into g_bwd_trace
   int dbg;    // diagnostics only: bit0 skip the dQ stage/reduce, bit1 skip the dQ MMA
-  int dq_red; // 1: dQ by red.global.add from registers (no smem stage), 0: smem stage + TMA reduce
   int chunk_row[SP_MAX_CHUNKS];
   int acc_row[SP_MAX_CHUNKS];
 };
@@ -347,19 +345,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       mbar_arrive(&ctl.dq_free[bb]);
       if (prm.dbg & 1) continue;
-      if (prm.dq_red) {
-        // lanes of a warp hold 32 consecutive head dims of one query row:
-        // every red.global is one coalesced 128-byte L2 reduction
-        float* g = prm.dq + int64_t(pair_row(jj)) * (int64_t(prm.group) * prm.acc_stride) + pair_head(jj) * D + d;
-        const int64_t rs = int64_t(prm.group) * prm.acc_stride;
-#pragma unroll
-        for (int x = 0; x < 32; ++x) {
-          asm volatile("red.global.add.f32 [%0], %1;" ::"l"(g + x * rs), "f"(a0[x]) : "memory");
-          asm volatile("red.global.add.f32 [%0], %1;" ::"l"(g + (32 + x) * rs), "f"(a1[x]) : "memory");
-        }
-        if (tl) TR(9, jj);
-        continue;
-      }
       if (dtid == 0) bulk_wait_read<0>();  // the previous reduce has read the stage
       named_bar_sync(1, kDrain);
       const uint32_t st = smem_u32(sm.stage[0]) + uint32_t(d) * 4u;
@@ -407,8 +392,6 @@ int attn_bwd_d128(const void* q, int64_t q_rows, int64_t q_stride, const void* k
   prm.delta = delta;
   prm.dk = dk_acc;
   prm.dv = dv_acc;
-  prm.dq = dq_acc;
-  prm.dq_red = getenv("SP_BWD_DQ_RED") ? 1 : 0;  // measured slower: L2 atomics at 64 per thread per pair
   prm.acc_stride = int64_t(kv_heads) * D;
   prm.trace = getenv("SP_BWD_TRACE") != nullptr;
   prm.dbg = getenv("SP_BWD_DBG") ? atoi(getenv("SP_BWD_DBG")) : 0;

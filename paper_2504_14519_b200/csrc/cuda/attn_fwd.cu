@@ -326,17 +326,16 @@ extern "C" int sp_attn_fwd(const void* q, int64_t q_rows, int64_t q_stride, cons
     return set_error(SP_ERR_CUDA, "sp_attn_fwd: cuTensorMapEncodeTiled failed (alignment?)");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int q_tiles = int(q_rows / 128);
-  static const bool v2 = getenv("SP_ATTN_FWD_V2") != nullptr;
+  // d=128: attn_fwd_v4.cu (production); SP_ATTN_FWD_V3 / SP_ATTN_FWD_V1 select
+  // the earlier designs for A/B measurements
+  static const bool v1 = getenv("SP_ATTN_FWD_V1") != nullptr;
   static const bool v3 = getenv("SP_ATTN_FWD_V3") != nullptr;
-  if (head_dim == 128 && !getenv("SP_ATTN_FWD_V1") && !v2 && !v3)
+  if (head_dim == 128 && !v1 && !v3)
     return attn_fwd_d128_ps(q, q_rows, q_stride, k_pool, v_pool, pool_rows, kv_stride, chunk_row, n_chunks, chunk_len,
                             heads, kv_heads, causal, o, o_stride, lse, st);
-  if (head_dim == 128 && !getenv("SP_ATTN_FWD_V1") && !v2)
+  if (head_dim == 128 && !v1)
     return attn_fwd_d128_pp(q, q_rows, q_stride, k_pool, v_pool, pool_rows, kv_stride, chunk_row, n_chunks, chunk_len,
                             heads, kv_heads, causal, o, o_stride, lse, st);
-  if (head_dim == 128 && !getenv("SP_ATTN_FWD_V1"))
-    return attn_fwd_d128(q, q_rows, q_stride, k_pool, v_pool, pool_rows, kv_stride, chunk_row, n_chunks, chunk_len,
-                         heads, kv_heads, causal, o, o_stride, lse, st);
   if (head_dim == 128) return launch_fwd<128, 2>(tq, tk, tv, prm, q_tiles, heads, st);
   return launch_fwd<64, 3>(tq, tk, tv, prm, q_tiles, heads, st);
 }

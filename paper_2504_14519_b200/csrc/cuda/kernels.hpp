@@ -38,9 +38,6 @@ int f32_to_bf16(const float* a, void* b, int64_t n, cudaStream_t st);
 int add_f32(float* dst, const float* src, int64_t n, cudaStream_t st);  // dst += src
 
 // attn_fwd_v2.cu — two-tile, P-in-TMEM d=128 forward (q_rows % 256 == 0)
-int attn_fwd_d128(const void* q, int64_t q_rows, int64_t q_stride, const void* k_pool, const void* v_pool,
-                  int64_t pool_rows, int64_t kv_stride, const int32_t* chunk_row, int n_chunks, int chunk_len,
-                  int heads, int kv_heads, int causal, void* o, int64_t o_stride, float* lse, cudaStream_t st);
 int attn_fwd_d128_pp(const void* q, int64_t q_rows, int64_t q_stride, const void* k_pool, const void* v_pool,
                   int64_t pool_rows, int64_t kv_stride, const int32_t* chunk_row, int n_chunks, int chunk_len,
                   int heads, int kv_heads, int causal, void* o, int64_t o_stride, float* lse, cudaStream_t st);

@@ -20,10 +20,8 @@ lib = native.lib()
 lib.sp_debug_bwd_trace(buf)
 t = np.array(buf[:], dtype=np.int64).reshape(12, 512)
 t = t - t[0, 0]
-names = ["mma_top", "sdp_issued", "pds_ready_ok", "mma_done", "drain_dqfull_ok(j)", "sdp_full_ok", "compute_done", "pds_free_ok", "pds_ready_arr", "drain_staged(j)", "qfull_ok", "dqfree_ok"]
-for j in [1, 2, 3, 50, 51, 52, 100, 101, 200]:
-    print(j, " ".join(f"{names[e]}={t[e, j]}" for e in range(12)))
+names = ["sdp_top(j)", "sdp_issued(j)", "acc: pds_ready_ok(j)", "acc: issued(j)", "drain_dqfull_ok(j)", "sdp_full_ok", "compute_done", "pds_free_ok", "pds_ready_arr", "drain_staged(j)", "sdp: q/dq/acc free ok(j)", "-"]
 per = np.diff(t[0, 10:250])
 print("mean period (cycles)", per.mean())
-for e in range(1, 12):
+for e in range(1, 11):
     print(names[e], "-", names[0], np.median(t[e, 10:250] - t[0, 10:250]))
