@@ -61,8 +61,9 @@ def parse():
     ap.add_argument("--seq-len", type=int, default=None, help="default: c2 128K, c3 256K, c4 1M")
     ap.add_argument("--slices", type=int, default=None, help="default: c2 8, c3 16, c4 32")
     ap.add_argument("--microbatches", type=int, default=None, help="default: c2 4, c3 4, c4 1")
-    ap.add_argument("--recompute", choices=["selective", "full"], default="selective",
-                    help="selective: the forward stashes attention O/LSE, the backward recomputes the rest")
+    ap.add_argument("--recompute", choices=["auto", "selective", "full"], default="auto",
+                    help="selective: the forward stashes attention O/LSE, the backward recomputes the rest; "
+                         "auto: selective when the stash fits in HBM")
     ap.add_argument("--exchange", choices=["off", "on", "early"], default="off",
                     help="attention workload redistribution (reference ExchangeMode); no effect at PP=1")
     ap.add_argument("--no-e2e", action="store_true")
@@ -356,7 +357,8 @@ def main():
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic tokens, random-init weights",
             "config": {"workload": workload_name(cfg, args.model), "model": MODEL_NAMES[args.model][1], "layers": cfg.layers,
                        "global_batch": cfg.microbatches, "seq_len": cfg.seq_len, "slices": cfg.slices,
-                       "parallelism": f"pp{world}", "exchange": cfg.exchange, "recompute": cfg.recompute,
+                       "parallelism": f"pp{world}", "exchange": cfg.exchange,
+                       "recompute": cfg.recompute if cfg.recompute != "auto" else f"auto->{mem['recompute']}",
                        "l2": "inputs larger than L2 (per-step working set tens of GB)"},
             "mfu": mfu, "mfu_nominal": mfu_nominal, "mfu_peak_tflops": peak_tf,
             "bubble_fraction": bubble,

@@ -153,11 +153,13 @@ typedef struct {
   int64_t seq_len;
   float rope_theta, norm_eps, lr;
   uint64_t seed;
-  /* 0 = selective (default): the forward pass stashes each layer's attention
-   * output O and LSE in the slot, the backward pass recomputes everything
-   * else (norms, GEMMs, RoPE, SwiGLU) but not K1;  1 = full: only the stage
-   * input is stashed and K1 runs again in the backward (reference Full
-   * checkpointing, workload.cpp:100-104). */
+  /* 0 = selective: the forward pass stashes each layer's attention output O
+   * and LSE in the slot, the backward pass recomputes everything else (norms,
+   * GEMMs, RoPE, SwiGLU) but not K1;  1 = full: only the stage input is
+   * stashed and K1 runs again in the backward (reference Full checkpointing,
+   * workload.cpp:100-104);  2 = auto: selective when the stash fits in the
+   * free HBM left after the rest of the arena, else full
+   * (sp_runtime_recompute reports the policy in effect). */
   int32_t recompute;
 } sp_model_config;
 
@@ -183,6 +185,7 @@ void* sp_runtime_stream(void* handle);
 int sp_runtime_timeline(void* handle, double* out, int cap);
 int sp_runtime_attn_stats(void* handle, double* out6);
 int sp_runtime_memory(void* handle, int64_t* out7);
+int sp_runtime_recompute(void* handle); /* policy in effect: 0 selective, 1 full */
 int sp_runtime_param(void* handle, int layer, int which, float* host, int64_t count, int dir);
 /* {passes with outgoing transfers, passes with incoming transfers, bytes sent
  *  by this rank through the exchange in the last step} */

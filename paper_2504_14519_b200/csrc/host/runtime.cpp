@@ -215,8 +215,8 @@ class Runtime {
     if (c.hidden != c.heads * c.head_dim) return set_error(SP_ERR_INVALID, "hidden != heads * head_dim");
     Lps = c.layers / p;
     Ls = c.seq_len / c.slices;
-    if (c.recompute != 0 && c.recompute != 1) return set_error(SP_ERR_INVALID, "recompute must be 0 or 1");
-    stash = c.recompute == 0;
+    if (c.recompute < 0 || c.recompute > 2) return set_error(SP_ERR_INVALID, "recompute must be 0, 1 or 2");
+    stash = c.recompute != 1;  // 2 (auto) is settled in alloc_arena once the parameters are resident
     h = c.hidden;
     H = c.ffn_hidden;
     qd = int64_t(c.heads) * c.head_dim;
@@ -558,6 +558,16 @@ class Runtime {
 
   int alloc_arena() {
     const int64_t rows = int64_t(slots) * Ls;
+    if (cfg.recompute == 2) {  // auto: stash O/LSE only if it leaves room for everything else
+      size_t free_b = 0, total_b = 0;
+      SP_CUDA(cudaMemGetInfo(&free_b, &total_b));
+      const double stash_b = double(Lps) * rows * (qd * 2 + double(cfg.heads) * 4);
+      const double rest_b = double(rows) * h * 2 + double(Lps) * rows * kvd * 4 +                 // x, K/V
+                            double(Lps) * cfg.slices * Ls * kvd * 8 +                               // dK/dV acc
+                            double(Lps) * Ls * (6.0 * h + 3.0 * H) * 2 +                          // layer workspace
+                            (stage == p ? double(Ls) * cfg.vocab * 4 * 2 : 0.0) + 4.0 * double(1 << 30);  // logits + margin
+      stash = stash_b + rest_b < double(free_b);
+    }
     SP_TRY(alloc(&x_pool, rows * h));
     if (stash) {
       o_pool.assign(Lps, nullptr);
@@ -1071,6 +1081,8 @@ int sp_runtime_exchange_stats(void* handle, int64_t* out3) {
 }
 
 // {slots, slots_high_water, slot_bytes, ledger_peak_units, bytes_allocated, n_params, layers_per_stage}
+int sp_runtime_recompute(void* handle) { return static_cast<Runtime*>(handle)->stash ? 0 : 1; }
+
 int sp_runtime_memory(void* handle, int64_t* out7) {
   Runtime* rt = static_cast<Runtime*>(handle);
   out7[0] = rt->slots;

@@ -27,7 +27,7 @@ class _Cfg(C.Structure):
         ("seed", C.c_uint64), ("recompute", C.c_int32)]
 
 
-RECOMPUTE = {"selective": 0, "full": 1}
+RECOMPUTE = {"selective": 0, "full": 1, "auto": 2}
 
 
 @dataclass(frozen=True)
@@ -43,7 +43,7 @@ class StepConfig:
     microbatches: int
     pp: int = 1
     exchange: str = "off"
-    recompute: str = "selective"  # "selective": stash attention O/LSE, "full": K1 again in the backward
+    recompute: str = "auto"  # "selective": stash attention O/LSE, "full": K1 again in the backward, "auto": selective if it fits
     rope_theta: float = 10000.0
     norm_eps: float = 1e-5
     lr: float = 1e-4
@@ -112,6 +112,7 @@ def _lib():
     lib.sp_runtime_timeline.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.c_int]
     lib.sp_runtime_attn_stats.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
     lib.sp_runtime_memory.argtypes = [C.c_void_p, C.POINTER(C.c_int64)]
+    lib.sp_runtime_recompute.argtypes = [C.c_void_p]
     lib.sp_runtime_param.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int64, C.c_int]
     return lib
 
@@ -219,7 +220,9 @@ class SlimPipeStep:
         N.check(_lib().sp_runtime_memory(self._h, b), "sp_runtime_memory")
         keys = ["slots", "slots_high_water", "slot_bytes", "ledger_peak_units", "bytes_allocated", "n_params",
                 "layers_per_stage"]
-        return dict(zip(keys, list(b)))
+        out = dict(zip(keys, list(b)))
+        out["recompute"] = "full" if _lib().sp_runtime_recompute(self._h) else "selective"
+        return out
 
     def exchange_stats(self) -> dict:
         b = (C.c_int64 * 3)()
