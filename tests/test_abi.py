@@ -2,6 +2,8 @@
 include/slimpipe.h declares (no compute calls here)."""
 import ctypes
 import re
+
+import pytest
 from pathlib import Path
 
 from paper_2504_14519_b200 import native
@@ -32,3 +34,24 @@ def test_status_strings_and_errors_without_gpu():
     rc = lib.sp_attn_fwd(None, 100, 128, None, None, 128, 128, rows, 1, 128, 1, 1, 128, 1, None, 128, None, None)
     assert rc == native.SP_ERR_UNSUPPORTED
     assert b"multiples of 128" in lib.sp_last_error()
+
+
+@pytest.mark.parametrize("kw,msg", [
+    ({"layers": 3, "pp": 2}, b"must divide by pp"),
+    ({"slices": 3}, b"divisible by slices"),
+    ({"pp": 2, "slices": 3, "seq_len": 3072, "layers": 2}, b"multiple of p"),   # schedule.cpp:249-252
+    ({"pp": 2, "microbatches": 0, "layers": 2}, b"m must be >= 1"),
+    ({"hidden": 250}, b"heads * head_dim"),
+])
+def test_runtime_rejects_invalid_configs_before_touching_the_device(kw, msg):
+    """Reference error behaviour (std::invalid_argument <-> SP_ERR_INVALID),
+    checked host-side before any CUDA call, so it runs without a GPU."""
+    from paper_2504_14519_b200.runtime import StepConfig, _lib
+    lib = _lib()
+    c = StepConfig.c1(**kw).to_c(0)
+    h = ctypes.c_void_p()
+    assert lib.sp_runtime_create(ctypes.byref(c), None, ctypes.byref(h)) == native.SP_ERR_INVALID
+    assert msg in lib.sp_last_error()
+    c = StepConfig.c1().to_c(0)
+    c.recompute = 7
+    assert lib.sp_runtime_create(ctypes.byref(c), None, ctypes.byref(h)) == native.SP_ERR_INVALID
