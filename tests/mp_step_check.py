@@ -31,7 +31,8 @@ def main():
     n = int(os.environ.get("SP_N", 4))
     xmode = os.environ.get("SP_X", "off")
     cfg = StepConfig.c1(pp=world, microbatches=m, slices=n, layers=2 * world, exchange=xmode,
-                        seq_len=1024 * n, recompute=os.environ.get("SP_RC", "selective"))
+                        seq_len=1024 * n, recompute=os.environ.get("SP_RC", "selective"),
+                        kv_heads=int(os.environ.get("SP_KV", 4)))
     step = SlimPipeStep(cfg, rank, world)
     rng = np.random.default_rng(0)
     tok = rng.integers(0, cfg.vocab, (cfg.microbatches, cfg.seq_len), dtype=np.int32)

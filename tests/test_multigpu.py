@@ -16,12 +16,15 @@ ROOT = Path(__file__).resolve().parents[1]
                                          (2, 2, 4, "on", "selective"), (2, 2, 4, "on", "full"),
                                          (2, 2, 8, "early", "selective"), (2, 3, 4, "on", "selective"),
                                          (4, 2, 4, "off", "selective"), (4, 2, 8, "on", "selective"),
-                                         (4, 2, 8, "early", "full")])
+                                         (4, 2, 8, "early", "full"),
+                                         (2, 2, 4, "on", "selective-gqa")])  # GQA 4:2 through the exchange
 def test_pipeline_parallel_step_matches_oracle(pp, m, n, x, rc):
     if not torch.cuda.is_available() or torch.cuda.device_count() < pp:
         pytest.skip(f"needs {pp} GPUs")
-    env = dict(os.environ, SP_M=str(m), SP_N=str(n), SP_X=x, SP_RC=rc)
-    port = 29500 + pp * 100 + m * 10 + n + len(x) + (50 if rc == "full" else 0)
+    gqa = rc.endswith("-gqa")
+    rc = rc.removesuffix("-gqa")
+    env = dict(os.environ, SP_M=str(m), SP_N=str(n), SP_X=x, SP_RC=rc, SP_KV="2" if gqa else "4")
+    port = 29500 + pp * 100 + m * 10 + n + len(x) + (50 if rc == "full" else 0) + (25 if gqa else 0)
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={pp}",
                         "--master-addr", "127.0.0.1", "--master-port", str(port),
                         str(ROOT / "tests" / "mp_step_check.py")], env=env, capture_output=True, text=True,
