@@ -254,36 +254,27 @@ __global__ void __launch_bounds__(kThreads, 1)
       // packed fp32x2 (FFMA2/FMUL2); statistics come from smem 8 columns at a
       // time with 128-bit loads (they are uniform across the warp)
       uint32_t pk[16], dk[16];
-      const float* lse_s = ctl.lse2[s] + c0;
-      const float* del_s = ctl.delta[s] + c0;
+      // per-query statistics: one coalesced load per warp (lane i holds column
+      // c0+i), then warp shuffles -- a broadcast LDS.128 per 4 columns cost 4
+      // shared-memory wavefronts and was ~20 % of this kernel's smem traffic
+      const float my_nl = -ctl.lse2[s][c0 + lane];
+      const float my_nd = -ctl.delta[s][c0 + lane] * prm.scale;
       const float2 sl2x2 = make_float2(prm.scale_log2, prm.scale_log2);
       const float2 scx2 = make_float2(prm.scale, prm.scale);
-      const float2 nscx2 = make_float2(-prm.scale, -prm.scale);
-      const float2 neg1 = make_float2(-1.f, -1.f);
 #pragma unroll
-      for (int g = 0; g < 4; ++g) {
-        const float4 la = *reinterpret_cast<const float4*>(lse_s + 8 * g);
-        const float4 lb = *reinterpret_cast<const float4*>(lse_s + 8 * g + 4);
-        const float4 da = *reinterpret_cast<const float4*>(del_s + 8 * g);
-        const float4 db = *reinterpret_cast<const float4*>(del_s + 8 * g + 4);
-        const float2 nl[4] = {fmul2(make_float2(la.x, la.y), neg1), fmul2(make_float2(la.z, la.w), neg1),
-                              fmul2(make_float2(lb.x, lb.y), neg1), fmul2(make_float2(lb.z, lb.w), neg1)};
-        const float2 nd[4] = {fmul2(make_float2(da.x, da.y), nscx2), fmul2(make_float2(da.z, da.w), nscx2),
-                              fmul2(make_float2(db.x, db.y), nscx2), fmul2(make_float2(db.z, db.w), nscx2)};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int x = 8 * g + 2 * e;
-          const float2 t = ffma2(make_float2(sv[x], sv[x + 1]), sl2x2, nl[e]);
-          float p0 = fast_exp2(t.x), p1 = fast_exp2(t.y);
-          if (need_mask) {
-            if (key_rel > qrow0 + c0 + x) p0 = 0.f;
-            if (key_rel > qrow0 + c0 + x + 1) p1 = 0.f;
-          }
-          const float2 u = ffma2(make_float2(dp[x], dp[x + 1]), scx2, nd[e]);
-          const float2 dd = fmul2(u, make_float2(p0, p1));
-          pk[x / 2] = pack_bf16(p0, p1);
-          dk[x / 2] = pack_bf16(dd.x, dd.y);
+      for (int x = 0; x < 32; x += 2) {
+        const float2 nl = make_float2(__shfl_sync(0xffffffffu, my_nl, x), __shfl_sync(0xffffffffu, my_nl, x + 1));
+        const float2 nd = make_float2(__shfl_sync(0xffffffffu, my_nd, x), __shfl_sync(0xffffffffu, my_nd, x + 1));
+        const float2 t = ffma2(make_float2(sv[x], sv[x + 1]), sl2x2, nl);
+        float p0 = fast_exp2(t.x), p1 = fast_exp2(t.y);
+        if (need_mask) {
+          if (key_rel > qrow0 + c0 + x) p0 = 0.f;
+          if (key_rel > qrow0 + c0 + x + 1) p1 = 0.f;
         }
+        const float2 u = ffma2(make_float2(dp[x], dp[x + 1]), scx2, nd);
+        const float2 dd = fmul2(u, make_float2(p0, p1));
+        pk[x / 2] = pack_bf16(p0, p1);
+        dk[x / 2] = pack_bf16(dd.x, dd.y);
       }
       if (tl) TR(6, j);
       if (j > 0) mbar_wait(&ctl.pds_free, (j - 1) & 1);
