@@ -161,6 +161,10 @@ typedef struct {
    * free HBM left after the rest of the arena, else full
    * (sp_runtime_recompute reports the policy in effect). */
   int32_t recompute;
+  /* 1: vocabulary parallelism (pp > 1): the LM head and the cross entropy are
+   * split by vocabulary across all stages (reference place_vocab with
+   * distribute = true, simulator.cpp:414-522); 0: the last stage owns them. */
+  int32_t vocab_parallel;
 } sp_model_config;
 
 #define SP_STEP_NO_OPTIMIZER 1

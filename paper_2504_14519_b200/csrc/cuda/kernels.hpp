@@ -35,6 +35,12 @@ int adamw(float* master, void* wbf, const float* g, float* m, float* v, int64_t 
 int init_params(float* master, void* wbf, int64_t n, uint64_t seed, float stdv, float constant, int use_const,
                 cudaStream_t st);
 int f32_to_bf16(const float* a, void* b, int64_t n, cudaStream_t st);
+// vocabulary-parallel cross entropy over a vocab shard [v0, v0+Vs)
+int xent_shard_stats(const float* logits, const int32_t* tgt, int64_t rows, int Vs, int v0, float* m_loc,
+                     float* m_glob, float* zt, cudaStream_t st);
+int xent_shard_rescale(const float* m_loc, const float* m_glob, float* z, int64_t rows, cudaStream_t st);
+int xent_shard_grad(const float* logits, const int32_t* tgt, int64_t rows, int Vs, int v0, const float* m_glob,
+                    const float* zt, float scale, void* dlogits, float* loss_sum, cudaStream_t st);
 int add_f32(float* dst, const float* src, int64_t n, cudaStream_t st);  // dst += src
 
 // attn_fwd_v2.cu — two-tile, P-in-TMEM d=128 forward (q_rows % 256 == 0)

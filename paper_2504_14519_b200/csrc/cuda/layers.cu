@@ -366,6 +366,83 @@ __global__ void xent_k(const float* __restrict__ logits, const int32_t* __restri
   if (threadIdx.x == 0 && t >= 0) atomicAdd(loss_sum, lse - lr[t]);
 }
 
+// ---- vocabulary-parallel cross entropy ---------------------
+// Each stage holds vocab rows [v0, v0+Vs) of the LM head.  Pass 1 (per shard):
+// row max m, sum exp(l - m) and the target logit (0 where the target is not in
+// the shard); the driver all-reduces M = max m, then Z = sum z*exp(m - M) and
+// T = sum t.  Pass 2: dlogits = (softmax - onehot) * scale on the shard, loss
+// log Z + M - T accumulated by one rank.
+__global__ void xent_shard_stats_k(const float* __restrict__ logits, const int32_t* __restrict__ tgt, int64_t rows,
+                                   int Vs, int v0, float* __restrict__ m_loc, float* __restrict__ m_glob,
+                                   float* __restrict__ zt) {
+  const int64_t r = blockIdx.x;
+  const float* lr = logits + r * Vs;
+  __shared__ float red[32];
+  __shared__ float bcast;
+  float mx = -INFINITY;
+  for (int c = threadIdx.x * 4; c < Vs; c += blockDim.x * 4) {
+    const float4 v = *reinterpret_cast<const float4*>(lr + c);
+    mx = fmaxf(mx, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float m = -INFINITY;
+    for (int i = 0; i < int(blockDim.x / 32); ++i) m = fmaxf(m, red[i]);
+    bcast = m;
+  }
+  __syncthreads();
+  mx = bcast;
+  float se = 0.f;
+  for (int c = threadIdx.x * 4; c < Vs; c += blockDim.x * 4) {
+    const float4 v = *reinterpret_cast<const float4*>(lr + c);
+    se += __expf(v.x - mx) + __expf(v.y - mx) + __expf(v.z - mx) + __expf(v.w - mx);
+  }
+  se = warp_sum(se);
+  __syncthreads();
+  if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = se;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float z = 0.f;
+    for (int i = 0; i < int(blockDim.x / 32); ++i) z += red[i];
+    const int t = tgt[r];
+    m_loc[r] = mx;
+    m_glob[r] = mx;
+    zt[r] = z;
+    zt[rows + r] = (t >= v0 && t < v0 + Vs) ? lr[t - v0] : 0.f;
+  }
+}
+
+__global__ void xent_shard_rescale_k(const float* __restrict__ m_loc, const float* __restrict__ m_glob,
+                                     float* __restrict__ z, int64_t rows) {
+  for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < rows; r += int64_t(gridDim.x) * blockDim.x)
+    z[r] *= __expf(m_loc[r] - m_glob[r]);
+}
+
+__global__ void xent_shard_grad_k(const float* __restrict__ logits, const int32_t* __restrict__ tgt, int64_t rows,
+                                  int Vs, int v0, const float* __restrict__ m_glob, const float* __restrict__ zt,
+                                  float scale, bf16* __restrict__ dlogits, float* __restrict__ loss_sum) {
+  const int64_t r = blockIdx.x;
+  const float* lr = logits + r * Vs;
+  const float mx = m_glob[r], inv = 1.f / zt[r];
+  const int t = tgt[r];
+  const float sc = t >= 0 ? scale : 0.f;
+  for (int c = threadIdx.x * 4; c < Vs; c += blockDim.x * 4) {
+    const float4 v = *reinterpret_cast<const float4*>(lr + c);
+    float p[4] = {__expf(v.x - mx) * inv, __expf(v.y - mx) * inv, __expf(v.z - mx) * inv, __expf(v.w - mx) * inv};
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if (v0 + c + e == t) p[e] -= 1.f;
+    uint2 u;
+    u.x = pack_bf16(p[0] * sc, p[1] * sc);
+    u.y = pack_bf16(p[2] * sc, p[3] * sc);
+    *reinterpret_cast<uint2*>(dlogits + r * Vs + c) = u;
+  }
+  if (loss_sum && threadIdx.x == 0 && t >= 0) atomicAdd(loss_sum, mx + __logf(zt[r]) - zt[rows + r]);
+}
+
 // ---- AdamW over flat fp32 master weights --------------------------------------
 __global__ void adamw_k(float* __restrict__ master, bf16* __restrict__ wbf, const float* __restrict__ g,
                         float* __restrict__ m, float* __restrict__ v, int64_t n, float lr, float b1, float b2,
@@ -506,6 +583,28 @@ int cross_entropy(const float* logits, const int32_t* tgt, int64_t rows, int V, 
   xent_k<<<unsigned(rows), 256, 0, st>>>(logits, tgt, rows, V, scale, (bf16*)dlogits, loss_sum);
   count_launch();
   return cuda_status(cudaGetLastError(), "cross_entropy");
+}
+
+int xent_shard_stats(const float* logits, const int32_t* tgt, int64_t rows, int Vs, int v0, float* m_loc,
+                     float* m_glob, float* zt, cudaStream_t st) {
+  if (Vs % 4) return set_error(SP_ERR_UNSUPPORTED, "vocab shard %% 4");
+  xent_shard_stats_k<<<unsigned(rows), 256, 0, st>>>(logits, tgt, rows, Vs, v0, m_loc, m_glob, zt);
+  count_launch();
+  return cuda_status(cudaGetLastError(), "xent_shard_stats");
+}
+
+int xent_shard_rescale(const float* m_loc, const float* m_glob, float* z, int64_t rows, cudaStream_t st) {
+  xent_shard_rescale_k<<<grid_for(rows, 256), 256, 0, st>>>(m_loc, m_glob, z, rows);
+  count_launch();
+  return cuda_status(cudaGetLastError(), "xent_shard_rescale");
+}
+
+int xent_shard_grad(const float* logits, const int32_t* tgt, int64_t rows, int Vs, int v0, const float* m_glob,
+                    const float* zt, float scale, void* dlogits, float* loss_sum, cudaStream_t st) {
+  xent_shard_grad_k<<<unsigned(rows), 256, 0, st>>>(logits, tgt, rows, Vs, v0, m_glob, zt, scale, (bf16*)dlogits,
+                                                    loss_sum);
+  count_launch();
+  return cuda_status(cudaGetLastError(), "xent_shard_grad");
 }
 
 int adamw(float* master, void* wbf, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2,

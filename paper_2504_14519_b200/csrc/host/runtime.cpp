@@ -97,6 +97,26 @@ class Runtime {
   int64_t emb = -1, final_norm = -1, head = -1;
   int opt_step = 0;
 
+  // ---- vocabulary parallelism (reference place_vocab,
+  // simulator.cpp:414-522): every stage holds vocab rows [v0, v0+Vs) of the
+  // LM head; per slice, VocabForward broadcasts the last stage's final hidden
+  // state and all-reduces the shard softmax statistics, VocabBackward turns
+  // them into the shard's dlogits, dW_head and a partial dX reduced onto the
+  // last stage.  The collectives run on the world communicator in the order
+  // place_vocab puts the vocab passes (identical on every rank).
+  bool vp = false;
+  int64_t Vs = 0, v0 = 0;
+  cudaStream_t s_vocab = nullptr;
+  struct VSlot {
+    bf16raw* xf = nullptr;  // [Ls, h] final hidden state of the slice
+    float* st = nullptr;    // [4][Ls]: local max, global max, Z, T
+  };
+  std::vector<VSlot> vslots;
+  std::vector<int> vfree;
+  std::map<std::pair<int, int>, int> vslot_of;
+  float *vlogits = nullptr, *vdxf = nullptr;
+  bf16raw* vdlog = nullptr;
+
   // arena: x stash + per-layer K/V pools, `slots` slice-sized slots
   int slots = 0;
   bf16raw* x_pool = nullptr;
@@ -247,6 +267,40 @@ class Runtime {
       ann = pipelab::apply_exchange(sched, cm, pipelab::ExchangeMode(c.exchange_mode));
       build_xplan();
     }
+    if (c.vocab_parallel && p > 1) {
+      if (c.vocab % p || (c.vocab / p) % 4)
+        return set_error(SP_ERR_INVALID, "vocab_parallel: vocab (%d) must split into p shards of a multiple of 4",
+                         c.vocab);
+      vp = true;
+      Vs = c.vocab / p;
+      v0 = int64_t(rank) * Vs;
+      // Base-simulation costs normalised so pass times are O(1): place_vocab
+      // compares anchors against pass ends with a fixed 1e-9 slack, which
+      // vanishes below one ulp once times reach ~1e7 (raw per-pair costs at
+      // 4K+ tokens) and then orders VF(k,i) before its own F(k,i,p).
+      pipelab::SimInputs in;
+      in.cost.alpha_linear = 1.0 / double(c.seq_len);
+      in.cost.beta_attn = 1.0 / (double(c.seq_len) * double(c.seq_len));
+      in.seq_len = c.seq_len;
+      try {
+        sched = pipelab::place_vocab(sched, true, in);  // appends vocab passes: F/BW pass ids unchanged
+      } catch (const std::exception& e) {
+        return set_error(SP_ERR_INVALID, "%s", e.what());
+      }
+      const pipelab::Diagnostics vd = pipelab::validate_schedule(sched);
+      if (!vd.ok()) return set_error(SP_ERR_RUNTIME, "vocab schedule invalid: %s", vd.first()->message.c_str());
+      order = sched.device_order[rank];
+      int live = 0, peak = 0;
+      for (pipelab::PassId id : order) {
+        // the last stage takes the slot at F(k,i,p) (it normalises the output there)
+        const auto acq = stage == p ? pipelab::PassKind::Forward : pipelab::PassKind::VocabForward;
+        if (sched.passes[id].kind == acq) peak = std::max(peak, ++live);
+        if (sched.passes[id].kind == pipelab::PassKind::VocabBackward) --live;
+      }
+      vslots.resize(std::max(peak, 1));
+    } else if (c.vocab_parallel < 0 || c.vocab_parallel > 1) {
+      return set_error(SP_ERR_INVALID, "vocab_parallel must be 0 or 1");
+    }
 
     SP_CUDA(cudaStreamCreateWithFlags(&comp, cudaStreamNonBlocking));
     for (cudaStream_t* st : {&s_act_in, &s_act_out, &s_grad_in, &s_grad_out})
@@ -300,6 +354,7 @@ class Runtime {
         }
       }
     }
+    if (vp) SP_CUDA(cudaStreamCreateWithFlags(&s_vocab, cudaStreamNonBlocking));
     SP_TRY(alloc_params());
     SP_TRY(alloc_arena());
     SP_TRY(alloc_workspace());
@@ -520,10 +575,9 @@ class Runtime {
       lp[l].wd = take(h * H);
     }
     if (stage == 1) emb = take(int64_t(cfg.vocab) * h);
-    if (stage == p) {
-      final_norm = take(h);
-      head = take(int64_t(cfg.vocab) * h);
-    }
+    if (stage == p) final_norm = take(h);
+    if (vp) head = take(Vs * h);  // this stage's vocab shard
+    else if (stage == p) head = take(int64_t(cfg.vocab) * h);
     SP_TRY(alloc(&w, n_params));
     SP_TRY(alloc(&master, n_params));
     SP_TRY(alloc(&grad, n_params));
@@ -552,7 +606,7 @@ class Runtime {
     }
     if (emb >= 0) SP_TRY(normal(emb, int64_t(cfg.vocab) * h));
     if (final_norm >= 0) SP_TRY(ones(final_norm, h));
-    if (head >= 0) SP_TRY(normal(head, int64_t(cfg.vocab) * h));
+    if (head >= 0) SP_TRY(normal(head, (vp ? Vs : int64_t(cfg.vocab)) * h));
     return SP_OK;
   }
 
@@ -565,7 +619,9 @@ class Runtime {
       const double rest_b = double(rows) * h * 2 + double(Lps) * rows * kvd * 4 +                 // x, K/V
                             double(Lps) * cfg.slices * Ls * kvd * 8 +                               // dK/dV acc
                             double(Lps) * Ls * (6.0 * h + 3.0 * H) * 2 +                          // layer workspace
-                            (stage == p ? double(Ls) * cfg.vocab * 4 * 2 : 0.0) + 4.0 * double(1 << 30);  // logits + margin
+                            (vp ? double(Ls) * double(Vs) * 6 + double(vslots.size()) * Ls * h * 2
+                                : stage == p ? double(Ls) * cfg.vocab * 4 * 2 : 0.0) +
+                            4.0 * double(1 << 30);  // logits (or the vocab shard's) + margin
       stash = stash_b + rest_b < double(free_b);
     }
     SP_TRY(alloc(&x_pool, rows * h));
@@ -636,8 +692,21 @@ class Runtime {
     if (stage == p) {
       SP_TRY(alloc(&xf, Ls * h));
       SP_TRY(alloc(&rstd_f, Ls));
-      SP_TRY(alloc(&logits, Ls * int64_t(cfg.vocab)));
-      SP_TRY(alloc(&dlogits, Ls * int64_t(cfg.vocab)));
+      if (!vp) {
+        SP_TRY(alloc(&logits, Ls * int64_t(cfg.vocab)));
+        SP_TRY(alloc(&dlogits, Ls * int64_t(cfg.vocab)));
+      }
+    }
+    if (vp) {
+      for (VSlot& v : vslots) {
+        SP_TRY(alloc(&v.xf, Ls * h));
+        SP_TRY(alloc(&v.st, 4 * Ls));
+      }
+      vfree.clear();
+      for (int x = int(vslots.size()) - 1; x >= 0; --x) vfree.push_back(x);
+      SP_TRY(alloc(&vlogits, Ls * Vs));
+      SP_TRY(alloc(&vdlog, Ls * Vs));
+      SP_TRY(alloc(&vdxf, Ls * h));
     }
     return SP_OK;
   }
@@ -780,7 +849,26 @@ class Runtime {
       cudaEventDestroy(done);
     } else {
       SP_TRY(stage_forward(k, i, x_final, px, false));
+      if (vp) {  // x_final is overwritten by later passes: normalise into the slice's vocab slot now
+        VSlot* vs = nullptr;
+        SP_TRY(vslot_acquire(k, i, &vs));
+        SP_TRY(rmsnorm_fwd(x_final, W(final_norm), vs->xf, rstd_f, Ls, int(h), cfg.norm_eps, comp));
+      }
     }
+    return SP_OK;
+  }
+
+  int vslot_acquire(int k, int i, VSlot** out) {
+    auto it = vslot_of.find({k, i});
+    if (it != vslot_of.end()) {
+      *out = &vslots[it->second];
+      return SP_OK;
+    }
+    if (vfree.empty()) return set_error(SP_ERR_RUNTIME, "vocab slots exhausted");
+    const int vs_i = vfree.back();
+    vfree.pop_back();
+    vslot_of[{k, i}] = vs_i;
+    *out = &vslots[vs_i];
     return SP_OK;
   }
 
@@ -863,6 +951,53 @@ class Runtime {
     return SP_OK;
   }
 
+  // VocabForward(k,i): final hidden state of the slice from the last stage
+  // (broadcast), logits of this shard, softmax statistics all-reduced.
+  int run_vocab_fwd(int k, int i, cudaEvent_t t0) {
+    SP_CUDA(cudaEventRecord(t0, comp));
+    VSlot* vsp = nullptr;
+    SP_TRY(vslot_acquire(k, i, &vsp));  // on the last stage F(k,i,p) already filled xf
+    VSlot& vs = *vsp;
+    const int64_t tok0 = int64_t(k - 1) * cfg.seq_len + int64_t(i - 1) * Ls;
+    SP_TRY(link(comp, s_vocab));
+    SP_NCCL(ncclBroadcast(vs.xf, vs.xf, Ls * h, ncclBfloat16, p - 1, nc_bwd, s_vocab));
+    SP_TRY(link(s_vocab, comp));
+    SP_TRY(gemm(false, true, Ls, Vs, h, vs.xf, h, W(head), h, vlogits, Vs, true, 1.f, 0.f, comp));
+    float* m_loc = vs.st;
+    float* m_glob = vs.st + Ls;
+    float* zt = vs.st + 2 * Ls;
+    SP_TRY(xent_shard_stats(vlogits, targets + tok0, Ls, int(Vs), int(v0), m_loc, m_glob, zt, comp));
+    SP_TRY(link(comp, s_vocab));
+    SP_NCCL(ncclAllReduce(m_glob, m_glob, Ls, ncclFloat32, ncclMax, nc_bwd, s_vocab));
+    SP_TRY(link(s_vocab, comp));
+    SP_TRY(xent_shard_rescale(m_loc, m_glob, zt, Ls, comp));
+    SP_TRY(link(comp, s_vocab));
+    SP_NCCL(ncclAllReduce(zt, zt, 2 * Ls, ncclFloat32, ncclSum, nc_bwd, s_vocab));
+    SP_TRY(link(s_vocab, comp));
+    return SP_OK;
+  }
+
+  // VocabBackward(k,i): shard dlogits (softmax - onehot), dW_head of the
+  // shard, partial dX of the final hidden state reduced onto the last stage.
+  int run_vocab_bwd(int k, int i, cudaEvent_t t0) {
+    SP_CUDA(cudaEventRecord(t0, comp));
+    const int vs_i = vslot_of.at({k, i});
+    VSlot& vs = vslots[vs_i];
+    const int64_t tok0 = int64_t(k - 1) * cfg.seq_len + int64_t(i - 1) * Ls;
+    SP_TRY(gemm(false, true, Ls, Vs, h, vs.xf, h, W(head), h, vlogits, Vs, true, 1.f, 0.f, comp));
+    const float scale = 1.f / float(int64_t(cfg.microbatches) * cfg.seq_len);
+    SP_TRY(xent_shard_grad(vlogits, targets + tok0, Ls, int(Vs), int(v0), vs.st + Ls, vs.st + 2 * Ls, scale, vdlog,
+                           stage == p ? loss_dev : nullptr, comp));
+    SP_TRY(gemm(false, false, Ls, h, Vs, vdlog, Vs, W(head), h, vdxf, h, true, 1.f, 0.f, comp));  // partial dX
+    SP_TRY(gemm(true, false, Vs, h, Ls, vdlog, Vs, vs.xf, h, G(head), h, true, 1.f, 1.f, comp));    // dW shard
+    SP_TRY(link(comp, s_vocab));
+    SP_NCCL(ncclReduce(vdxf, vdxf, Ls * h, ncclFloat32, ncclSum, p - 1, nc_bwd, s_vocab));
+    SP_TRY(link(s_vocab, comp));
+    vfree.push_back(vs_i);
+    vslot_of.erase({k, i});
+    return SP_OK;
+  }
+
   int run_backward(int pid, int k, int i, cudaEvent_t t0) {
     const PassX* px = pass_x(pid);
     if (px && !px->in.empty()) SP_TRY(post_remote(*px));
@@ -894,6 +1029,13 @@ class Runtime {
     if (stage == p) {
       SP_CUDA(cudaStreamWaitEvent(comp, ev_gout_free[gout_idx], 0));
       SP_TRY(stage_forward(k, i, x_final, px, true));
+      if (vp) {  // dX of the final hidden state = sum of the shards' partials (VocabBackward, just before)
+        SP_TRY(rmsnorm_fwd(x_final, W(final_norm), xf, rstd_f, Ls, int(h), cfg.norm_eps, comp));
+        SP_TRY(f32_to_bf16(vdxf, tmp_h, Ls * h, comp));
+        SP_TRY(rmsnorm_bwd(tmp_h, x_final, W(final_norm), rstd_f, nullptr, dx, G(final_norm), Ls, int(h), comp));
+      }
+    }
+    if (stage == p && !vp) {
       // LM head + cross entropy
       const int64_t V = cfg.vocab;
       SP_TRY(rmsnorm_fwd(x_final, W(final_norm), xf, rstd_f, Ls, int(h), cfg.norm_eps, comp));
@@ -903,7 +1045,7 @@ class Runtime {
       SP_TRY(gemm(false, false, Ls, h, V, dlogits, V, W(head), h, tmp_h, h, false, 1.f, 0.f, comp));  // dxf
       SP_TRY(gemm(true, false, V, h, Ls, dlogits, V, xf, h, G(head), h, true, 1.f, 1.f, comp));        // dWhead
       SP_TRY(rmsnorm_bwd(tmp_h, x_final, W(final_norm), rstd_f, nullptr, dx, G(final_norm), Ls, int(h), comp));
-    } else {
+    } else if (stage < p) {
       SP_TRY(stage_forward(k, i, top, px, true));
     }
     for (int l = Lps - 1; l >= 0; --l) SP_TRY(layer_backward(l, k, i, dx, px));
@@ -947,7 +1089,7 @@ class Runtime {
     SP_CUDA(cudaEventRecord(step_start, comp));
     const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     if (stage == 1 && tok) SP_CUDA(cudaMemcpyAsync(tokens, tok, ntok * 4, kind, comp));
-    if (stage == p && tgt) SP_CUDA(cudaMemcpyAsync(targets, tgt, ntok * 4, kind, comp));
+    if ((stage == p || vp) && tgt) SP_CUDA(cudaMemcpyAsync(targets, tgt, ntok * 4, kind, comp));
     SP_CUDA(cudaMemsetAsync(loss_dev, 0, 4, comp));
     for (pipelab::PassId id : order) {
       const pipelab::Pass& ps = sched.passes[id];
@@ -955,6 +1097,8 @@ class Runtime {
       SP_CUDA(cudaEventCreate(&t.start));
       SP_CUDA(cudaEventCreate(&t.end));
       if (ps.kind == pipelab::PassKind::Forward) SP_TRY(run_forward(id, ps.microbatch, ps.slice, t.start));
+      else if (ps.kind == pipelab::PassKind::VocabForward) SP_TRY(run_vocab_fwd(ps.microbatch, ps.slice, t.start));
+      else if (ps.kind == pipelab::PassKind::VocabBackward) SP_TRY(run_vocab_bwd(ps.microbatch, ps.slice, t.start));
       else SP_TRY(run_backward(id, ps.microbatch, ps.slice, t.start));
       SP_CUDA(cudaEventRecord(t.end, comp));
       times.push_back(t);
@@ -977,6 +1121,7 @@ class Runtime {
         SP_TRY(link(cx[c], comp));
         SP_TRY(link(rx[c], comp));
       }
+    if (s_vocab) SP_TRY(link(s_vocab, comp));
     cudaEventDestroy(e1);
     cudaEventDestroy(e2);
     SP_CUDA(cudaEventRecord(step_end, comp));
@@ -1114,8 +1259,8 @@ int sp_runtime_param(void* handle, int layer, int which, float* host, int64_t co
     off = rt->emb, n = int64_t(rt->cfg.vocab) * h;
   } else if (which == 7) {
     off = rt->final_norm, n = h;
-  } else if (which == 8) {
-    off = rt->head, n = int64_t(rt->cfg.vocab) * h;
+  } else if (which == 8) {  // the full head, or this stage's vocab shard under vocab parallelism
+    off = rt->head, n = (rt->vp ? rt->Vs : int64_t(rt->cfg.vocab)) * h;
   }
   if (off < 0) return sp::set_error(SP_ERR_INVALID, "parameter %d not on this stage", which);
   if (count != n) return sp::set_error(SP_ERR_INVALID, "parameter size %lld != %lld", (long long)count, (long long)n);

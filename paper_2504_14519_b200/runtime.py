@@ -24,7 +24,7 @@ class _Cfg(C.Structure):
     _fields_ = [(n, C.c_int32) for n in ("layers", "hidden", "ffn_hidden", "heads", "kv_heads", "head_dim", "vocab",
                                          "microbatches", "slices", "pp", "rank", "exchange_mode")] + [
         ("seq_len", C.c_int64), ("rope_theta", C.c_float), ("norm_eps", C.c_float), ("lr", C.c_float),
-        ("seed", C.c_uint64), ("recompute", C.c_int32)]
+        ("seed", C.c_uint64), ("recompute", C.c_int32), ("vocab_parallel", C.c_int32)]
 
 
 RECOMPUTE = {"selective": 0, "full": 1, "auto": 2}
@@ -44,6 +44,7 @@ class StepConfig:
     pp: int = 1
     exchange: str = "off"
     recompute: str = "auto"  # "selective": stash attention O/LSE, "full": K1 again in the backward, "auto": selective if it fits
+    vocab_parallel: bool = False  # LM head + cross entropy split by vocabulary across the pp stages
     rope_theta: float = 10000.0
     norm_eps: float = 1e-5
     lr: float = 1e-4
@@ -81,7 +82,8 @@ class StepConfig:
     def to_c(self, rank: int) -> _Cfg:
         return _Cfg(self.layers, self.hidden, self.ffn_hidden, self.heads, self.kv_heads, self.head_dim, self.vocab,
                     self.microbatches, self.slices, self.pp, rank, N.MODES[self.exchange], self.seq_len,
-                    self.rope_theta, self.norm_eps, self.lr, self.seed, RECOMPUTE[self.recompute])
+                    self.rope_theta, self.norm_eps, self.lr, self.seed, RECOMPUTE[self.recompute],
+                    int(self.vocab_parallel))
 
     # ---- accounting ----
     def linear_params_per_layer(self) -> int:
@@ -235,7 +237,7 @@ class SlimPipeStep:
         h, H, qkv = c.hidden, c.ffn_hidden, (c.heads + 2 * c.kv_heads) * c.head_dim
         return {"attn_norm": (h,), "wqkv": (qkv, h), "wo": (h, c.heads * c.head_dim), "mlp_norm": (h,),
                 "wgu": (2 * H, h), "wd": (h, H), "embedding": (c.vocab, h), "final_norm": (h,),
-                "head": (c.vocab, h)}[which]
+                "head": (c.vocab // c.pp if (c.vocab_parallel and c.pp > 1) else c.vocab, h)}[which]
 
     def _param_io(self, layer: int, which: str, arr: np.ndarray | None, direction: int) -> np.ndarray:
         shape = self._param_shape(which)

@@ -32,7 +32,7 @@ def main():
     xmode = os.environ.get("SP_X", "off")
     cfg = StepConfig.c1(pp=world, microbatches=m, slices=n, layers=2 * world, exchange=xmode,
                         seq_len=1024 * n, recompute=os.environ.get("SP_RC", "selective"),
-                        kv_heads=int(os.environ.get("SP_KV", 4)))
+                        kv_heads=int(os.environ.get("SP_KV", 4)), vocab_parallel=os.environ.get("SP_VP") == "1")
     step = SlimPipeStep(cfg, rank, world)
     rng = np.random.default_rng(0)
     tok = rng.integers(0, cfg.vocab, (cfg.microbatches, cfg.seq_len), dtype=np.int32)
@@ -49,9 +49,13 @@ def main():
         mine["params"][(None, "embedding")] = step.get_param(0, "embedding")
         mine["grads"][(None, "embedding")] = step.get_grad(0, "embedding")
     if step.is_last:
-        for k in ("final_norm", "head"):
-            mine["params"][(None, k)] = step.get_param(0, k)
-            mine["grads"][(None, k)] = step.get_grad(0, k)
+        mine["params"][(None, "final_norm")] = step.get_param(0, "final_norm")
+        mine["grads"][(None, "final_norm")] = step.get_grad(0, "final_norm")
+    if cfg.vocab_parallel:  # every stage holds a vocabulary shard of the head
+        mine["head_shard"] = (step.get_param(0, "head"), step.get_grad(0, "head"))
+    elif step.is_last:
+        mine["params"][(None, "head")] = step.get_param(0, "head")
+        mine["grads"][(None, "head")] = step.get_grad(0, "head")
     mem = step.memory()
     mine["mem"] = mem
     mine["x"] = step.exchange_stats()
@@ -64,13 +68,17 @@ def main():
         for d in allv:
             P.update(d["params"])
             G.update(d["grads"])
+        if cfg.vocab_parallel:
+            P[(None, "head")] = np.concatenate([d["head_shard"][0] for d in allv], axis=0)
+            G[(None, "head")] = np.concatenate([d["head_shard"][1] for d in allv], axis=0)
         rnd = lambda x: torch.from_numpy(x).bfloat16().double().numpy()
         W = {k: [rnd(P[(l, k)]) for l in range(cfg.layers)] for k in NAMES}
         for k in ("embedding", "final_norm", "head"):
             W[k] = rnd(P[(None, k)])
         ref_loss, ref_g = MO.Model(W, cfg.heads, cfg.kv_heads, cfg.rope_theta, cfg.norm_eps).step(tok, tgt, n)
         gpu_loss = allv[-1]["loss"]
-        print(f"pp={world} m={m} n={n} exchange={xmode} loss gpu {gpu_loss:.6f} oracle {ref_loss:.6f}")
+        print(f"pp={world} m={m} n={n} exchange={xmode} vocab_parallel={cfg.vocab_parallel} "
+              f"loss gpu {gpu_loss:.6f} oracle {ref_loss:.6f}")
         xs = [d["x"] for d in allv]
         print("exchange stats per rank:", xs)
         if xmode != "off":

@@ -17,14 +17,18 @@ ROOT = Path(__file__).resolve().parents[1]
                                          (2, 2, 8, "early", "selective"), (2, 3, 4, "on", "selective"),
                                          (4, 2, 4, "off", "selective"), (4, 2, 8, "on", "selective"),
                                          (4, 2, 8, "early", "full"),
-                                         (2, 2, 4, "on", "selective-gqa")])  # GQA 4:2 through the exchange
+                                         (2, 2, 4, "on", "selective-gqa"),  # GQA 4:2 through the exchange
+                                         (2, 2, 4, "off", "selective-vp"),  # vocabulary parallelism (§8f)
+                                         (4, 2, 8, "off", "full-vp"), (4, 2, 8, "on", "selective-vp")])
 def test_pipeline_parallel_step_matches_oracle(pp, m, n, x, rc):
     if not torch.cuda.is_available() or torch.cuda.device_count() < pp:
         pytest.skip(f"needs {pp} GPUs")
-    gqa = rc.endswith("-gqa")
-    rc = rc.removesuffix("-gqa")
-    env = dict(os.environ, SP_M=str(m), SP_N=str(n), SP_X=x, SP_RC=rc, SP_KV="2" if gqa else "4")
-    port = 29500 + pp * 100 + m * 10 + n + len(x) + (50 if rc == "full" else 0) + (25 if gqa else 0)
+    gqa, vp = rc.endswith("-gqa"), rc.endswith("-vp")
+    rc = rc.removesuffix("-gqa").removesuffix("-vp")
+    env = dict(os.environ, SP_M=str(m), SP_N=str(n), SP_X=x, SP_RC=rc, SP_KV="2" if gqa else "4",
+               SP_VP="1" if vp else "0")
+    port = 29500 + pp * 100 + m * 10 + n + len(x) + (50 if rc == "full" else 0) + (25 if gqa else 0) + (
+        13 if vp else 0)
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={pp}",
                         "--master-addr", "127.0.0.1", "--master-port", str(port),
                         str(ROOT / "tests" / "mp_step_check.py")], env=env, capture_output=True, text=True,
