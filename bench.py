@@ -68,6 +68,8 @@ def parse():
                     help="attention workload redistribution (reference ExchangeMode); no effect at PP=1")
     ap.add_argument("--vocab-parallel", action="store_true",
                     help="shard the LM head and cross entropy over all stages (PP>1; SURVEY §8f rank 1)")
+    ap.add_argument("--interleave", type=int, default=1,
+                    help="v stages per GPU (interleaved SlimPipe, even PP; SURVEY §8f rank 2)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -85,13 +87,14 @@ def make_cfg(args, world):
     kw = {k: v for k, v in (("layers", args.layers or DEPTH[args.model]), ("seq_len", args.seq_len),
                             ("slices", args.slices), ("microbatches", args.microbatches)) if v is not None}
     return base.__class__(**{**base.__dict__, **kw, "pp": world, "exchange": args.exchange,
-                             "recompute": args.recompute, "vocab_parallel": bool(args.vocab_parallel and world > 1)})
+                             "recompute": args.recompute, "vocab_parallel": bool(args.vocab_parallel and world > 1),
+                             "interleave": args.interleave if world > 1 else 1})
 
 
 def workload_name(cfg, model="c2"):
     return (f"{MODEL_NAMES[model][0]} layer shapes x{cfg.layers} layers, {cfg.seq_len // 1024}K ctx, n={cfg.slices} slices, "
             f"m={cfg.microbatches}, PP={cfg.pp}, exchange={cfg.exchange}, recompute={cfg.recompute}"
-            + (", vocab-parallel" if cfg.vocab_parallel else ""))
+            + (", vocab-parallel" if cfg.vocab_parallel else "") + (f", v={cfg.interleave}" if cfg.interleave > 1 else ""))
 
 
 # ----------------------------------------------------------------- clocks
@@ -360,7 +363,7 @@ def main():
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic tokens, random-init weights",
             "config": {"workload": workload_name(cfg, args.model), "model": MODEL_NAMES[args.model][1], "layers": cfg.layers,
                        "global_batch": cfg.microbatches, "seq_len": cfg.seq_len, "slices": cfg.slices,
-                       "parallelism": f"pp{world}", "exchange": cfg.exchange, "vocab_parallel": cfg.vocab_parallel,
+                       "parallelism": f"pp{world}", "exchange": cfg.exchange, "vocab_parallel": cfg.vocab_parallel, "interleave": cfg.interleave,
                        "recompute": cfg.recompute if cfg.recompute != "auto" else f"auto->{mem['recompute']}",
                        "l2": "inputs larger than L2 (per-step working set tens of GB)"},
             "mfu": mfu, "mfu_nominal": mfu_nominal, "mfu_peak_tflops": peak_tf,

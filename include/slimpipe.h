@@ -165,6 +165,11 @@ typedef struct {
    * split by vocabulary across all stages (reference place_vocab with
    * distribute = true, simulator.cpp:414-522); 0: the last stage owns them. */
   int32_t vocab_parallel;
+  /* v, stages per device (interleaved SlimPipe, reference gen_slimpipe with
+   * v > 1, schedule.cpp:261-270): device d owns stages d+1, d+1+p, ...;
+   * 0 or 1 = one stage per device.  v > 1 needs an even pp >= 2, exchange
+   * off and vocab_parallel 0. */
+  int32_t interleave;
 } sp_model_config;
 
 #define SP_STEP_NO_OPTIMIZER 1
@@ -189,7 +194,11 @@ void* sp_runtime_stream(void* handle);
 int sp_runtime_timeline(void* handle, double* out, int cap);
 int sp_runtime_attn_stats(void* handle, double* out6);
 int sp_runtime_memory(void* handle, int64_t* out7);
-int sp_runtime_recompute(void* handle); /* policy in effect: 0 selective, 1 full */
+int sp_runtime_recompute(void* handle);
+/* Diagnostics: position in this rank's pass order of the first pass not yet
+ * finished on the compute stream (-1: all done); out4 = kind, microbatch,
+ * slice, stage of that pass.  Non-blocking. */
+int sp_runtime_progress(void* handle, int32_t* out4); /* policy in effect: 0 selective, 1 full */
 int sp_runtime_param(void* handle, int layer, int which, float* host, int64_t count, int dir);
 /* {passes with outgoing transfers, passes with incoming transfers, bytes sent
  *  by this rank through the exchange in the last step} */

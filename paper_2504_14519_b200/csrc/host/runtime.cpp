@@ -1,5 +1,7 @@
-// The B200 sliced-1F1B step executor: one process (rank) per GPU, pipeline
-// stage s = rank + 1 (v = 1, reference stage_owner schedule.cpp:158-164).
+// The B200 sliced-1F1B step executor: one process (rank) per GPU owning
+// pipeline stages s = rank + 1 + c*p, c < v (reference stage_owner,
+// schedule.cpp:158-164; v > 1 is interleaved SlimPipe, the stage links then
+// form a ring and the last device sends stage c*p+p's output to device 0).
 //
 // It walks device_order[rank] of gen_slimpipe (bit-exact host planning) and
 // executes each pass on the GPU:
@@ -31,6 +33,7 @@
 #include <map>
 #include <memory>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "errors.hpp"
@@ -83,7 +86,9 @@ struct AttnTimer {
 class Runtime {
  public:
   sp_model_config cfg{};
-  int rank = 0, p = 1, stage = 1, Lps = 1;
+  int rank = 0, p = 1, stage = 1, Lps = 1;  // stage: the current pass's (global) stage
+  int v = 1, nst = 1, cur = 0, lbase = 0;   // stages per device, total stages, pass's local chunk, its first layer
+  bool first_dev = true, last_dev = true;   // owns stage 1 / stage nst
   int64_t Ls = 0, h = 0, H = 0, qd = 0, kvd = 0, qkv_w = 0;
   pipelab::Schedule sched;
   std::vector<pipelab::PassId> order;
@@ -223,6 +228,8 @@ class Runtime {
   }
 
   bf16raw* W(int64_t off) { return w + off; }
+  // arena slot key of slice (k, j) at the current pass's local chunk
+  std::pair<int, int> sk(int k, int j) const { return {k, (cur << 20) | j}; }
   float* G(int64_t off) { return grad + off; }
 
   int init(const sp_model_config& c, const void* ids) {
@@ -230,10 +237,18 @@ class Runtime {
     rank = c.rank;
     p = c.pp;
     stage = rank + 1;
-    if (c.layers % p) return set_error(SP_ERR_INVALID, "layers (%d) must divide by pp (%d)", c.layers, p);
+    v = c.interleave <= 0 ? 1 : c.interleave;
+    nst = p * v;
+    first_dev = rank == 0;
+    last_dev = rank == p - 1;
+    if (v > 1 && (p < 2 || p % 2))
+      return set_error(SP_ERR_UNSUPPORTED, "interleave > 1 needs an even pp >= 2 (stage ring links)");
+    if (v > 1 && (c.exchange_mode != 0 || c.vocab_parallel))
+      return set_error(SP_ERR_UNSUPPORTED, "interleave > 1 runs with exchange off and vocab_parallel 0");
+    if (c.layers % nst) return set_error(SP_ERR_INVALID, "layers (%d) must divide by pp*v (%d)", c.layers, nst);
     if (c.seq_len % c.slices) return set_error(SP_ERR_INVALID, "run: seq_len must be divisible by slices");
     if (c.hidden != c.heads * c.head_dim) return set_error(SP_ERR_INVALID, "hidden != heads * head_dim");
-    Lps = c.layers / p;
+    Lps = c.layers / nst;
     Ls = c.seq_len / c.slices;
     if (c.recompute < 0 || c.recompute > 2) return set_error(SP_ERR_INVALID, "recompute must be 0, 1 or 2");
     stash = c.recompute != 1;  // 2 (auto) is settled in alloc_arena once the parameters are resident
@@ -246,7 +261,7 @@ class Runtime {
 
     pipelab::GenConfig gc;
     gc.p = p;
-    gc.v = 1;
+    gc.v = v;
     gc.m = c.microbatches;
     gc.n = c.slices;
     gc.seq_len = c.seq_len;
@@ -258,7 +273,8 @@ class Runtime {
     const pipelab::Diagnostics diag = pipelab::validate_schedule(sched);
     if (!diag.ok()) return set_error(SP_ERR_RUNTIME, "schedule invalid: %s", diag.first()->message.c_str());
     order = sched.device_order[rank];
-    ledger = pipelab::ledger_from_order(sched, pipelab::unit_memory_model(p, 1, c.slices));
+    ledger = pipelab::ledger_from_order(sched, pipelab::unit_memory_model(p, v, c.slices));
+    if (v > 1) SP_TRY(check_ring_order());
     slots = int(ledger.per_device[rank].chunk_pool_size);
     if (c.exchange_mode != 0 && p > 1) {
       if (c.head_dim != 128 && c.head_dim != 64) return set_error(SP_ERR_UNSUPPORTED, "exchange: head_dim");
@@ -293,7 +309,7 @@ class Runtime {
       int live = 0, peak = 0;
       for (pipelab::PassId id : order) {
         // the last stage takes the slot at F(k,i,p) (it normalises the output there)
-        const auto acq = stage == p ? pipelab::PassKind::Forward : pipelab::PassKind::VocabForward;
+        const auto acq = last_dev ? pipelab::PassKind::Forward : pipelab::PassKind::VocabForward;
         if (sched.passes[id].kind == acq) peak = std::max(peak, ++live);
         if (sched.passes[id].kind == pipelab::PassKind::VocabBackward) --live;
       }
@@ -324,23 +340,28 @@ class Runtime {
       SP_NCCL(ncclCommInitRank(&nc_fwd, p, id[0], rank));
       SP_NCCL(ncclCommInitRank(&nc_bwd, p, id[1], rank));
       // link (r, r+1) comes from split A when r is even, split B when r is odd
-      auto split = [&](ncclComm_t parent, int color, ncclComm_t* out) -> int {
-        SP_NCCL(ncclCommSplit(parent, color, rank, out, nullptr));
+      auto split = [&](ncclComm_t parent, int color, int key, ncclComm_t* out) -> int {
+        SP_NCCL(ncclCommSplit(parent, color, key, out, nullptr));
         return SP_OK;
       };
-      const int colA = rank / 2;                                   // {0,1} {2,3} ...
-      const int colB = rank == 0 ? NCCL_SPLIT_NOCOLOR : (rank + 1) / 2;  // {1,2} {3,4} ...
+      // v > 1 (even p): split B also carries the ring's wrap link (p-1, 0),
+      // where rank 0 is the receiving end and so takes link rank 1 (key p)
+      const bool ring = v > 1;
+      const int colA = rank / 2;  // {0,1} {2,3} ...
+      const int colB = ring ? (rank % 2 ? (rank + 1) / 2 : rank / 2) % (p / 2)
+                            : (rank == 0 ? NCCL_SPLIT_NOCOLOR : (rank + 1) / 2);  // {1,2} {3,4} ... [{p-1,0}]
+      const int keyB = ring && rank == 0 ? p : rank;
       ncclComm_t fa = nullptr, fb = nullptr, ga = nullptr, gb = nullptr;
-      SP_TRY(split(nc_fwd, (rank == p - 1 && rank % 2 == 0) ? NCCL_SPLIT_NOCOLOR : colA, &fa));
-      SP_TRY(split(nc_fwd, (rank == p - 1 && rank % 2 == 1) ? NCCL_SPLIT_NOCOLOR : colB, &fb));
-      SP_TRY(split(nc_bwd, (rank == p - 1 && rank % 2 == 0) ? NCCL_SPLIT_NOCOLOR : colA, &ga));
-      SP_TRY(split(nc_bwd, (rank == p - 1 && rank % 2 == 1) ? NCCL_SPLIT_NOCOLOR : colB, &gb));
+      SP_TRY(split(nc_fwd, (rank == p - 1 && rank % 2 == 0) ? NCCL_SPLIT_NOCOLOR : colA, rank, &fa));
+      SP_TRY(split(nc_fwd, (!ring && rank == p - 1 && rank % 2 == 1) ? NCCL_SPLIT_NOCOLOR : colB, keyB, &fb));
+      SP_TRY(split(nc_bwd, (rank == p - 1 && rank % 2 == 0) ? NCCL_SPLIT_NOCOLOR : colA, rank, &ga));
+      SP_TRY(split(nc_bwd, (!ring && rank == p - 1 && rank % 2 == 1) ? NCCL_SPLIT_NOCOLOR : colB, keyB, &gb));
       const bool even = rank % 2 == 0;
-      if (stage < p) {  // link to the next stage
+      if (!last_dev || ring) {  // link to the next stage
         c_act_out = even ? fa : fb;
         c_grad_in = even ? ga : gb;
       }
-      if (stage > 1) {  // link to the previous stage (r-1, r): split A iff r-1 even
+      if (!first_dev || ring) {  // link to the previous stage (r-1, r): split A iff r-1 even
         c_act_in = even ? fb : fa;
         c_grad_out = even ? gb : ga;
       }
@@ -361,6 +382,46 @@ class Runtime {
     SP_TRY(alloc_exchange());
     SP_TRY(init_weights(c.seed));
     SP_CUDA(cudaStreamSynchronize(comp));
+    return SP_OK;
+  }
+
+  // Interleaved pre-flight (v > 1): every stage link is one FIFO pair of
+  // NCCL streams, so the sender's order of F outputs (B input grads) on a
+  // link must equal the receiver's order of the passes consuming them; and
+  // each local chunk's backward must run a microbatch's slices n..1
+  // back to back (one dK/dV accumulator set per chunk).
+  int check_ring_order() const {
+    using Key = std::tuple<int, int, int>;
+    for (int d = 0; d < p; ++d) {
+      const int nx = (d + 1) % p;
+      std::vector<Key> snd, rcv, gsnd, grcv;
+      for (pipelab::PassId id : sched.device_order[d]) {
+        const pipelab::Pass& q = sched.passes[id];
+        if (q.kind == pipelab::PassKind::Forward && q.stage < nst) snd.emplace_back(q.microbatch, q.slice, q.stage);
+        if (q.kind == pipelab::PassKind::BackwardFused && q.stage > 1)
+          gsnd.emplace_back(q.microbatch, q.slice, q.stage - 1);
+      }
+      for (pipelab::PassId id : sched.device_order[nx]) {
+        const pipelab::Pass& q = sched.passes[id];
+        if (q.kind == pipelab::PassKind::Forward && q.stage > 1) rcv.emplace_back(q.microbatch, q.slice, q.stage - 1);
+      }
+      for (pipelab::PassId id : sched.device_order[(d + p - 1) % p]) {
+        const pipelab::Pass& q = sched.passes[id];
+        if (q.kind == pipelab::PassKind::BackwardFused && q.stage < nst)
+          grcv.emplace_back(q.microbatch, q.slice, q.stage);
+      }
+      if (snd != rcv || gsnd != grcv)
+        return set_error(SP_ERR_UNSUPPORTED, "interleaved schedule: link %d order differs between its ends", d);
+      std::vector<std::vector<std::pair<int, int>>> per(static_cast<size_t>(v));
+      for (pipelab::PassId id : sched.device_order[d]) {
+        const pipelab::Pass& q = sched.passes[id];
+        if (q.kind != pipelab::PassKind::Forward) per[size_t((q.stage - 1) / p)].emplace_back(q.microbatch, q.slice);
+      }
+      for (const auto& seq : per)
+        for (std::size_t x = 0; x < seq.size(); ++x)
+          if (seq[x].second != cfg.slices - int(x % cfg.slices) || (x % cfg.slices && seq[x].first != seq[x - 1].first))
+            return set_error(SP_ERR_UNSUPPORTED, "interleaved schedule: backward slices of a chunk interleave");
+    }
     return SP_OK;
   }
 
@@ -459,10 +520,10 @@ class Runtime {
   }
   int send_chunks(int l, int k, const XOut& xo, int c) {
     for (int ch : xo.chunks)
-      SP_NCCL(ncclSend(k_pool[l] + int64_t(slot_of.at({k, ch})) * Ls * kvd, Ls * kvd, ncclBfloat16, xo.peer, nc_x[c],
+      SP_NCCL(ncclSend(k_pool[l] + int64_t(slot_of.at(sk(k, ch))) * Ls * kvd, Ls * kvd, ncclBfloat16, xo.peer, nc_x[c],
                        cx[c]));
     for (int ch : xo.chunks)
-      SP_NCCL(ncclSend(v_pool[l] + int64_t(slot_of.at({k, ch})) * Ls * kvd, Ls * kvd, ncclBfloat16, xo.peer, nc_x[c],
+      SP_NCCL(ncclSend(v_pool[l] + int64_t(slot_of.at(sk(k, ch))) * Ls * kvd, Ls * kvd, ncclBfloat16, xo.peer, nc_x[c],
                        cx[c]));
     x_bytes_sent += 2 * int64_t(xo.chunks.size()) * Ls * kvd * 2;
     return SP_OK;
@@ -479,7 +540,7 @@ class Runtime {
         for (int ch : xo.chunks) shipped[ch] = 1;
     for (int j = 1; j <= i; ++j)
       if (!shipped[j]) {
-        rows.push_back(int32_t(slot_of.at({k, j}) * Ls));
+        rows.push_back(int32_t(slot_of.at(sk(k, j)) * Ls));
         acc.push_back(int32_t((j - 1) * Ls));
       }
     causal = shipped[i] ? 0 : 1;
@@ -565,8 +626,8 @@ class Runtime {
       n_params += (n + 127) / 128 * 128;
       return off;
     };
-    lp.resize(Lps);
-    for (int l = 0; l < Lps; ++l) {
+    lp.resize(size_t(v) * Lps);  // local chunk c's layers at [c*Lps, (c+1)*Lps)
+    for (int l = 0; l < v * Lps; ++l) {
       lp[l].attn_norm = take(h);
       lp[l].wqkv = take(qkv_w * h);
       lp[l].wo = take(h * qd);
@@ -574,10 +635,10 @@ class Runtime {
       lp[l].wgu = take(2 * H * h);
       lp[l].wd = take(h * H);
     }
-    if (stage == 1) emb = take(int64_t(cfg.vocab) * h);
-    if (stage == p) final_norm = take(h);
+    if (first_dev) emb = take(int64_t(cfg.vocab) * h);
+    if (last_dev) final_norm = take(h);
     if (vp) head = take(Vs * h);  // this stage's vocab shard
-    else if (stage == p) head = take(int64_t(cfg.vocab) * h);
+    else if (last_dev) head = take(int64_t(cfg.vocab) * h);
     SP_TRY(alloc(&w, n_params));
     SP_TRY(alloc(&master, n_params));
     SP_TRY(alloc(&grad, n_params));
@@ -591,12 +652,12 @@ class Runtime {
 
   int init_weights(uint64_t seed) {
     const float std_w = 0.02f;
-    uint64_t tag = seed * 1000003ull + uint64_t(stage) * 7919ull;
+    uint64_t tag = seed * 1000003ull + uint64_t(rank + 1) * 7919ull;
     auto normal = [&](int64_t off, int64_t n) {
       return init_params(master + off, w + off, n, ++tag, std_w, 0.f, 0, comp);
     };
     auto ones = [&](int64_t off, int64_t n) { return init_params(master + off, w + off, n, ++tag, 0.f, 1.f, 1, comp); };
-    for (int l = 0; l < Lps; ++l) {
+    for (int l = 0; l < v * Lps; ++l) {
       SP_TRY(ones(lp[l].attn_norm, h));
       SP_TRY(normal(lp[l].wqkv, qkv_w * h));
       SP_TRY(normal(lp[l].wo, h * qd));
@@ -617,10 +678,10 @@ class Runtime {
       SP_CUDA(cudaMemGetInfo(&free_b, &total_b));
       const double stash_b = double(Lps) * rows * (qd * 2 + double(cfg.heads) * 4);
       const double rest_b = double(rows) * h * 2 + double(Lps) * rows * kvd * 4 +                 // x, K/V
-                            double(Lps) * cfg.slices * Ls * kvd * 8 +                               // dK/dV acc
+                            double(v) * Lps * cfg.slices * Ls * kvd * 8 +                           // dK/dV acc
                             double(Lps) * Ls * (6.0 * h + 3.0 * H) * 2 +                          // layer workspace
                             (vp ? double(Ls) * double(Vs) * 6 + double(vslots.size()) * Ls * h * 2
-                                : stage == p ? double(Ls) * cfg.vocab * 4 * 2 : 0.0) +
+                                : last_dev ? double(Ls) * cfg.vocab * 4 * 2 : 0.0) +
                             4.0 * double(1 << 30);  // logits (or the vocab shard's) + margin
       stash = stash_b + rest_b < double(free_b);
     }
@@ -635,12 +696,14 @@ class Runtime {
     }
     k_pool.assign(Lps, nullptr);
     v_pool.assign(Lps, nullptr);
-    dk_acc.assign(Lps, nullptr);
-    dv_acc.assign(Lps, nullptr);
+    dk_acc.assign(size_t(v) * Lps, nullptr);  // per local chunk and layer
+    dv_acc.assign(size_t(v) * Lps, nullptr);
     const int64_t acc_rows = int64_t(cfg.slices) * Ls;
     for (int l = 0; l < Lps; ++l) {
       SP_TRY(alloc(&k_pool[l], rows * kvd));
       SP_TRY(alloc(&v_pool[l], rows * kvd));
+    }
+    for (int l = 0; l < v * Lps; ++l) {
       SP_TRY(alloc(&dk_acc[l], acc_rows * kvd));
       SP_TRY(alloc(&dv_acc[l], acc_rows * kvd));
       SP_CUDA(cudaMemsetAsync(dk_acc[l], 0, acc_rows * kvd * 4, comp));
@@ -676,7 +739,7 @@ class Runtime {
     SP_TRY(alloc(&tmp_H, Ls * H));
     SP_TRY(alloc(&tmp_2H, Ls * 2 * H));
     for (int x = 0; x < 2; ++x) {
-      if (stage > 1) SP_TRY(alloc(&ain_buf[x], Ls * h));
+      if (!first_dev || v > 1) SP_TRY(alloc(&ain_buf[x], Ls * h));
       SP_TRY(alloc(&out_buf[x], Ls * h));
       SP_TRY(alloc(&gin_buf[x], Ls * h));
       SP_TRY(alloc(&gout_buf[x], Ls * h));
@@ -689,7 +752,7 @@ class Runtime {
     SP_TRY(alloc(&loss_dev, 1));
     SP_TRY(alloc(&tokens, int64_t(cfg.microbatches) * cfg.seq_len));
     SP_TRY(alloc(&targets, int64_t(cfg.microbatches) * cfg.seq_len));
-    if (stage == p) {
+    if (last_dev) {
       SP_TRY(alloc(&xf, Ls * h));
       SP_TRY(alloc(&rstd_f, Ls));
       if (!vp) {
@@ -714,7 +777,7 @@ class Runtime {
   // -------------------------------------------------------------- passes
   std::vector<int32_t> chunk_rows(int k, int i) const {
     std::vector<int32_t> rows;
-    for (int j = 1; j <= i; ++j) rows.push_back(int32_t(slot_of.at({k, j}) * Ls));
+    for (int j = 1; j <= i; ++j) rows.push_back(int32_t(slot_of.at(sk(k, j)) * Ls));
     return rows;
   }
 
@@ -784,8 +847,8 @@ class Runtime {
 
   int layer_forward(int l, int k, int i, bf16raw* x_out, const PassX* px, bool recompute) {
     LayerWs& x = ws[l];
-    const LayerParams& P = lp[l];
-    const int slot = slot_of.at({k, i});
+    const LayerParams& P = lp[lbase + l];
+    const int slot = slot_of.at(sk(k, i));
     bind_attn_out(l, slot);
     const int64_t pos0 = int64_t(i - 1) * Ls;
     SP_TRY(rmsnorm_fwd(x.x_in, W(P.attn_norm), x.xn, x.rstd1, Ls, int(h), cfg.norm_eps, comp));
@@ -815,7 +878,7 @@ class Runtime {
     if (free_slots.empty()) return set_error(SP_ERR_RUNTIME, "arena exhausted (ledger/schedule mismatch)");
     const int slot = free_slots.back();
     free_slots.pop_back();
-    slot_of[{k, i}] = slot;
+    slot_of[sk(k, i)] = slot;
     slots_high_water = std::max(slots_high_water, ++slots_in_use);
     bf16raw* xs = x_pool + int64_t(slot) * Ls * h;
     const int64_t tok0 = int64_t(k - 1) * cfg.seq_len + int64_t(i - 1) * Ls;
@@ -835,7 +898,7 @@ class Runtime {
       SP_CUDA(cudaEventRecord(ev_ain_free[b], comp));
     }
     SP_CUDA(cudaMemcpyAsync(ws[0].x_in, xs, Ls * h * 2, cudaMemcpyDeviceToDevice, comp));
-    if (stage < p) {
+    if (stage < nst) {
       const int b = out_idx;
       out_idx ^= 1;
       SP_CUDA(cudaStreamWaitEvent(comp, ev_out_free[b], 0));
@@ -873,9 +936,9 @@ class Runtime {
   }
 
   int layer_backward(int l, int k, int i, bf16raw* dx, const PassX* px) {
-    bind_attn_out(l, slot_of.at({k, i}));
+    bind_attn_out(l, slot_of.at(sk(k, i)));
     LayerWs& x = ws[l];
-    const LayerParams& P = lp[l];
+    const LayerParams& P = lp[lbase + l];
     const int64_t pos0 = int64_t(i - 1) * Ls;
     // MLP
     SP_TRY(gemm(false, false, Ls, H, h, dx, h, W(P.wd), H, tmp_H, H, false, 1.f, 0.f, comp));      // d_act
@@ -917,7 +980,7 @@ class Runtime {
     SP_CUDA(cudaEventRecord(t.a, comp));
     SP_TRY(sp_attn_bwd_core(x.q, Ls, qd, k_pool[l], v_pool[l], int64_t(slots) * Ls, kvd, rows.data(), int(rows.size()),
                             int(Ls), cfg.heads, cfg.kv_heads, cfg.head_dim, causal, tmp_h, qd, delta_ws, dq_acc,
-                            dk_acc[l], dv_acc[l], int64_t(cfg.slices) * Ls, acc_rows.data(), comp));
+                            dk_acc[lbase + l], dv_acc[lbase + l], int64_t(cfg.slices) * Ls, acc_rows.data(), comp));
     SP_CUDA(cudaEventRecord(t.b, comp));
     attn_times.push_back(t);
     if (out) {
@@ -937,13 +1000,13 @@ class Runtime {
         SP_TRY(add_f32(dq_acc, b.dq_rem + tt * Ls * qd, Ls * qd, comp));
         for (std::size_t x2 = 0; x2 < xo.chunks.size(); ++x2) {
           const int64_t dst = int64_t(xo.chunks[x2] - 1) * Ls * kvd, src = int64_t(xo.base + x2) * Ls * kvd;
-          SP_TRY(add_f32(dk_acc[l] + dst, b.dk_rem + src, Ls * kvd, comp));
-          SP_TRY(add_f32(dv_acc[l] + dst, b.dv_rem + src, Ls * kvd, comp));
+          SP_TRY(add_f32(dk_acc[lbase + l] + dst, b.dk_rem + src, Ls * kvd, comp));
+          SP_TRY(add_f32(dv_acc[lbase + l] + dst, b.dv_rem + src, Ls * kvd, comp));
         }
       }
     }
     // chunk i's dK/dV is complete: RoPE backward into d_qkv and reset the rows
-    SP_TRY(rope_qkv_bwd(dq_acc, dk_acc[l] + pos0 * kvd, dv_acc[l] + pos0 * kvd, kvd, Ls, cfg.heads, cfg.kv_heads,
+    SP_TRY(rope_qkv_bwd(dq_acc, dk_acc[lbase + l] + pos0 * kvd, dv_acc[lbase + l] + pos0 * kvd, kvd, Ls, cfg.heads, cfg.kv_heads,
                         cfg.head_dim, pos0, rope_cos, rope_sin, dqkv, 1, comp));
     SP_TRY(gemm(false, false, Ls, h, qkv_w, dqkv, qkv_w, W(P.wqkv), h, tmp_h, h, false, 1.f, 0.f, comp));   // dxn
     SP_TRY(gemm(true, false, qkv_w, h, Ls, dqkv, qkv_w, x.xn, h, G(P.wqkv), h, true, 1.f, 1.f, comp));      // dWqkv
@@ -987,7 +1050,7 @@ class Runtime {
     SP_TRY(gemm(false, true, Ls, Vs, h, vs.xf, h, W(head), h, vlogits, Vs, true, 1.f, 0.f, comp));
     const float scale = 1.f / float(int64_t(cfg.microbatches) * cfg.seq_len);
     SP_TRY(xent_shard_grad(vlogits, targets + tok0, Ls, int(Vs), int(v0), vs.st + Ls, vs.st + 2 * Ls, scale, vdlog,
-                           stage == p ? loss_dev : nullptr, comp));
+                           last_dev ? loss_dev : nullptr, comp));
     SP_TRY(gemm(false, false, Ls, h, Vs, vdlog, Vs, W(head), h, vdxf, h, true, 1.f, 0.f, comp));  // partial dX
     SP_TRY(gemm(true, false, Vs, h, Ls, vdlog, Vs, vs.xf, h, G(head), h, true, 1.f, 1.f, comp));    // dW shard
     SP_TRY(link(comp, s_vocab));
@@ -1001,13 +1064,13 @@ class Runtime {
   int run_backward(int pid, int k, int i, cudaEvent_t t0) {
     const PassX* px = pass_x(pid);
     if (px && !px->in.empty()) SP_TRY(post_remote(*px));
-    const int slot = slot_of.at({k, i});
+    const int slot = slot_of.at(sk(k, i));
     bf16raw* xs = x_pool + int64_t(slot) * Ls * h;
     const int64_t tok0 = int64_t(k - 1) * cfg.seq_len + int64_t(i - 1) * Ls;
     // gradient input
     bf16raw* dx = nullptr;
     int gb = -1;
-    if (stage < p) {
+    if (stage < nst) {
       gb = gin_idx;
       gin_idx ^= 1;
       dx = gin_buf[gb];
@@ -1025,8 +1088,8 @@ class Runtime {
     }
     // recompute (Full checkpointing)
     SP_CUDA(cudaMemcpyAsync(ws[0].x_in, xs, Ls * h * 2, cudaMemcpyDeviceToDevice, comp));
-    bf16raw* top = stage < p ? tmp_h : x_final;
-    if (stage == p) {
+    bf16raw* top = stage < nst ? tmp_h : x_final;
+    if (stage == nst) {
       SP_CUDA(cudaStreamWaitEvent(comp, ev_gout_free[gout_idx], 0));
       SP_TRY(stage_forward(k, i, x_final, px, true));
       if (vp) {  // dX of the final hidden state = sum of the shards' partials (VocabBackward, just before)
@@ -1035,7 +1098,7 @@ class Runtime {
         SP_TRY(rmsnorm_bwd(tmp_h, x_final, W(final_norm), rstd_f, nullptr, dx, G(final_norm), Ls, int(h), comp));
       }
     }
-    if (stage == p && !vp) {
+    if (stage == nst && !vp) {
       // LM head + cross entropy
       const int64_t V = cfg.vocab;
       SP_TRY(rmsnorm_fwd(x_final, W(final_norm), xf, rstd_f, Ls, int(h), cfg.norm_eps, comp));
@@ -1045,7 +1108,7 @@ class Runtime {
       SP_TRY(gemm(false, false, Ls, h, V, dlogits, V, W(head), h, tmp_h, h, false, 1.f, 0.f, comp));  // dxf
       SP_TRY(gemm(true, false, V, h, Ls, dlogits, V, xf, h, G(head), h, true, 1.f, 1.f, comp));        // dWhead
       SP_TRY(rmsnorm_bwd(tmp_h, x_final, W(final_norm), rstd_f, nullptr, dx, G(final_norm), Ls, int(h), comp));
-    } else if (stage < p) {
+    } else if (stage < nst) {
       SP_TRY(stage_forward(k, i, top, px, true));
     }
     for (int l = Lps - 1; l >= 0; --l) SP_TRY(layer_backward(l, k, i, dx, px));
@@ -1067,7 +1130,7 @@ class Runtime {
       }
     }
     free_slots.push_back(slot);  // LIFO reuse
-    slot_of.erase({k, i});
+    slot_of.erase(sk(k, i));
     --slots_in_use;
     return SP_OK;
   }
@@ -1088,12 +1151,17 @@ class Runtime {
     const int64_t ntok = int64_t(cfg.microbatches) * cfg.seq_len;
     SP_CUDA(cudaEventRecord(step_start, comp));
     const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-    if (stage == 1 && tok) SP_CUDA(cudaMemcpyAsync(tokens, tok, ntok * 4, kind, comp));
-    if ((stage == p || vp) && tgt) SP_CUDA(cudaMemcpyAsync(targets, tgt, ntok * 4, kind, comp));
+    if (first_dev && tok) SP_CUDA(cudaMemcpyAsync(tokens, tok, ntok * 4, kind, comp));
+    if ((last_dev || vp) && tgt) SP_CUDA(cudaMemcpyAsync(targets, tgt, ntok * 4, kind, comp));
     SP_CUDA(cudaMemsetAsync(loss_dev, 0, 4, comp));
     for (pipelab::PassId id : order) {
       const pipelab::Pass& ps = sched.passes[id];
       PassTime t{id, nullptr, nullptr};
+      if (ps.kind == pipelab::PassKind::Forward || ps.kind == pipelab::PassKind::BackwardFused) {
+        stage = ps.stage;
+        cur = (stage - 1) / p;
+        lbase = cur * Lps;
+      }
       SP_CUDA(cudaEventCreate(&t.start));
       SP_CUDA(cudaEventCreate(&t.end));
       if (ps.kind == pipelab::PassKind::Forward) SP_TRY(run_forward(id, ps.microbatch, ps.slice, t.start));
@@ -1129,7 +1197,7 @@ class Runtime {
       float l = 0.f;
       SP_CUDA(cudaMemcpyAsync(&l, loss_dev, 4, cudaMemcpyDeviceToHost, comp));
       SP_CUDA(cudaStreamSynchronize(comp));
-      *loss_out = stage == p ? l / float(ntok) : 0.f;
+      *loss_out = last_dev ? l / float(ntok) : 0.f;
     }
     return SP_OK;
   }
@@ -1166,6 +1234,21 @@ int sp_runtime_destroy(void* handle) {
 int sp_runtime_step(void* handle, const int32_t* tokens, const int32_t* targets, int on_device, int flags,
                     float* loss) {
   return static_cast<Runtime*>(handle)->step(tokens, targets, on_device, flags, loss);
+}
+
+// Diagnostics: index (in device order) of the first pass whose end event has
+// not completed on the compute stream, or -1 when all have; writes that
+// pass's (kind, microbatch, slice, stage) to out4.
+int sp_runtime_progress(void* handle, int32_t* out4) {
+  Runtime* rt = static_cast<Runtime*>(handle);
+  for (std::size_t x = 0; x < rt->times.size(); ++x) {
+    if (cudaEventQuery(rt->times[x].end) == cudaErrorNotReady) {
+      const pipelab::Pass& q = rt->sched.passes[size_t(rt->times[x].pass)];
+      out4[0] = int32_t(q.kind), out4[1] = q.microbatch, out4[2] = q.slice, out4[3] = q.stage;
+      return int(x);
+    }
+  }
+  return -1;
 }
 
 int sp_runtime_sync(void* handle) {
@@ -1249,7 +1332,8 @@ int sp_runtime_param(void* handle, int layer, int which, float* host, int64_t co
   int64_t off = -1, n = 0;
   const int64_t h = rt->h, H = rt->H;
   if (which <= 5) {
-    if (layer < 0 || layer >= rt->Lps) return sp::set_error(SP_ERR_INVALID, "layer %d not on this stage", layer);
+    if (layer < 0 || layer >= rt->v * rt->Lps)  // local index c*Lps + l (stage rank+1+c*p, its layer l)
+      return sp::set_error(SP_ERR_INVALID, "layer %d not on this device", layer);
     const sp::LayerParams& P = rt->lp[layer];
     const int64_t offs[6] = {P.attn_norm, P.wqkv, P.wo, P.mlp_norm, P.wgu, P.wd};
     const int64_t ns[6] = {h, rt->qkv_w * h, h * rt->qd, h, 2 * H * h, h * H};

@@ -24,7 +24,8 @@ class _Cfg(C.Structure):
     _fields_ = [(n, C.c_int32) for n in ("layers", "hidden", "ffn_hidden", "heads", "kv_heads", "head_dim", "vocab",
                                          "microbatches", "slices", "pp", "rank", "exchange_mode")] + [
         ("seq_len", C.c_int64), ("rope_theta", C.c_float), ("norm_eps", C.c_float), ("lr", C.c_float),
-        ("seed", C.c_uint64), ("recompute", C.c_int32), ("vocab_parallel", C.c_int32)]
+        ("seed", C.c_uint64), ("recompute", C.c_int32), ("vocab_parallel", C.c_int32),
+        ("interleave", C.c_int32)]
 
 
 RECOMPUTE = {"selective": 0, "full": 1, "auto": 2}
@@ -45,6 +46,7 @@ class StepConfig:
     exchange: str = "off"
     recompute: str = "auto"  # "selective": stash attention O/LSE, "full": K1 again in the backward, "auto": selective if it fits
     vocab_parallel: bool = False  # LM head + cross entropy split by vocabulary across the pp stages
+    interleave: int = 1  # v stages per device (interleaved SlimPipe; even pp, exchange off)
     rope_theta: float = 10000.0
     norm_eps: float = 1e-5
     lr: float = 1e-4
@@ -83,7 +85,7 @@ class StepConfig:
         return _Cfg(self.layers, self.hidden, self.ffn_hidden, self.heads, self.kv_heads, self.head_dim, self.vocab,
                     self.microbatches, self.slices, self.pp, rank, N.MODES[self.exchange], self.seq_len,
                     self.rope_theta, self.norm_eps, self.lr, self.seed, RECOMPUTE[self.recompute],
-                    int(self.vocab_parallel))
+                    int(self.vocab_parallel), int(self.interleave))
 
     # ---- accounting ----
     def linear_params_per_layer(self) -> int:
@@ -115,6 +117,7 @@ def _lib():
     lib.sp_runtime_attn_stats.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
     lib.sp_runtime_memory.argtypes = [C.c_void_p, C.POINTER(C.c_int64)]
     lib.sp_runtime_recompute.argtypes = [C.c_void_p]
+    lib.sp_runtime_progress.argtypes = [C.c_void_p, C.POINTER(C.c_int32)]
     lib.sp_runtime_param.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int64, C.c_int]
     return lib
 
@@ -161,6 +164,13 @@ class SlimPipeStep:
         self.is_first = self.stage == 1
         self.is_last = self.stage == cfg.pp
 
+    def global_layer(self, local: int) -> int:
+        """Model layer index of this device's local layer `local` (= c*Lps + l:
+        layer l of stage rank+1+c*pp)."""
+        c = self.cfg
+        lps = c.layers // (c.pp * c.interleave)
+        return ((local // lps) * c.pp + self.rank) * lps + local % lps
+
     def close(self):
         if getattr(self, "_h", None):
             _lib().sp_runtime_destroy(self._h)
@@ -199,11 +209,20 @@ class SlimPipeStep:
         N.check(_lib().sp_runtime_step(self._h, C.c_void_p(tokens_dev), C.c_void_p(targets_dev), 1,
                                        0 if optimizer else 1, None), "sp_runtime_step")
 
+    def progress(self):
+        """(position, (kind, microbatch, slice, stage)) of the first unfinished
+        pass of the last enqueued step on the compute stream, or None."""
+        b = (C.c_int32 * 4)()
+        x = _lib().sp_runtime_progress(self._h, b)
+        return None if x < 0 else (x, tuple(b))
+
     def sync(self):
         N.check(_lib().sp_runtime_sync(self._h), "sp_runtime_sync")
 
     def timeline(self):
-        n_pass = 2 * self.cfg.microbatches * self.cfg.slices
+        c = self.cfg
+        vp = c.vocab_parallel and c.pp > 1  # + one VocabForward and one VocabBackward per slice
+        n_pass = (4 if vp else 2) * c.interleave * c.microbatches * c.slices
         buf = (C.c_double * (1 + 3 * n_pass))()
         n = _lib().sp_runtime_timeline(self._h, buf, len(buf))
         if n < 0:

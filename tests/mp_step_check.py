@@ -30,9 +30,12 @@ def main():
     m = int(os.environ.get("SP_M", 2))
     n = int(os.environ.get("SP_N", 4))
     xmode = os.environ.get("SP_X", "off")
+    vp = os.environ.get("SP_VP") == "1"
     cfg = StepConfig.c1(pp=world, microbatches=m, slices=n, layers=2 * world, exchange=xmode,
+                        vocab=1024 if vp else 1000,  # vocab shards must be a multiple of 4 wide
                         seq_len=1024 * n, recompute=os.environ.get("SP_RC", "selective"),
-                        kv_heads=int(os.environ.get("SP_KV", 4)), vocab_parallel=os.environ.get("SP_VP") == "1")
+                        kv_heads=int(os.environ.get("SP_KV", 4)), vocab_parallel=vp,
+                        interleave=int(os.environ.get("SP_V", 1)))
     step = SlimPipeStep(cfg, rank, world)
     rng = np.random.default_rng(0)
     tok = rng.integers(0, cfg.vocab, (cfg.microbatches, cfg.seq_len), dtype=np.int32)
@@ -41,10 +44,10 @@ def main():
     loss = step.step(tok, tgt, optimizer=False)
     lps = cfg.layers // world
     mine = {"loss": loss, "params": {}, "grads": {}}
-    for l in range(lps):
+    for l in range(lps):  # lps local layers: v chunks of layers/(pp v)
         for k in NAMES:
-            mine["params"][(rank * lps + l, k)] = step.get_param(l, k)
-            mine["grads"][(rank * lps + l, k)] = step.get_grad(l, k)
+            mine["params"][(step.global_layer(l), k)] = step.get_param(l, k)
+            mine["grads"][(step.global_layer(l), k)] = step.get_grad(l, k)
     if step.is_first:
         mine["params"][(None, "embedding")] = step.get_param(0, "embedding")
         mine["grads"][(None, "embedding")] = step.get_grad(0, "embedding")
@@ -77,7 +80,7 @@ def main():
             W[k] = rnd(P[(None, k)])
         ref_loss, ref_g = MO.Model(W, cfg.heads, cfg.kv_heads, cfg.rope_theta, cfg.norm_eps).step(tok, tgt, n)
         gpu_loss = allv[-1]["loss"]
-        print(f"pp={world} m={m} n={n} exchange={xmode} vocab_parallel={cfg.vocab_parallel} "
+        print(f"pp={world} v={cfg.interleave} m={m} n={n} exchange={xmode} vocab_parallel={cfg.vocab_parallel} "
               f"loss gpu {gpu_loss:.6f} oracle {ref_loss:.6f}")
         xs = [d["x"] for d in allv]
         print("exchange stats per rank:", xs)
@@ -94,7 +97,7 @@ def main():
                 ok = False
         for r_, d in enumerate(allv):
             mm = d["mem"]
-            expect = n + 2 * (world - 1 - r_) if m * n >= n + 2 * (world - 1) else None
+            expect = n + 2 * (world - 1 - r_) if m * n >= n + 2 * (world - 1) and cfg.interleave == 1 else None
             print(f"rank {r_}: slots {mm['slots']} high-water {mm['slots_high_water']} ledger {mm['ledger_peak_units']}"
                   f" (n+2(p-d) = {expect})")
             ok &= mm["slots_high_water"] == mm["ledger_peak_units"]
