@@ -74,6 +74,11 @@ int sp_plan_exchange_volume(int64_t p, int64_t n, int64_t layers, int64_t mh_num
  * comm={bandwidth,latency}; mem_rats = 6 (num,den) pairs or NULL (unit model) */
 int sp_plan_simulate_json(int p, int v, int m, int n, int mode, const double* cost, const double* comm,
                           int64_t seq_len, const int64_t* mem_rats, char** out);
+/* reference simulator.cpp:414-522 (place_vocab) on gen_slimpipe(p, v, m, n),
+ * base-simulation costs alpha (per token) and beta (per query-key pair):
+ * {"valid", "violations", "order": per device [[kind, microbatch, slice, stage], ...]} */
+int sp_plan_vocab_json(int p, int v, int m, int n, int distribute, double alpha, double beta, int64_t seq_len,
+                       char** out);
 
 /* ------------------------------------------------- sliced causal attention
  * Replaces reference attention.cpp:94-111 (chunk_attention) for the

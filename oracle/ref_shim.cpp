@@ -239,6 +239,35 @@ char* ref_exchange_volume(int64_t p, int64_t n, int64_t L, int64_t mh_num, int64
 // cost = {alpha, beta, bwd_in, bwd_w}; comm = {bandwidth, latency}; memory is
 // the unit model (slice_stage = exchange_slice = 1, M_h = n) unless
 // mem_rats (6 num/den pairs: ptl, mh, ma, slice_stage, logits, exchange) given.
+char* ref_vocab_json(int p, int v, int m, int n, int distribute, double alpha, double beta, int64_t seq_len) {
+  try {
+    Schedule s = gen_slimpipe(make_cfg(p, v, m, n));
+    SimInputs in;
+    in.cost.alpha_linear = alpha;
+    in.cost.beta_attn = beta;
+    in.seq_len = seq_len;
+    const Schedule out = place_vocab(s, distribute != 0, in);
+    const Diagnostics d = validate_schedule(out);
+    std::ostringstream os;
+    os << "{\"valid\":" << (d.ok() ? "true" : "false") << ",\"violations\":" << d.violations.size()
+       << ",\"order\":[";
+    for (std::size_t dev = 0; dev < out.device_order.size(); ++dev) {
+      os << (dev ? "," : "") << "[";
+      for (std::size_t x = 0; x < out.device_order[dev].size(); ++x) {
+        const Pass& q = out.passes[out.device_order[dev][x]];
+        os << (x ? "," : "") << "[" << int(q.kind) << "," << q.microbatch << "," << q.slice << "," << q.stage << "]";
+      }
+      os << "]";
+    }
+    os << "]}";
+    return dup(os.str());
+  } catch (const std::invalid_argument& e) {
+    return error_json("invalid_argument", e);
+  } catch (const std::exception& e) {
+    return error_json("runtime_error", e);
+  }
+}
+
 char* ref_simulate_json(int p, int v, int m, int n, int mode, const double* cost,
                         const double* comm, int64_t seq_len, const int64_t* mem_rats) {
   try {

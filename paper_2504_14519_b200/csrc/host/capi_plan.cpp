@@ -297,4 +297,33 @@ int sp_plan_simulate_json(int p, int v, int m, int n, int mode, const double* co
   });
 }
 
+// place_vocab (simulator.cpp:414-522) on gen_slimpipe(p, v, m, n) with the
+// given base-simulation costs; the result's validity and per-device order
+// ([kind, microbatch, slice, stage] per pass).
+int sp_plan_vocab_json(int p, int v, int m, int n, int distribute, double alpha, double beta, int64_t seq_len,
+                       char** out) {
+  return guarded(out, [&] {
+    Schedule s = gen_slimpipe(gen_cfg(p, v, m, n));
+    SimInputs in;
+    in.cost.alpha_linear = alpha;
+    in.cost.beta_attn = beta;
+    in.seq_len = seq_len;
+    const Schedule out = place_vocab(s, distribute != 0, in);
+    const Diagnostics d = validate_schedule(out);
+    std::ostringstream os;
+    os << "{\"valid\":" << (d.ok() ? "true" : "false") << ",\"violations\":" << d.violations.size()
+       << ",\"order\":[";
+    for (std::size_t dev = 0; dev < out.device_order.size(); ++dev) {
+      os << (dev ? "," : "") << "[";
+      for (std::size_t x = 0; x < out.device_order[dev].size(); ++x) {
+        const Pass& q = out.passes[out.device_order[dev][x]];
+        os << (x ? "," : "") << "[" << int(q.kind) << "," << q.microbatch << "," << q.slice << "," << q.stage << "]";
+      }
+      os << "]";
+    }
+    os << "]}";
+    return os.str();
+  });
+}
+
 }  // extern "C"

@@ -43,6 +43,7 @@ _SIGS = {
     "sp_plan_exchange_volume": (C.c_int, [C.c_int64] * 5 + [_charpp]),
     "sp_plan_analytics_json": (C.c_int, [C.c_int] + [C.c_int64] * 6 + [_charpp]),
     "sp_plan_simulate_json": (C.c_int, [C.c_int] * 5 + [_f64p, _f64p, C.c_int64, _i64p, _charpp]),
+    "sp_plan_vocab_json": (C.c_int, [C.c_int] * 5 + [C.c_double, C.c_double, C.c_int64, _charpp]),
     "sp_attn_fwd": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
                               _i32p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p,
                               C.c_int64, C.c_void_p, C.c_void_p]),

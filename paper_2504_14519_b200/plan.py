@@ -111,3 +111,15 @@ def simulate_text(p: int, v: int, m: int, n: int, mode: str = "off", cost=(1.0, 
 def simulate(*args, **kw) -> dict:
     """reference simulator.cpp:110-412 on gen_slimpipe(p,v,m,n)."""
     return json.loads(simulate_text(*args, **kw))
+
+
+def place_vocab_text(p: int, v: int, m: int, n: int, distribute: bool = True, alpha: float = 1.0,
+                     beta: float = 1.0, seq_len: int | None = None) -> str:
+    seq_len = n if seq_len is None else seq_len
+    return N._json_call("sp_plan_vocab_json", p, v, m, n, int(distribute), float(alpha), float(beta), seq_len)
+
+
+def place_vocab(*args, **kw) -> dict:
+    """reference simulator.cpp:414-522 on gen_slimpipe(p,v,m,n): validity of the
+    result and the per-device pass order ([kind, microbatch, slice, stage])."""
+    return json.loads(place_vocab_text(*args, **kw))

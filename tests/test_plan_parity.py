@@ -238,3 +238,53 @@ def test_ledger_peaks_n_plus_2_p_minus_d():  # tests/test_simulator.cpp:113-172
 def test_activation_70b_1m_full_is_160gib():  # verify.cpp:85-96
     mm = P.activation_bytes(P.ModelShape(80, 8192, 28672, 64, 8, 128000), 8, 1, 1, 1, 1 << 20, 1, 1, "full")
     assert mm["ma"] == 160 * 2**30
+
+
+# ---- vocabulary placement --------------------------------
+
+@needs_ref
+def test_place_vocab_matches_live_reference():
+    """place_vocab (simulator.cpp:414-522), tail and distributed, raw and
+    normalised base costs: byte-identical order and validity."""
+    n_checked = 0
+    for p in (1, 2, 4):
+        for m in (1, 2, 4):
+            for n in (4, 8):
+                for dist in (0, 1):
+                    for S, a, b in ((4096, 1.0, 1.0), (1024 * n, 1.0 / (1024 * n), 1.0 / (1024 * n) ** 2)):
+                        mine = P.place_vocab_text(p, 1, m, n, bool(dist), a, b, S)
+                        ref = O.ref_text("ref_vocab_json", p, 1, m, n, dist, a, b, S)
+                        assert mine == ref, (p, m, n, dist, S)
+                        n_checked += 1
+    assert n_checked == 72
+
+
+def test_place_vocab_normalised_costs_always_valid():
+    """The executor's choice (runtime.cpp init): alpha = 1/S, beta = 1/S^2 keeps
+    pass times O(1), so place_vocab's 1e-9 slack is meaningful and every
+    distributed placement validates; each VF(k,i) follows F(k,i,p) on the last
+    device and all devices run the vocab passes in one order (their
+    collectives pair up)."""
+    for p in (2, 4, 8):
+        for m in (1, 2, 4):
+            for n in (p, 2 * p, 4 * p):
+                S = 1024 * n
+                r = P.place_vocab(p, 1, m, n, True, 1.0 / S, 1.0 / S ** 2, S)
+                assert r["valid"], (p, m, n)
+                vocab = [[tuple(x) for x in dev if x[0] in (4, 5)] for dev in r["order"]]
+                assert all(v == vocab[0] for v in vocab), (p, m, n)
+                last = [tuple(x) for x in r["order"][-1]]
+                for k in range(1, m + 1):
+                    for i in range(1, n + 1):
+                        assert last.index((0, k, i, p)) < last.index((4, k, i, p))
+
+
+def test_place_vocab_raw_costs_reference_quirk():
+    """Reference behaviour pinned: with raw per-pair costs the base times reach
+    ~1e7, the anchor slack (anchor <= end - 1e-9, simulator.cpp:514) is below
+    one ulp, and VF(1,2) lands before its own F(1,2,2): the schedule fails
+    validation (the same bytes as the compiled reference, test above)."""
+    r = P.place_vocab(2, 1, 2, 2, True, 1.0, 1.0, 4096)
+    assert not r["valid"]
+    last = [tuple(x) for x in r["order"][1]]
+    assert last.index((4, 1, 2, 2)) < last.index((0, 1, 2, 2))
