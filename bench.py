@@ -70,6 +70,10 @@ def parse():
                     help="shard the LM head and cross entropy over all stages (PP>1; SURVEY §8f rank 1)")
     ap.add_argument("--interleave", type=int, default=1,
                     help="v stages per GPU (interleaved SlimPipe, even PP; SURVEY §8f rank 2)")
+    ap.add_argument("--scenario", default=None,
+                    help="reference scenario JSON (scenario.cpp schema) for the model/run shape; overrides --model etc.")
+    ap.add_argument("--gantt", default=None,
+                    help="write the measured last-step timeline in the reference's Gantt JSON format (rank 0)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -83,6 +87,11 @@ DEPTH = {"c2": 8, "c3": 8, "c4": 2}  # reduced depth (BASELINE.json: "reduced de
 
 def make_cfg(args, world):
     from paper_2504_14519_b200.runtime import StepConfig
+    if args.scenario:  # a reference scenario file (scenario.cpp schema) names the whole step
+        cfg = StepConfig.from_scenario(open(args.scenario).read())
+        if cfg.pp != world:
+            raise SystemExit(f"scenario pp={cfg.pp} but {world} rank(s) launched")
+        return cfg
     base = getattr(StepConfig, args.model)()
     kw = {k: v for k, v in (("layers", args.layers or DEPTH[args.model]), ("seq_len", args.seq_len),
                             ("slices", args.slices), ("microbatches", args.microbatches)) if v is not None}
@@ -298,6 +307,16 @@ def main():
 
     # last timed step: per-pass busy (bubble) and attention kernel timings
     step_ms, passes = step.timeline()
+    if args.gantt:  # measured timeline in the reference's Gantt schema (gantt.cpp:52-106)
+        from paper_2504_14519_b200 import plan as P
+        per_dev = [passes]
+        if world > 1:
+            per_dev = [None] * world
+            dist.all_gather_object(per_dev, passes)
+        if rank == 0:
+            with open(args.gantt, "w") as f:
+                f.write(P.gantt_measured_text(world, cfg.interleave, cfg.microbatches, cfg.slices, per_dev,
+                                              cfg.vocab_parallel, cfg.seq_len))
     busy = sum(e - s for _, s, e in passes)
     makespan = max_over_ranks(step_ms)
     busy_all = sum_over_ranks(busy)
@@ -361,7 +380,10 @@ def main():
             "metric": "tokens/s", "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic tokens, random-init weights",
-            "config": {"workload": workload_name(cfg, args.model), "model": MODEL_NAMES[args.model][1], "layers": cfg.layers,
+            "config": {"workload": (f"scenario {os.path.basename(args.scenario)}: L={cfg.layers} h={cfg.hidden} "
+                                    f"S={cfg.seq_len} n={cfg.slices} m={cfg.microbatches} PP={cfg.pp}"
+                                    if args.scenario else workload_name(cfg, args.model)),
+                       "model": "scenario" if args.scenario else MODEL_NAMES[args.model][1], "layers": cfg.layers,
                        "global_batch": cfg.microbatches, "seq_len": cfg.seq_len, "slices": cfg.slices,
                        "parallelism": f"pp{world}", "exchange": cfg.exchange, "vocab_parallel": cfg.vocab_parallel, "interleave": cfg.interleave,
                        "recompute": cfg.recompute if cfg.recompute != "auto" else f"auto->{mem['recompute']}",

@@ -79,6 +79,18 @@ int sp_plan_simulate_json(int p, int v, int m, int n, int mode, const double* co
  * {"valid", "violations", "order": per device [[kind, microbatch, slice, stage], ...]} */
 int sp_plan_vocab_json(int p, int v, int m, int n, int distribute, double alpha, double beta, int64_t seq_len,
                        char** out);
+/* reference scenario.cpp:72-193: scenario text -> normalised scenario JSON
+ * (strict: unknown fields / bad values are SP_ERR_INVALID) */
+int sp_plan_scenario_json(const char* text, char** out);
+/* reference gantt.cpp:52-106 on simulate(gen_slimpipe(p,v,m,n)) (inputs as
+ * sp_plan_simulate_json, unit memory model); svg != 0: the SVG form */
+int sp_plan_gantt_json(int p, int v, int m, int n, int mode, const double* cost, const double* comm,
+                       int64_t seq_len, int svg, char** out);
+/* the same export for a measured step: per-device CUDA-event spans (counts[d]
+ * entries of pass id / start / end, devices concatenated) against the
+ * executor's schedule */
+int sp_plan_gantt_measured(int p, int v, int m, int n, int vocab_parallel, int64_t seq_len, const int32_t* counts,
+                           const int32_t* pass_ids, const double* starts, const double* ends, int svg, char** out);
 
 /* ------------------------------------------------- sliced causal attention
  * Replaces reference attention.cpp:94-111 (chunk_attention) for the

@@ -22,6 +22,8 @@
 #include "pipelab/attention.hpp"
 #include "pipelab/analytics.hpp"
 #include "pipelab/exchange.hpp"
+#include "pipelab/gantt.hpp"
+#include "pipelab/scenario.hpp"
 #include "pipelab/schedule.hpp"
 #include "pipelab/simulator.hpp"
 #include "pipelab/workload.hpp"
@@ -263,6 +265,60 @@ char* ref_vocab_json(int p, int v, int m, int n, int distribute, double alpha, d
     return dup(os.str());
   } catch (const std::invalid_argument& e) {
     return error_json("invalid_argument", e);
+  } catch (const std::exception& e) {
+    return error_json("runtime_error", e);
+  }
+}
+
+char* ref_scenario_json(const char* text) {
+  try {
+    return dup(scenario_to_json(scenario_from_json(text)));
+  } catch (const std::invalid_argument& e) {
+    return error_json("invalid_argument", e);
+  } catch (const std::exception& e) {
+    return error_json("runtime_error", e);
+  }
+}
+
+char* ref_gantt_json(int p, int v, int m, int n, int mode, const double* cost, const double* comm, int64_t seq_len,
+                     int svg) {
+  try {
+    Schedule s = gen_slimpipe(make_cfg(p, v, m, n));
+    SimInputs in;
+    in.cost.alpha_linear = cost[0];
+    in.cost.beta_attn = cost[1];
+    in.cost.bwd_input_mult = cost[2];
+    in.cost.bwd_weight_mult = cost[3];
+    in.comm.bandwidth = comm[0];
+    in.comm.latency = comm[1];
+    in.seq_len = seq_len;
+    in.exchange = static_cast<ExchangeMode>(mode);
+    in.memory = unit_memory_model(p, v, n);
+    SimResult r = simulate(s, in);
+    return dup(svg ? gantt_svg(s, r.timeline) : gantt_json(s, r.timeline));
+  } catch (const std::exception& e) {
+    return error_json("runtime_error", e);
+  }
+}
+
+// a measured timeline given as arrays, through the reference's own exporter
+char* ref_gantt_measured(int p, int v, int m, int n, const int32_t* counts, const int32_t* pass_ids,
+                         const double* starts, const double* ends, int svg) {
+  try {
+    Schedule s = gen_slimpipe(make_cfg(p, v, m, n));
+    Timeline tl;
+    tl.per_device.resize(p);
+    int64_t x = 0;
+    for (int d = 0; d < p; ++d)
+      for (int e = 0; e < counts[d]; ++e, ++x) {
+        TimelineEntry te;
+        te.pass = pass_ids[x];
+        te.start = starts[x];
+        te.end = ends[x];
+        tl.per_device[d].push_back(te);
+        if (ends[x] > tl.makespan) tl.makespan = ends[x];
+      }
+    return dup(svg ? gantt_svg(s, tl) : gantt_json(s, tl));
   } catch (const std::exception& e) {
     return error_json("runtime_error", e);
   }

@@ -24,6 +24,10 @@ CUDA = Path(os.environ.get("CUDA_HOME", "/usr/local/cuda"))
 NVCC = str(CUDA / "bin" / "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 INCLUDES = [f"-I{ROOT / 'include'}", f"-I{CSRC / 'host'}", f"-I{CSRC / 'cuda'}", f"-I{CUDA / 'include'}"]
+# nlohmann/json (header-only; the scenario / Gantt text in csrc/host): the copy
+# the image ships with cudnn_frontend, the same header the reference includes.
+_NLOHMANN = [Path(p) / "include" / "cudnn_frontend" / "thirdparty" for p in sys.path if p.endswith("site-packages")]
+HOST_INCLUDES = [f"-isystem{p}" for p in _NLOHMANN if (p / "nlohmann" / "json.hpp").exists()][:1]
 
 
 def _headers() -> list[Path]:
@@ -44,7 +48,7 @@ def _compile_cmd(src: Path, obj: Path) -> list[str]:
         return [NVCC, *ARCH, "-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
                 "-Xptxas", "-warn-spills", *INCLUDES, "-c", str(src), "-o", str(obj)]
     return ["g++", "-std=c++20", "-O2", "-fPIC", "-Wall", "-Wextra", "-Wno-unused-parameter", *INCLUDES,
-            "-c", str(src), "-o", str(obj)]
+            *HOST_INCLUDES, "-c", str(src), "-o", str(obj)]
 
 
 def build(verbose: bool = False, jobs: int | None = None) -> Path:

@@ -3,6 +3,7 @@
 // host mirror and the parity tests as JSON text in the neutral format that
 // oracle/ref_shim.cpp emits for the reference, so plans can be compared
 // byte-for-byte.  Status codes, no exceptions across the ABI.
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -11,6 +12,8 @@
 
 #include "pipelab/analytics.hpp"
 #include "pipelab/exchange.hpp"
+#include "pipelab/gantt.hpp"
+#include "pipelab/scenario.hpp"
 #include "pipelab/schedule.hpp"
 #include "pipelab/simulator.hpp"
 #include "pipelab/workload.hpp"
@@ -27,6 +30,15 @@ char* to_c(const std::string& s) {
   return p;
 }
 
+std::string escaped(const char* what) {  // for the {"error", "what"} JSON
+  std::string s;
+  for (const char* c = what; *c; ++c) {
+    if (*c == '"' || *c == '\\') s += '\\';
+    s += *c;
+  }
+  return s;
+}
+
 template <class F>
 int guarded(char** out, F&& body) {
   try {
@@ -34,11 +46,11 @@ int guarded(char** out, F&& body) {
     return SP_OK;
   } catch (const std::invalid_argument& e) {
     sp::last_error() = e.what();
-    *out = to_c(std::string("{\"error\":\"invalid_argument\",\"what\":\"") + e.what() + "\"}");
+    *out = to_c(std::string("{\"error\":\"invalid_argument\",\"what\":\"") + escaped(e.what()) + "\"}");
     return SP_ERR_INVALID;
   } catch (const std::exception& e) {
     sp::last_error() = e.what();
-    *out = to_c(std::string("{\"error\":\"runtime_error\",\"what\":\"") + e.what() + "\"}");
+    *out = to_c(std::string("{\"error\":\"runtime_error\",\"what\":\"") + escaped(e.what()) + "\"}");
     return SP_ERR_RUNTIME;
   }
 }
@@ -323,6 +335,63 @@ int sp_plan_vocab_json(int p, int v, int m, int n, int distribute, double alpha,
     }
     os << "]}";
     return os.str();
+  });
+}
+
+// Scenario text -> the normalised scenario JSON (reference scenario.cpp
+// scenario_from_json then scenario_to_json); malformed JSON, wrong types and
+// unknown fields are SP_ERR_INVALID.
+int sp_plan_scenario_json(const char* text, char** out) {
+  return guarded(out, [&] { return scenario_to_json(scenario_from_json(text)); });
+}
+
+// Gantt (JSON, or SVG when svg != 0) of simulate(gen_slimpipe(p, v, m, n))
+// with the inputs of sp_plan_simulate_json and the unit memory model.
+int sp_plan_gantt_json(int p, int v, int m, int n, int mode, const double* cost, const double* comm,
+                       int64_t seq_len, int svg, char** out) {
+  return guarded(out, [&] {
+    const Schedule s = gen_slimpipe(gen_cfg(p, v, m, n));
+    SimInputs in;
+    in.cost.alpha_linear = cost[0];
+    in.cost.beta_attn = cost[1];
+    in.cost.bwd_input_mult = cost[2];
+    in.cost.bwd_weight_mult = cost[3];
+    in.comm.bandwidth = comm[0];
+    in.comm.latency = comm[1];
+    in.seq_len = seq_len;
+    in.exchange = ExchangeMode(mode);
+    in.memory = unit_memory_model(p, v, n);
+    const SimResult r = simulate(s, in);
+    return svg ? gantt_svg(s, r.timeline) : gantt_json(s, r.timeline);
+  });
+}
+
+// Gantt of a MEASURED step: the executors' schedule (gen_slimpipe(p, v, m, n),
+// plus place_vocab with the runtime's normalised costs when vocab_parallel)
+// and each device's CUDA-event spans (counts[d] passes: pass id, start, end
+// in ms, devices concatenated in order).
+int sp_plan_gantt_measured(int p, int v, int m, int n, int vocab_parallel, int64_t seq_len, const int32_t* counts,
+                           const int32_t* pass_ids, const double* starts, const double* ends, int svg, char** out) {
+  return guarded(out, [&] {
+    Schedule s = gen_slimpipe(gen_cfg(p, v, m, n));
+    if (vocab_parallel) {
+      SimInputs in;
+      in.cost.alpha_linear = 1.0 / double(seq_len);
+      in.cost.beta_attn = 1.0 / (double(seq_len) * double(seq_len));
+      in.seq_len = seq_len;
+      s = place_vocab(s, true, in);
+    }
+    Timeline tl;
+    tl.per_device.resize(static_cast<size_t>(p));
+    int64_t x = 0;
+    for (int d = 0; d < p; ++d)
+      for (int e = 0; e < counts[d]; ++e, ++x) {
+        if (pass_ids[x] < 0 || size_t(pass_ids[x]) >= s.passes.size())
+          throw std::invalid_argument("gantt: pass id out of range");
+        tl.per_device[size_t(d)].push_back({PassId(pass_ids[x]), starts[x], ends[x]});
+        tl.makespan = std::max(tl.makespan, ends[x]);
+      }
+    return svg ? gantt_svg(s, tl) : gantt_json(s, tl);
   });
 }
 

@@ -123,3 +123,35 @@ def place_vocab(*args, **kw) -> dict:
     """reference simulator.cpp:414-522 on gen_slimpipe(p,v,m,n): validity of the
     result and the per-device pass order ([kind, microbatch, slice, stage])."""
     return json.loads(place_vocab_text(*args, **kw))
+
+
+# ---- scenario files and Gantt export (SURVEY §8f rank 3) ----------------------
+
+def scenario_text(text: str) -> str:
+    """reference scenario.cpp:72-193: strict parse + normalised re-serialisation
+    (ValueError on unknown fields, bad values or malformed JSON)."""
+    return N._json_call("sp_plan_scenario_json", text.encode())
+
+
+def scenario(text: str) -> dict:
+    return json.loads(scenario_text(text))
+
+
+def gantt_text(p: int, v: int, m: int, n: int, mode: str = "off", cost=(1.0, 0.0, 2.0, 1.0), comm=(0.0, 0.0),
+               seq_len: int | None = None, svg: bool = False) -> str:
+    """reference gantt.cpp:52-106 on the simulated timeline of gen_slimpipe(p,v,m,n)."""
+    seq_len = n if seq_len is None else seq_len
+    return N._json_call("sp_plan_gantt_json", p, v, m, n, N.MODES[mode], N.arr(C.c_double, cost),
+                        N.arr(C.c_double, comm), seq_len, int(svg))
+
+
+def gantt_measured_text(p: int, v: int, m: int, n: int, per_device, vocab_parallel: bool = False,
+                        seq_len: int = 1, svg: bool = False) -> str:
+    """The same export for a measured step: per_device[d] = [(pass id, start ms,
+    end ms), ...] as returned by SlimPipeStep.timeline() on rank d."""
+    counts = [len(rows) for rows in per_device]
+    flat = [e for rows in per_device for e in rows]
+    return N._json_call("sp_plan_gantt_measured", p, v, m, n, int(vocab_parallel), seq_len,
+                        N.arr(C.c_int32, counts), N.arr(C.c_int32, [int(e[0]) for e in flat]),
+                        N.arr(C.c_double, [float(e[1]) for e in flat]), N.arr(C.c_double, [float(e[2]) for e in flat]),
+                        int(svg))

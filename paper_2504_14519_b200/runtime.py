@@ -81,6 +81,32 @@ class StepConfig:
         """Llama-70B layer shapes (GQA 64/8), 1M context, 32 slices, m1 (depth reduced)."""
         return replace(StepConfig(16, 8192, 28672, 64, 8, 128000, 1 << 20, 32, 1), **kw)
 
+    @staticmethod
+    def from_scenario(text: str, **overrides) -> "StepConfig":
+        """A reference scenario file (scenario.cpp schema) as the executed step:
+        the same file drives plan.simulate / plan.gantt_text and the GPU run.
+        Only what the executor runs is accepted: scheme slimpipe, tp = cp = dp
+        = ep = 1, checkpointing selective or full, no offload."""
+        from . import plan as P
+        sc = P.scenario(text)  # strict: unknown fields and bad values raise ValueError
+        md, pa, rn = sc["model"], sc["parallelism"], sc["run"]
+        if sc["scheme"] != "slimpipe":
+            raise ValueError(f"scenario: the executor runs scheme slimpipe, not {sc['scheme']}")
+        for k in ("tp", "cp", "dp", "ep"):
+            if pa[k] != 1:
+                raise ValueError(f"scenario: {k} = {pa[k]} is not on the executed path (pipeline only)")
+        if rn["checkpointing"] not in ("selective", "full"):
+            raise ValueError(f"scenario: checkpointing {rn['checkpointing']} (the executor recomputes: selective|full)")
+        if rn["offload_ratio"] != 0:
+            raise ValueError("scenario: activation offload is not executed")
+        kw = dict(layers=md["layers"], hidden=md["hidden"], ffn_hidden=md["ffn"], heads=md["heads"],
+                  kv_heads=md["query_groups"], vocab=md["vocab"], seq_len=rn["seq_len"], slices=rn["slices"],
+                  microbatches=rn["microbatches"], pp=pa["pp"], interleave=pa["stages_per_device"],
+                  exchange=sc["exchange"], recompute=rn["checkpointing"], vocab_parallel=bool(rn["vocab_parallel"]),
+                  seed=sc["seed"])
+        kw.update(overrides)
+        return StepConfig(**kw)
+
     def to_c(self, rank: int) -> _Cfg:
         return _Cfg(self.layers, self.hidden, self.ffn_hidden, self.heads, self.kv_heads, self.head_dim, self.vocab,
                     self.microbatches, self.slices, self.pp, rank, N.MODES[self.exchange], self.seq_len,

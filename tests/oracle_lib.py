@@ -44,7 +44,8 @@ def ref():
             raise FileNotFoundError("oracle/_ref/libpipelab_ref.so not built and /root/reference absent")
         _ref = C.CDLL(str(REF_SO))
         for fn in ["ref_schedule_json", "ref_validate_json", "ref_balance_json", "ref_exchange_json",
-                   "ref_activation_json", "ref_exchange_volume", "ref_simulate_json", "ref_analytics_json", "ref_vocab_json"]:
+                   "ref_activation_json", "ref_exchange_volume", "ref_simulate_json", "ref_analytics_json", "ref_vocab_json", "ref_scenario_json",
+                   "ref_gantt_json", "ref_gantt_measured"]:
             getattr(_ref, fn).restype = C.c_void_p
         _ref.ref_free.argtypes = [C.c_void_p]
         _ref.ref_schedule_json.argtypes = [C.c_int] * 5
@@ -56,6 +57,9 @@ def ref():
         _ref.ref_analytics_json.argtypes = [C.c_int] + [C.c_int64] * 6
         _ref.ref_simulate_json.argtypes = [C.c_int] * 5 + [_dp, _dp, C.c_int64, C.POINTER(C.c_int64)]
         _ref.ref_vocab_json.argtypes = [C.c_int] * 5 + [C.c_double, C.c_double, C.c_int64]
+        _ref.ref_scenario_json.argtypes = [C.c_char_p]
+        _ref.ref_gantt_json.argtypes = [C.c_int] * 5 + [_dp, _dp, C.c_int64, C.c_int]
+        _ref.ref_gantt_measured.argtypes = [C.c_int] * 4 + [C.POINTER(C.c_int32)] * 2 + [_dp, _dp, C.c_int]
         _ref.ref_chunk_attention.argtypes = [_dp, C.c_int, C.c_int, _dp, _dp, _ip, C.c_int, C.c_int, _dp, _dp,
                                              _dp, _dp]
         _ref.ref_merge.argtypes = [C.c_int, C.c_int] + [_dp] * 10
