@@ -288,3 +288,44 @@ def test_place_vocab_raw_costs_reference_quirk():
     assert not r["valid"]
     last = [tuple(x) for x in r["order"][1]]
     assert last.index((4, 1, 2, 2)) < last.index((0, 1, 2, 2))
+
+
+# ---- interleaved execution pre-flight ---------------------
+
+def _link_orders(sched):
+    """Per device d: the order in which d sends stage outputs / input grads on
+    its ring links, and the order in which its neighbours consume them
+    (runtime.cpp check_ring_order restated)."""
+    p, v = sched["p"], sched["v"]
+    P_ = p * v
+    ps = sched["passes"]
+    out = []
+    for d in range(p):
+        mine = [ps[i] for i in sched["device_order"][d]]
+        nxt = [ps[i] for i in sched["device_order"][(d + 1) % p]]
+        prv = [ps[i] for i in sched["device_order"][(d - 1) % p]]
+        snd = [(q["microbatch"], q["slice"], q["stage"]) for q in mine if q["kind"] == "F" and q["stage"] < P_]
+        rcv = [(q["microbatch"], q["slice"], q["stage"] - 1) for q in nxt if q["kind"] == "F" and q["stage"] > 1]
+        gsnd = [(q["microbatch"], q["slice"], q["stage"] - 1) for q in mine if q["kind"] == "BW" and q["stage"] > 1]
+        grcv = [(q["microbatch"], q["slice"], q["stage"]) for q in prv if q["kind"] == "BW" and q["stage"] < P_]
+        out.append((snd, rcv, gsnd, grcv))
+    return out
+
+
+@pytest.mark.parametrize("p,v,m,n", [(2, 2, 1, 4), (2, 2, 2, 4), (2, 2, 3, 8), (4, 2, 2, 8), (4, 2, 4, 8),
+                                     (4, 4, 2, 8), (8, 2, 4, 16), (2, 1, 2, 4), (4, 1, 4, 8)])
+def test_interleaved_ring_links_are_fifo_consistent(p, v, m, n):
+    """Every stage link is one in-order NCCL pair: what a device sends must be
+    what its neighbour consumes next; and each local chunk's backward runs a
+    microbatch's slices n..1 back to back (one dK/dV accumulator per chunk)."""
+    sched = P.gen_slimpipe(p, v, m, n)
+    links = _link_orders(sched)
+    for snd, rcv, gsnd, grcv in links:
+        assert snd == rcv and gsnd == grcv
+    assert sum(len(x[0]) for x in links) == sum(len(x[2]) for x in links) == m * n * (p * v - 1)
+    ps = sched["passes"]
+    for d in range(p):
+        for c in range(v):
+            seq = [(ps[i]["microbatch"], ps[i]["slice"]) for i in sched["device_order"][d]
+                   if ps[i]["kind"] == "BW" and (ps[i]["stage"] - 1) // p == c]
+            assert seq == [(k, i) for k in range(1, m + 1) for i in range(n, 0, -1)]
