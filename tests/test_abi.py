@@ -55,3 +55,21 @@ def test_runtime_rejects_invalid_configs_before_touching_the_device(kw, msg):
     c = StepConfig.c1().to_c(0)
     c.recompute = 7
     assert lib.sp_runtime_create(ctypes.byref(c), None, ctypes.byref(h)) == native.SP_ERR_INVALID
+
+
+@pytest.mark.parametrize("kw,code,msg", [
+    ({"pp": 3, "layers": 6, "slices": 3, "seq_len": 3072, "interleave": 2}, "SP_ERR_UNSUPPORTED", b"even pp"),
+    ({"pp": 2, "layers": 4, "interleave": 2, "vocab_parallel": True}, "SP_ERR_UNSUPPORTED", b"vocab_parallel 0"),
+    ({"pp": 2, "layers": 4, "interleave": 2, "exchange": "on"}, "SP_ERR_UNSUPPORTED", b"exchange off"),
+    ({"pp": 2, "layers": 6, "interleave": 2}, "SP_ERR_INVALID", b"pp*v"),
+    ({"pp": 2, "layers": 2, "vocab": 1002, "vocab_parallel": True}, "SP_ERR_INVALID", b"multiple of 4"),
+])
+def test_experimental_paths_reject_unsupported_configs_host_side(kw, code, msg):
+    """Interleaving / vocabulary parallelism preconditions (runtime.cpp init),
+    checked before any CUDA or NCCL call."""
+    from paper_2504_14519_b200.runtime import StepConfig, _lib
+    lib = _lib()
+    c = StepConfig.c1(**kw).to_c(0)
+    h = ctypes.c_void_p()
+    assert lib.sp_runtime_create(ctypes.byref(c), None, ctypes.byref(h)) == getattr(native, code)
+    assert msg in lib.sp_last_error()
