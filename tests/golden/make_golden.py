@@ -88,5 +88,50 @@ def main():
     print("wrote", sorted(p.name for p in HERE.iterdir()))
 
 
+# ---- SURVEY §8f fixtures: place_vocab, scenario files, Gantt export ----------
+
+EXTRA_SCENARIOS = [
+    "{}",
+    '{"model":{"layers":8,"hidden":4096,"ffn":11008,"heads":32,"query_groups":32,"vocab":32000},'
+    '"parallelism":{"pp":2},"run":{"seq_len":131072,"microbatches":4,"slices":8,"checkpointing":"selective"},'
+    '"scheme":"slimpipe","exchange":"off","seed":7}',
+    '{"model":{"layers":80,"hidden":8192,"ffn":28672,"heads":64,"query_groups":8,"vocab":128000},'
+    '"parallelism":{"tp":8,"pp":8,"stages_per_device":2},"run":{"seq_len":1048576,"microbatches":2,"slices":32,'
+    '"checkpointing":"full","offload_ratio":0.25,"vocab_parallel":true},"cost":{"alpha_linear":1.5,'
+    '"beta_attn":2.5e-07,"vocab_gemm":0.125},"comm":{"bandwidth":4.5e11,"latency":1e-05},'
+    '"coeffs":{"key":0.5,"value":0.5},"exchange":"on+early","seed":123}',
+    '{"model":{"layerz":1}}',
+    '{"parallelism":{"pp":4},"run":{"slices":6}}',
+]
+
+
+def extras():
+    out = {"scenario": {}, "gantt": {}, "gantt_full": {}, "vocab": {}}
+    for t in EXTRA_SCENARIOS:
+        r = O.ref_text("ref_scenario_json", t.encode())
+        out["scenario"][t] = "error" if r.startswith('{"error') else r
+    cost = (C.c_double * 4)(1.0, 1e-3, 2.0, 1.0)
+    comm = (C.c_double * 2)(1e3, 0.5)
+    for p, v, m, n in [(1, 1, 2, 4), (2, 1, 2, 4), (2, 2, 2, 4), (4, 1, 4, 8), (4, 2, 2, 8), (8, 1, 4, 16)]:
+        for mode in ((0, 1) if v == 1 else (0,)):
+            for svg in (0, 1):
+                text = O.ref_text("ref_gantt_json", p, v, m, n, mode, cost, comm, 1024 * n, svg)
+                key = f"p{p}v{v}m{m}n{n}mode{mode}svg{svg}"
+                out["gantt"][key] = hashlib.sha256(text.encode()).hexdigest()
+                if (p, v, m, n, mode) == (2, 1, 2, 4, 0):
+                    out["gantt_full"][key] = text
+    for p, m, n in [(2, 2, 4), (2, 4, 8), (4, 2, 8), (8, 2, 16)]:
+        S = 1024 * n
+        for raw in (0, 1):
+            a, b = (1.0, 1.0) if raw else (1.0 / S, 1.0 / S ** 2)
+            text = O.ref_text("ref_vocab_json", p, 1, m, n, 1, a, b, 4096 if raw else S)
+            out["vocab"][f"p{p}m{m}n{n}raw{raw}"] = hashlib.sha256(text.encode()).hexdigest()
+    (HERE / "planning_extras.json").write_text(json.dumps(out, indent=0, sort_keys=True) + "\n")
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["--extras"]:
+        extras()
+    else:
+        main()
+        extras()

@@ -121,3 +121,52 @@ def test_bundled_scenarios_are_the_bench_configs():
         text = (root / f"c2_llama7b_shapes_128k_pp{pp}.json").read_text()
         assert P.scenario_text(text) + "\n" == text
         assert StepConfig.from_scenario(text) == StepConfig.c2(pp=pp, recompute="selective")
+
+
+# ---- the same parity against committed fixtures (no reference needed) --------
+
+def _extras():
+    import hashlib
+    from pathlib import Path
+    g = json.loads((Path(__file__).resolve().parent / "golden" / "planning_extras.json").read_text())
+    return g, (lambda s: hashlib.sha256(s.encode()).hexdigest())
+
+
+def test_scenarios_match_golden():
+    g, _ = _extras()
+    assert len(g["scenario"]) == 5
+    for text, ref in g["scenario"].items():
+        if ref == "error":
+            with pytest.raises(ValueError):
+                P.scenario_text(text)
+        else:
+            assert P.scenario_text(text) == ref
+
+
+def test_gantt_matches_golden():
+    g, sha = _extras()
+    cost, comm = (1.0, 1e-3, 2.0, 1.0), (1e3, 0.5)
+    for key, digest in g["gantt"].items():
+        p, rest = key[1:].split("v", 1)
+        v, rest = rest.split("m", 1)
+        m, rest = rest.split("n", 1)
+        n, rest = rest.split("mode", 1)
+        mode, svg = rest.split("svg")
+        p, v, m, n, mode, svg = map(int, (p, v, m, n, mode, svg))
+        text = P.gantt_text(p, v, m, n, ["off", "on", "early"][mode], cost, comm, 1024 * n, bool(svg))
+        assert sha(text) == digest, key
+        if key in g["gantt_full"]:
+            assert text == g["gantt_full"][key]
+    assert len(g["gantt"]) == 20
+
+
+def test_place_vocab_matches_golden():
+    g, sha = _extras()
+    for key, digest in g["vocab"].items():
+        p, rest = key[1:].split("m", 1)
+        m, rest = rest.split("n", 1)
+        n, raw = rest.split("raw")
+        p, m, n, raw = map(int, (p, m, n, raw))
+        S = 1024 * n
+        a, b = (1.0, 1.0) if raw else (1.0 / S, 1.0 / S ** 2)
+        assert sha(P.place_vocab_text(p, 1, m, n, True, a, b, 4096 if raw else S)) == digest, key
