@@ -29,6 +29,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -376,12 +377,31 @@ class Runtime {
       }
     }
     if (vp) SP_CUDA(cudaStreamCreateWithFlags(&s_vocab, cudaStreamNonBlocking));
+    if (vp && std::getenv("SP_VOCAB_WARMUP")) SP_TRY(vocab_warmup());  // diagnostics
     SP_TRY(alloc_params());
     SP_TRY(alloc_arena());
     SP_TRY(alloc_workspace());
     SP_TRY(alloc_exchange());
     SP_TRY(init_weights(c.seed));
     SP_CUDA(cudaStreamSynchronize(comp));
+    return SP_OK;
+  }
+
+  // Diagnostics for the open vocab-parallel stall: run each
+  // vocab collective once at its real message size before the arena exists,
+  // so NCCL's lazy connection setup happens here (same order on all ranks)
+  // instead of inside the asynchronously enqueued step.
+  int vocab_warmup() {
+    void* buf = nullptr;
+    SP_CUDA(cudaMalloc(&buf, size_t(Ls) * size_t(h) * 4));
+    SP_CUDA(cudaMemsetAsync(buf, 0, size_t(Ls) * size_t(h) * 4, s_vocab));
+    float* f = static_cast<float*>(buf);
+    SP_NCCL(ncclBroadcast(buf, buf, Ls * h, ncclBfloat16, p - 1, nc_bwd, s_vocab));
+    SP_NCCL(ncclAllReduce(f, f, Ls, ncclFloat32, ncclMax, nc_bwd, s_vocab));
+    SP_NCCL(ncclAllReduce(f, f, 2 * Ls, ncclFloat32, ncclSum, nc_bwd, s_vocab));
+    SP_NCCL(ncclReduce(f, f, Ls * h, ncclFloat32, ncclSum, p - 1, nc_bwd, s_vocab));
+    SP_CUDA(cudaStreamSynchronize(s_vocab));
+    SP_CUDA(cudaFree(buf));
     return SP_OK;
   }
 
