@@ -338,11 +338,25 @@ class Runtime {
     if (p > 1) {
       ncclUniqueId id[SP_NCCL_IDS];
       std::memcpy(id, ids, sizeof id);
-      SP_NCCL(ncclCommInitRank(&nc_fwd, p, id[0], rank));
-      SP_NCCL(ncclCommInitRank(&nc_bwd, p, id[1], rank));
+      // SP_NCCL_MAX_CTAS=N (diagnostics, default unset = NCCL's choice) caps
+      // the CTAs of every stage communicator's kernels
+      ncclConfig_t ccfg = NCCL_CONFIG_INITIALIZER;
+      ncclConfig_t* pcfg = nullptr;
+      if (const char* mc = std::getenv("SP_NCCL_MAX_CTAS")) {
+        ccfg.maxCTAs = std::max(1, std::atoi(mc));
+        ccfg.minCTAs = 1;
+        pcfg = &ccfg;
+      }
+      if (pcfg) {
+        SP_NCCL(ncclCommInitRankConfig(&nc_fwd, p, id[0], rank, pcfg));
+        SP_NCCL(ncclCommInitRankConfig(&nc_bwd, p, id[1], rank, pcfg));
+      } else {
+        SP_NCCL(ncclCommInitRank(&nc_fwd, p, id[0], rank));
+        SP_NCCL(ncclCommInitRank(&nc_bwd, p, id[1], rank));
+      }
       // link (r, r+1) comes from split A when r is even, split B when r is odd
       auto split = [&](ncclComm_t parent, int color, int key, ncclComm_t* out) -> int {
-        SP_NCCL(ncclCommSplit(parent, color, key, out, nullptr));
+        SP_NCCL(ncclCommSplit(parent, color, key, out, pcfg));
         return SP_OK;
       };
       // v > 1 (even p): split B also carries the ring's wrap link (p-1, 0),
