@@ -90,6 +90,10 @@ class Runtime {
   int rank = 0, p = 1, stage = 1, Lps = 1;  // stage: the current pass's (global) stage
   int v = 1, nst = 1, cur = 0, lbase = 0;   // stages per device, total stages, pass's local chunk, its first layer
   bool first_dev = true, last_dev = true;   // owns stage 1 / stage nst
+  // SP_JIT_RECV=1 (diagnostics): stage receives wait for the
+  // compute stream to reach their pass instead of being posted as soon as a
+  // ring buffer frees (fewer NCCL kernels spinning on the SMs at once)
+  bool jit_recv = std::getenv("SP_JIT_RECV") != nullptr;
   int64_t Ls = 0, h = 0, H = 0, qd = 0, kvd = 0, qkv_w = 0;
   pipelab::Schedule sched;
   std::vector<pipelab::PassId> order;
@@ -925,6 +929,7 @@ class Runtime {
       const int b = ain_idx;
       ain_idx ^= 1;
       SP_CUDA(cudaStreamWaitEvent(s_act_in, ev_ain_free[b], 0));
+      if (jit_recv) SP_TRY(link(comp, s_act_in));  // post the receive only when this pass starts
       SP_NCCL(ncclRecv(ain_buf[b], Ls * h, ncclBfloat16, 0, c_act_in, s_act_in));
       SP_TRY(link(s_act_in, comp));
       SP_CUDA(cudaEventRecord(t0, comp));  // busy time starts once the input is here
@@ -1109,6 +1114,7 @@ class Runtime {
       gin_idx ^= 1;
       dx = gin_buf[gb];
       SP_CUDA(cudaStreamWaitEvent(s_grad_in, ev_gin_free[gb], 0));
+      if (jit_recv) SP_TRY(link(comp, s_grad_in));
       SP_NCCL(ncclRecv(dx, Ls * h, ncclBfloat16, 1, c_grad_in, s_grad_in));
       cudaEvent_t got;
       SP_CUDA(cudaEventCreateWithFlags(&got, cudaEventDisableTiming));

@@ -26,7 +26,7 @@ def device_orders(p, v, m, n, vp):
               s["passes"][i]["stage"]) for i in dev] for dev in s["device_order"]]
 
 
-def build(devs, p, v, vp, depth=2):
+def build(devs, p, v, vp, depth=2, jit_recv=False):
     nst = p * v
     ops = {}  # (rank, stream) -> list of op dicts
     seqs = {}
@@ -49,7 +49,8 @@ def build(devs, p, v, vp, depth=2):
             if kind == 0:  # F
                 if s > 1:
                     b = ain; ain = (ain + 1) % depth
-                    add("act_in", "recv", [ev[("ain", b)]], ("act", (r - 1) % p, r, k, i, s - 1))
+                    add("act_in", "recv", [ev[("ain", b)], cur("act_in")] + ([cur("comp")] if jit_recv else []),
+                        ("act", (r - 1) % p, r, k, i, s - 1))
                     add("comp", "wait", [cur("act_in"), cur("comp")])
                     rec(("ain", b), "comp")
                 if s < nst:
@@ -68,7 +69,8 @@ def build(devs, p, v, vp, depth=2):
                 gb = None
                 if s < nst:
                     gb = gin; gin = (gin + 1) % depth
-                    add("grad_in", "recv", [ev[("gin", gb)], cur("grad_in")], ("grad", (r + 1) % p, r, k, i, s + 1))
+                    add("grad_in", "recv", [ev[("gin", gb)], cur("grad_in")] + ([cur("comp")] if jit_recv else []),
+                        ("grad", (r + 1) % p, r, k, i, s + 1))
                     add("comp", "wait", [cur("grad_in"), cur("comp")])
                     add("comp", "bwd", [cur("comp")])
                 else:
@@ -182,8 +184,8 @@ def run_capped(ops, p, Q, seqs):
 
 
 
-def deadlocks(p, v, m, n, vp=False, depth=2, host_queue=None) -> bool:
-    ops, seqs = build(device_orders(p, v, m, n, vp), p, v, vp, depth)
+def deadlocks(p, v, m, n, vp=False, depth=2, host_queue=None, jit_recv=False) -> bool:
+    ops, seqs = build(device_orders(p, v, m, n, vp), p, v, vp, depth, jit_recv)
     if host_queue is None:
         return bool(run(ops, p))
     return run_capped(ops, p, host_queue, seqs)
