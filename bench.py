@@ -317,6 +317,9 @@ def main():
             with open(args.gantt, "w") as f:
                 f.write(P.gantt_measured_text(world, cfg.interleave, cfg.microbatches, cfg.slices, per_dev,
                                               cfg.vocab_parallel, cfg.seq_len))
+            with open(args.gantt + ".metrics.json", "w") as f:  # reference metric definitions, measured
+                json.dump(P.metrics_measured(world, cfg.interleave, cfg.microbatches, cfg.slices, per_dev,
+                                             cfg.vocab_parallel, cfg.seq_len), f, indent=1)
     busy = sum(e - s for _, s, e in passes)
     makespan = max_over_ranks(step_ms)
     busy_all = sum_over_ranks(busy)

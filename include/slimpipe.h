@@ -89,6 +89,10 @@ int sp_plan_gantt_json(int p, int v, int m, int n, int mode, const double* cost,
 /* the same export for a measured step: per-device CUDA-event spans (counts[d]
  * entries of pass id / start / end, devices concatenated) against the
  * executor's schedule */
+/* the reference's metric definitions (simulator.cpp:348-409) on a measured
+ * step (inputs as sp_plan_gantt_measured): makespan, bubble, busy, idle, phases */
+int sp_plan_metrics_measured(int p, int v, int m, int n, int vocab_parallel, int64_t seq_len, const int32_t* counts,
+                             const int32_t* pass_ids, const double* starts, const double* ends, char** out);
 int sp_plan_gantt_measured(int p, int v, int m, int n, int vocab_parallel, int64_t seq_len, const int32_t* counts,
                            const int32_t* pass_ids, const double* starts, const double* ends, int svg, char** out);
 

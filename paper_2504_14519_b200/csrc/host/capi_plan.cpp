@@ -366,6 +366,56 @@ int sp_plan_gantt_json(int p, int v, int m, int n, int mode, const double* cost,
   });
 }
 
+namespace {
+// executor schedule + a measured per-device timeline (see sp_plan_gantt_measured)
+std::pair<Schedule, Timeline> measured(int p, int v, int m, int n, int vocab_parallel, int64_t seq_len,
+                                       const int32_t* counts, const int32_t* pass_ids, const double* starts,
+                                       const double* ends) {
+  Schedule s = gen_slimpipe(gen_cfg(p, v, m, n));
+  if (vocab_parallel) {
+    SimInputs in;
+    in.cost.alpha_linear = 1.0 / double(seq_len);
+    in.cost.beta_attn = 1.0 / (double(seq_len) * double(seq_len));
+    in.seq_len = seq_len;
+    s = place_vocab(s, true, in);
+  }
+  Timeline tl;
+  tl.per_device.resize(static_cast<size_t>(p));
+  int64_t x = 0;
+  for (int d = 0; d < p; ++d)
+    for (int e = 0; e < counts[d]; ++e, ++x) {
+      if (pass_ids[x] < 0 || size_t(pass_ids[x]) >= s.passes.size())
+        throw std::invalid_argument("measured timeline: pass id out of range");
+      tl.per_device[size_t(d)].push_back({PassId(pass_ids[x]), starts[x], ends[x]});
+      tl.makespan = std::max(tl.makespan, ends[x]);
+    }
+  return {std::move(s), std::move(tl)};
+}
+}  // namespace
+
+// The reference's metric definitions (simulator.cpp:348-409) on a measured
+// timeline: makespan, bubble fraction, per-device busy / idle and phases.
+int sp_plan_metrics_measured(int p, int v, int m, int n, int vocab_parallel, int64_t seq_len, const int32_t* counts,
+                             const int32_t* pass_ids, const double* starts, const double* ends, char** out) {
+  return guarded(out, [&] {
+    auto [s, tl] = measured(p, v, m, n, vocab_parallel, seq_len, counts, pass_ids, starts, ends);
+    const Metrics mt = metrics_from_timeline(s, tl, unit_memory_model(p, v, n), ExchangeAnnotation{});
+    std::ostringstream os;
+    os << "{\"makespan\":" << g17(mt.makespan) << ",\"bubble\":" << g17(mt.bubble_fraction) << ",\"busy\":[";
+    for (int d = 0; d < p; ++d) os << (d ? "," : "") << g17(mt.device_busy[size_t(d)]);
+    os << "],\"idle\":[";
+    for (int d = 0; d < p; ++d) os << (d ? "," : "") << g17(mt.device_idle[size_t(d)]);
+    os << "],\"phases\":[";
+    for (int d = 0; d < p; ++d) {
+      const DevicePhases& ph = mt.phases[size_t(d)];
+      os << (d ? "," : "") << "[" << g17(ph.warmup_idle) << "," << g17(ph.midstream_idle) << ","
+         << g17(ph.cooldown_idle) << "]";
+    }
+    os << "]}";
+    return os.str();
+  });
+}
+
 // Gantt of a MEASURED step: the executors' schedule (gen_slimpipe(p, v, m, n),
 // plus place_vocab with the runtime's normalised costs when vocab_parallel)
 // and each device's CUDA-event spans (counts[d] passes: pass id, start, end
@@ -373,24 +423,7 @@ int sp_plan_gantt_json(int p, int v, int m, int n, int mode, const double* cost,
 int sp_plan_gantt_measured(int p, int v, int m, int n, int vocab_parallel, int64_t seq_len, const int32_t* counts,
                            const int32_t* pass_ids, const double* starts, const double* ends, int svg, char** out) {
   return guarded(out, [&] {
-    Schedule s = gen_slimpipe(gen_cfg(p, v, m, n));
-    if (vocab_parallel) {
-      SimInputs in;
-      in.cost.alpha_linear = 1.0 / double(seq_len);
-      in.cost.beta_attn = 1.0 / (double(seq_len) * double(seq_len));
-      in.seq_len = seq_len;
-      s = place_vocab(s, true, in);
-    }
-    Timeline tl;
-    tl.per_device.resize(static_cast<size_t>(p));
-    int64_t x = 0;
-    for (int d = 0; d < p; ++d)
-      for (int e = 0; e < counts[d]; ++e, ++x) {
-        if (pass_ids[x] < 0 || size_t(pass_ids[x]) >= s.passes.size())
-          throw std::invalid_argument("gantt: pass id out of range");
-        tl.per_device[size_t(d)].push_back({PassId(pass_ids[x]), starts[x], ends[x]});
-        tl.makespan = std::max(tl.makespan, ends[x]);
-      }
+    auto [s, tl] = measured(p, v, m, n, vocab_parallel, seq_len, counts, pass_ids, starts, ends);
     return svg ? gantt_svg(s, tl) : gantt_json(s, tl);
   });
 }

@@ -48,6 +48,8 @@ _SIGS = {
     "sp_plan_gantt_json": (C.c_int, [C.c_int] * 5 + [_f64p, _f64p, C.c_int64, C.c_int, _charpp]),
     "sp_plan_gantt_measured": (C.c_int, [C.c_int] * 5 + [C.c_int64, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                                          _f64p, _f64p, C.c_int, _charpp]),
+    "sp_plan_metrics_measured": (C.c_int, [C.c_int] * 5 + [C.c_int64, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                                           _f64p, _f64p, _charpp]),
     "sp_attn_fwd": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
                               _i32p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p,
                               C.c_int64, C.c_void_p, C.c_void_p]),

@@ -155,3 +155,15 @@ def gantt_measured_text(p: int, v: int, m: int, n: int, per_device, vocab_parall
                         N.arr(C.c_int32, counts), N.arr(C.c_int32, [int(e[0]) for e in flat]),
                         N.arr(C.c_double, [float(e[1]) for e in flat]), N.arr(C.c_double, [float(e[2]) for e in flat]),
                         int(svg))
+
+
+def metrics_measured(p: int, v: int, m: int, n: int, per_device, vocab_parallel: bool = False,
+                     seq_len: int = 1) -> dict:
+    """The reference's metric definitions (simulator.cpp:348-409) on a measured
+    step's per-device (pass id, start, end) spans."""
+    counts = [len(rows) for rows in per_device]
+    flat = [e for rows in per_device for e in rows]
+    return json.loads(N._json_call("sp_plan_metrics_measured", p, v, m, n, int(vocab_parallel), seq_len,
+                                   N.arr(C.c_int32, counts), N.arr(C.c_int32, [int(e[0]) for e in flat]),
+                                   N.arr(C.c_double, [float(e[1]) for e in flat]),
+                                   N.arr(C.c_double, [float(e[2]) for e in flat])))

@@ -170,3 +170,18 @@ def test_place_vocab_matches_golden():
         S = 1024 * n
         a, b = (1.0, 1.0) if raw else (1.0 / S, 1.0 / S ** 2)
         assert sha(P.place_vocab_text(p, 1, m, n, True, a, b, 4096 if raw else S)) == digest, key
+
+
+@pytest.mark.parametrize("p,v,m,n", [(2, 1, 2, 4), (4, 1, 4, 8), (4, 2, 2, 8), (8, 1, 4, 16)])
+def test_metrics_of_a_measured_timeline_use_the_reference_definitions(p, v, m, n):
+    """Fed simulate()'s own timeline as if it were measured, the measured-run
+    metrics reproduce simulate()'s makespan, bubble, busy time and phases
+    (simulator.cpp:348-409) — the definitions bench.py's timelines go through."""
+    sim = P.simulate(p, v, m, n, "off", (1.0, 1e-3, 2.0, 1.0), (0.0, 0.0), 1024 * n)
+    rows = [[tuple(e) for e in dev] for dev in sim["timeline"]]
+    got = P.metrics_measured(p, v, m, n, rows)
+    assert got["makespan"] == pytest.approx(sim["makespan"], rel=1e-12)
+    assert got["bubble"] == pytest.approx(sim["bubble"], rel=1e-9, abs=1e-12)
+    assert got["busy"] == pytest.approx(sim["busy"], rel=1e-12)
+    for a, b in zip(got["phases"], sim["phases"]):
+        assert a == pytest.approx(b, rel=1e-9, abs=1e-9)
