@@ -167,3 +167,17 @@ def metrics_measured(p: int, v: int, m: int, n: int, per_device, vocab_parallel:
                                    N.arr(C.c_int32, counts), N.arr(C.c_int32, [int(e[0]) for e in flat]),
                                    N.arr(C.c_double, [float(e[1]) for e in flat]),
                                    N.arr(C.c_double, [float(e[2]) for e in flat])))
+
+
+def simulate_scenario(text: str) -> dict:
+    """simulate() of a scenario file's run (gen_slimpipe(pp, stages_per_device,
+    microbatches, slices) under its cost / comm model, sequence length and
+    exchange mode; unit memory model): the predicted side of the same file
+    StepConfig.from_scenario executes."""
+    sc = scenario(text)
+    if sc["scheme"] != "slimpipe":
+        raise ValueError("simulate_scenario: scheme slimpipe only")
+    pa, rn, co, cm = sc["parallelism"], sc["run"], sc["cost"], sc["comm"]
+    return simulate(pa["pp"], pa["stages_per_device"], rn["microbatches"], rn["slices"], sc["exchange"],
+                    (co["alpha_linear"], co["beta_attn"], co["bwd_input_mult"], co["bwd_weight_mult"]),
+                    (cm["bandwidth"], cm["latency"]), rn["seq_len"])

@@ -185,3 +185,13 @@ def test_metrics_of_a_measured_timeline_use_the_reference_definitions(p, v, m, n
     assert got["busy"] == pytest.approx(sim["busy"], rel=1e-12)
     for a, b in zip(got["phases"], sim["phases"]):
         assert a == pytest.approx(b, rel=1e-9, abs=1e-9)
+
+
+def test_one_scenario_file_drives_simulate_and_the_step():
+    from pathlib import Path
+    text = (Path(__file__).resolve().parents[1] / "scenarios" / "c2_llama7b_shapes_128k_pp2.json").read_text()
+    cfg = StepConfig.from_scenario(text)
+    sim = P.simulate_scenario(text)
+    direct = P.simulate(cfg.pp, cfg.interleave, cfg.microbatches, cfg.slices, cfg.exchange, (1.0, 0.0, 2.0, 1.0),
+                        (0.0, 0.0), cfg.seq_len)
+    assert sim == direct and len(sim["busy"]) == cfg.pp
