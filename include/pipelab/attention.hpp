@@ -4,19 +4,18 @@
 // (proj/include/pipelab/attention.hpp:14-61), realised on the
 // B200: chunk_attention / accumulate_chunk run K1 (sm_100a tcgen05, bf16
 // operands, fp32 softmax statistics) on the current CUDA device; the fp64
-// types and signatures are the reference's.  Differences, by design:
-//   * operands are rounded to bf16 on the way in (results agree with the fp64
-//     reference within the bf16 tolerance of the parity tests);
-//   * a state's row_max holds the row's log-sum-exp and row_sumexp 1 (any
-//     stabiliser is valid for the merge/finalize algebra; fully masked rows
-//     keep the reference's -inf / 0);
-//   * shapes the kernels do not tile throw std::invalid_argument: head_dim in
-//     {64, 128}, query rows and every chunk length multiples of 128, and for
-//     accumulate_chunk a chunk that is either fully visible or the diagonal
-//     chunk of a slice (rows == chunk length, chunk ends at total_kv) — the
-//     two cases of the sliced schedule.  There is no CPU fallback.
-// merge_partials / finalize are O(rows·d) host glue with the reference's
-// formulas (attention.cpp:63-92).
+// types, signatures, state semantics and exceptions are the reference's:
+//   * any query rows, chunk lengths, chunk positions and head widths up to
+//     128 (the host pads to the kernel tiles and masks the padding; the scale
+//     is 1/sqrt(d) of the real width);
+//   * the state is the reference's: unnormalised partial output, the true
+//     row max of the scaled scores, and the row sum of exponentials relative
+//     to it (the kernel reports its row max next to the log-sum-exp);
+//   * operands are rounded to bf16 on the way in, so results agree with the
+//     fp64 reference within the bf16 tolerance (rel 2e-2), not to 1e-12.
+// merge_partials / finalize are O(rows·d) host arithmetic on the returned
+// host states with the reference's formulas (attention.cpp:63-92).
+// There is no CPU fallback: without a CUDA device every call throws.
 
 #include <cstdint>
 #include <utility>

@@ -111,12 +111,28 @@ int sp_plan_gantt_measured(int p, int v, int m, int n, int vocab_parallel, int64
  *          scores (row_max + log(row_sumexp)); -inf for fully masked rows
  * Query head h reads kv head h / (heads / kv_heads).
  * Requirements: head_dim in {64, 128}; q_rows, chunk_len multiples of 128;
- * strides multiples of 8 elements. */
-#define SP_MAX_CHUNKS 64
+ * strides multiples of 8 elements.  The chunk table travels in kernel
+ * parameter space (SP_MAX_CHUNKS entries). */
+#define SP_MAX_CHUNKS 256
 int sp_attn_fwd(const void* q, int64_t q_rows, int64_t q_stride, const void* k_pool, const void* v_pool,
                 int64_t pool_rows, int64_t kv_stride, const int32_t* chunk_row, int n_chunks, int chunk_len,
                 int heads, int kv_heads, int head_dim, int causal, void* o, int64_t o_stride, float* lse,
                 sp_stream_t stream);
+
+/* sp_attn_fwd with the mask and scale spelled out — what the pipelab
+ * attention API (attention.hpp: arbitrary rows, chunk lengths, head_dim <=
+ * 128, chunks at any position) runs after padding to the kernel tiles:
+ *   causal: query row r sees keys <= r + causal_off (sp_attn_fwd uses
+ *           total_kv - q_rows, reference attention.cpp:34-35);
+ *   keys >= kv_valid are masked (padding; kv_valid <= n_chunks*chunk_len);
+ *   scale: softmax scale (reference 1/sqrt(d) of the UNPADDED head_dim, :31);
+ *   row_max (optional, fp32 [heads][q_rows]): the true row max of the scaled
+ *           scores, so the caller can form the reference's unnormalised state
+ *           (row_sumexp = exp(lse - row_max), partial = O * row_sumexp). */
+int sp_attn_fwd_masked(const void* q, int64_t q_rows, int64_t q_stride, const void* k_pool, const void* v_pool,
+                       int64_t pool_rows, int64_t kv_stride, const int32_t* chunk_row, int n_chunks, int chunk_len,
+                       int heads, int kv_heads, int head_dim, int causal, int64_t causal_off, int64_t kv_valid,
+                       double scale, void* o, int64_t o_stride, float* lse, float* row_max, sp_stream_t stream);
 
 /* Backward of sp_attn_fwd.  Accumulates (+=) into fp32 buffers:
  *   dq_acc  fp32 [q_rows][heads*head_dim]
@@ -204,6 +220,17 @@ int sp_nccl_unique_id(void* out128);
  * apply_exchange are executed: Q (+ KV chunks, dO and statistics in backward
  * ticks) go to the receiving stage, which returns attention partials. */
 int sp_runtime_create(const sp_model_config* cfg, const void* nccl_ids, void** handle);
+/* Single-GPU loopback transport (tests, one-GPU boxes): all pp ranks run as
+ * host threads of ONE process on the current device; each thread creates
+ * its rank's runtime with sp_runtime_create_loopback on a shared world and
+ * calls sp_runtime_step concurrently.  Stage links and exchange transfers
+ * then move through device-side flags + copy kernels instead of NCCL, with
+ * the same send/recv order and group semantics (csrc/host/transport.hpp).
+ * Vocabulary parallelism (collectives) is not offered on it. */
+int sp_loopback_create(int ranks, void** world);
+int sp_loopback_destroy(void* world);
+int sp_loopback_errors(void* world); /* message size mismatches seen so far (0 = none) */
+int sp_runtime_create_loopback(const sp_model_config* cfg, void* world, void** handle);
 int sp_runtime_destroy(void* handle);
 /* tokens/targets: [microbatches][seq_len] int32 (host, or device when on_device);
  * only stage 1 reads tokens and only the last stage reads targets (< 0 = ignore).

@@ -10,6 +10,8 @@
  *   orc_merge_partials     follows merge_partials     attention.cpp:63-82
  *   orc_finalize           follows finalize           attention.cpp:84-92
  *   orc_chunk_attention    follows chunk_attention    attention.cpp:94-111
+ *   orc_fwd_rows / orc_bwd_rows / orc_bwd_keys  sampled rows and keys of one
+ *                          head at bench size (same algebra; see below)
  *   orc_attn_bwd_head      NEW (not in the reference): exact softmax-attention
  *                          gradients; pinned against the reference forward by
  *                          finite differences in tests/test_oracle.py, the way
@@ -314,5 +316,175 @@ int orc_mha_bwd(const float *q, int rows, int a, int d, const float *k, const fl
   pthread_mutex_init(&jb.mu, NULL);
   run_threads(&jb, bwd_worker);
   pthread_mutex_destroy(&jb.mu);
+  return 0;
+}
+
+/* ---- sampled rows / keys of one head at full (bench) size ----------------
+ * For the bench-scale parity tests (tests/test_attn_scale_gpu.py): exact fp64
+ * values of a few query rows / key rows of a slice whose full oracle would be
+ * far too expensive on the CPU.  One head: q[rows][qs], k/v[total_kv][ks]
+ * (fp32 values, bf16-rounded by the caller), causal bottom-right aligned as
+ * attention.cpp:34-35 (row r sees keys <= total_kv - rows + r).
+ *
+ *   orc_fwd_rows   O and natural-log LSE of the selected rows: the reference
+ *                  fold (accumulate_chunk :49-59 + finalize :84-92) over the
+ *                  whole visible prefix in one pass-pair (max, then sums).
+ *   orc_bwd_rows   dQ of the selected rows, and
+ *   orc_bwd_keys   dK/dV of the selected keys, both for the backward taken as
+ *                  the kernel defines it: a function of (Q, K, V, O, dO, LSE)
+ *                  with O / LSE given (D_i = rowsum(dO_i * O_i)), the same
+ *                  algebra as orc_attn_bwd_head above.
+ * Work is split over `threads` pthreads by selected item. */
+typedef struct {
+  const float *q, *k, *v, *dout, *o;
+  const double *lse;
+  int qs, ks, dos, os, rows, d, causal, n, threads, next;
+  int64_t total_kv;
+  const int *sel;
+  double *out0, *out1;
+  pthread_mutex_t mu;
+} smp_job;
+
+static int smp_next(smp_job *jb) {
+  pthread_mutex_lock(&jb->mu);
+  int x = jb->next++;
+  pthread_mutex_unlock(&jb->mu);
+  return x;
+}
+
+static int64_t smp_limit(const smp_job *jb, int r) {
+  int64_t lim = jb->causal ? jb->total_kv - jb->rows + r : jb->total_kv - 1;
+  return lim >= jb->total_kv ? jb->total_kv - 1 : lim;
+}
+
+static double smp_dot(const float *a, const float *b, int d) {
+  double s = 0.0;
+  for (int c = 0; c < d; ++c) s += (double)a[c] * (double)b[c];
+  return s;
+}
+
+static void *fwd_rows_worker(void *arg) {
+  smp_job *jb = (smp_job *)arg;
+  const int d = jb->d;
+  const double scale = 1.0 / sqrt((double)d);
+  double *acc = (double *)malloc(sizeof(double) * d);
+  for (int x; (x = smp_next(jb)) < jb->n;) {
+    const int r = jb->sel[x];
+    const int64_t lim = smp_limit(jb, r);
+    const float *qr = jb->q + (size_t)r * jb->qs;
+    double m = -INFINITY, l = 0.0;
+    for (int64_t j = 0; j <= lim; ++j) {
+      const double s = smp_dot(qr, jb->k + (size_t)j * jb->ks, d) * scale;
+      if (s > m) m = s;
+    }
+    for (int c = 0; c < d; ++c) acc[c] = 0.0;
+    for (int64_t j = 0; j <= lim; ++j) {
+      const double e = exp(smp_dot(qr, jb->k + (size_t)j * jb->ks, d) * scale - m);
+      l += e;
+      const float *vj = jb->v + (size_t)j * jb->ks;
+      for (int c = 0; c < d; ++c) acc[c] += e * vj[c];
+    }
+    for (int c = 0; c < d; ++c) jb->out0[(size_t)x * d + c] = l > 0.0 ? acc[c] / l : 0.0;
+    jb->out1[x] = l > 0.0 ? m + log(l) : -INFINITY;
+  }
+  free(acc);
+  return NULL;
+}
+
+static double smp_delta(const smp_job *jb, int r) {
+  return smp_dot(jb->dout + (size_t)r * jb->dos, jb->o + (size_t)r * jb->os, jb->d);
+}
+
+static void *bwd_rows_worker(void *arg) {
+  smp_job *jb = (smp_job *)arg;
+  const int d = jb->d;
+  const double scale = 1.0 / sqrt((double)d);
+  for (int x; (x = smp_next(jb)) < jb->n;) {
+    const int r = jb->sel[x];
+    const int64_t lim = smp_limit(jb, r);
+    const float *qr = jb->q + (size_t)r * jb->qs, *dor = jb->dout + (size_t)r * jb->dos;
+    const double D = smp_delta(jb, r);
+    double *dq = jb->out0 + (size_t)x * d;
+    for (int c = 0; c < d; ++c) dq[c] = 0.0;
+    if (jb->lse[r] == -INFINITY) continue;
+    for (int64_t j = 0; j <= lim; ++j) {
+      const float *kj = jb->k + (size_t)j * jb->ks;
+      const double p = exp(smp_dot(qr, kj, d) * scale - jb->lse[r]);
+      const double ds = p * (smp_dot(dor, jb->v + (size_t)j * jb->ks, d) - D) * scale;
+      for (int c = 0; c < d; ++c) dq[c] += ds * kj[c];
+    }
+  }
+  return NULL;
+}
+
+static void *bwd_keys_worker(void *arg) {
+  smp_job *jb = (smp_job *)arg;
+  const int d = jb->d;
+  const double scale = 1.0 / sqrt((double)d);
+  for (int x; (x = smp_next(jb)) < jb->n;) {
+    const int64_t j = jb->sel[x];
+    const float *kj = jb->k + (size_t)j * jb->ks, *vj = jb->v + (size_t)j * jb->ks;
+    double *dk = jb->out0 + (size_t)x * d, *dv = jb->out1 + (size_t)x * d;
+    for (int c = 0; c < d; ++c) dk[c] = dv[c] = 0.0;
+    for (int r = 0; r < jb->rows; ++r) {
+      if (smp_limit(jb, r) < j || jb->lse[r] == -INFINITY) continue;
+      const float *qr = jb->q + (size_t)r * jb->qs, *dor = jb->dout + (size_t)r * jb->dos;
+      const double p = exp(smp_dot(qr, kj, d) * scale - jb->lse[r]);
+      const double ds = p * (smp_dot(dor, vj, d) - smp_delta(jb, r)) * scale;
+      for (int c = 0; c < d; ++c) {
+        dv[c] += p * dor[c];
+        dk[c] += ds * qr[c];
+      }
+    }
+  }
+  return NULL;
+}
+
+static void smp_run(smp_job *jb, void *(*fn)(void *)) {
+  pthread_mutex_init(&jb->mu, NULL);
+  int nt = jb->threads < 1 ? 1 : jb->threads;
+  pthread_t *th = (pthread_t *)malloc(sizeof(pthread_t) * nt);
+  for (int t = 0; t < nt; ++t) pthread_create(&th[t], NULL, fn, jb);
+  for (int t = 0; t < nt; ++t) pthread_join(th[t], NULL);
+  free(th);
+  pthread_mutex_destroy(&jb->mu);
+}
+
+/* o[nsel][d], lse[nsel] */
+int orc_fwd_rows(const float *q, int qs, int rows, int d, const float *k, const float *v, int ks,
+                 int64_t total_kv, int causal, const int *sel, int nsel, double *o, double *lse,
+                 int threads) {
+  smp_job jb;
+  memset(&jb, 0, sizeof jb);
+  jb.q = q; jb.qs = qs; jb.rows = rows; jb.d = d; jb.k = k; jb.v = v; jb.ks = ks;
+  jb.total_kv = total_kv; jb.causal = causal; jb.sel = sel; jb.n = nsel; jb.out0 = o; jb.out1 = lse;
+  jb.threads = threads;
+  smp_run(&jb, fwd_rows_worker);
+  return 0;
+}
+
+/* dq[nsel][d]; lse[rows] (natural log), o/dout[rows][os/dos] */
+int orc_bwd_rows(const float *q, int qs, int rows, int d, const float *k, const float *v, int ks,
+                 int64_t total_kv, int causal, const float *o, int os, const float *dout, int dos,
+                 const double *lse, const int *sel, int nsel, double *dq, int threads) {
+  smp_job jb;
+  memset(&jb, 0, sizeof jb);
+  jb.q = q; jb.qs = qs; jb.rows = rows; jb.d = d; jb.k = k; jb.v = v; jb.ks = ks; jb.o = o; jb.os = os;
+  jb.dout = dout; jb.dos = dos; jb.lse = lse; jb.total_kv = total_kv; jb.causal = causal; jb.sel = sel;
+  jb.n = nsel; jb.out0 = dq; jb.threads = threads;
+  smp_run(&jb, bwd_rows_worker);
+  return 0;
+}
+
+/* dk/dv[nsel][d] for key rows sel[] */
+int orc_bwd_keys(const float *q, int qs, int rows, int d, const float *k, const float *v, int ks,
+                 int64_t total_kv, int causal, const float *o, int os, const float *dout, int dos,
+                 const double *lse, const int *sel, int nsel, double *dk, double *dv, int threads) {
+  smp_job jb;
+  memset(&jb, 0, sizeof jb);
+  jb.q = q; jb.qs = qs; jb.rows = rows; jb.d = d; jb.k = k; jb.v = v; jb.ks = ks; jb.o = o; jb.os = os;
+  jb.dout = dout; jb.dos = dos; jb.lse = lse; jb.total_kv = total_kv; jb.causal = causal; jb.sel = sel;
+  jb.n = nsel; jb.out0 = dk; jb.out1 = dv; jb.threads = threads;
+  smp_run(&jb, bwd_keys_worker);
   return 0;
 }

@@ -367,12 +367,7 @@ int launch_bwd(const CUtensorMap& tq, const CUtensorMap& tdo, const CUtensorMap&
                const BwdParams& prm, int k_tiles, int kv_heads, cudaStream_t st) {
   auto kern = attn_bwd_kernel<D>;
   const size_t smem = sizeof(BwdSmem<D>) + 1024;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return cuda_status(e, "attn_bwd: set smem");
-    configured = true;
-  }
+  if (int rc = set_smem_once(reinterpret_cast<const void*>(kern), smem, "attn_bwd: set smem")) return rc;
   kern<<<dim3(k_tiles, kv_heads), kThreads, smem, st>>>(tq, tdo, tk, tv, prm);
   count_launch(1);
   return cuda_status(cudaGetLastError(), "attn_bwd launch");
@@ -438,7 +433,7 @@ extern "C" int sp_attn_bwd_core(const void* q, int64_t q_rows, int64_t q_stride,
     if (chunk_row[c] < 0 || int64_t(chunk_row[c]) + chunk_len > pool_rows || acc_row[c] < 0 ||
         int64_t(acc_row[c]) + chunk_len > acc_rows)
       return set_error(SP_ERR_INVALID, "sp_attn_bwd: chunk %d outside the pool/accumulator", c);
-  if (head_dim == 128 && !getenv("SP_ATTN_BWD_V1"))
+  if (head_dim == 128)  // attn_bwd_v2.cu
     return attn_bwd_d128(q, q_rows, q_stride, k_pool, v_pool, pool_rows, kv_stride, chunk_row, n_chunks, chunk_len,
                          heads, kv_heads, causal, dout, do_stride, lse2, delta, dq_acc, dk_acc, dv_acc, acc_rows,
                          acc_row, st);
@@ -448,7 +443,7 @@ extern "C" int sp_attn_bwd_core(const void* q, int64_t q_rows, int64_t q_stride,
   prm.chunk_len = chunk_len;
   prm.group = heads / kv_heads;
   prm.causal = causal;
-  const int bq = head_dim == 128 ? 64 : 128;
+  const int bq = 128;
   prm.n_qtiles = int(q_rows / bq);
   prm.scale = float(1.0 / sqrt(double(head_dim)));
   prm.scale_log2 = float(1.4426950408889634 / sqrt(double(head_dim)));
@@ -470,7 +465,6 @@ extern "C" int sp_attn_bwd_core(const void* q, int64_t q_rows, int64_t q_stride,
       !make_tmap_bf16(&tv, v_pool, uint64_t(kv_stride), uint64_t(pool_rows), uint64_t(kv_stride), 128))
     return set_error(SP_ERR_CUDA, "sp_attn_bwd: cuTensorMapEncodeTiled failed (alignment?)");
   const int k_tiles = int(total_kv / 128);
-  if (head_dim == 128) return launch_bwd<128>(tq, tdo, tk, tv, prm, k_tiles, kv_heads, st);
   return launch_bwd<64>(tq, tdo, tk, tv, prm, k_tiles, kv_heads, st);
 }
 

@@ -23,7 +23,6 @@
 #include "kernels.hpp"
 #include "sm100.cuh"
 
-#include <cstdlib>
 
 namespace sp {
 namespace {
@@ -42,8 +41,6 @@ struct Params {
   float* dk;
   float* dv;
   int64_t acc_stride;
-  int trace;  // record a per-pair timeline of CTA (0,0) into g_bwd_trace
-  int dbg;    // diagnostics only: bit0 skip the dQ stage/reduce, bit1 skip the dQ MMA
   int chunk_row[SP_MAX_CHUNKS];
   int acc_row[SP_MAX_CHUNKS];
 };
@@ -65,12 +62,6 @@ struct Ctl {  // static shared memory: statistics and barriers
       acc_done;
   uint32_t tmem_base;
 };
-
-__device__ long long g_bwd_trace[12][512];
-#define TR(e, j)                                                                        \
-  do {                                                                                 \
-    if (tracing && (j) < 512) g_bwd_trace[e][(j)] = clock64();                        \
-  } while (0)
 
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -99,7 +90,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int n_pairs = per_head > 0 ? per_head * prm.group : 0;
   const int chunk = key0 / prm.chunk_len;
   const int kv_prow = prm.chunk_row[chunk] + key0 % prm.chunk_len;
-  const bool tracing = prm.trace && blockIdx.x == 0 && blockIdx.y == 0;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tm_q);
@@ -171,13 +161,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (warp == 1) {
         for (int j = 0; j < n_pairs; ++j) {
           const int s = j % NS, b = j & 1;
-          TR(0, j);
           mbar_wait(&ctl.q_full[s], (j / NS) & 1);
           if (j >= 2) {  // buffer b: dQ(j-2) drained, dV/dK(j-2) done reading P/dS
             mbar_wait(&ctl.dq_free[b], ((j >> 1) - 1) & 1);
             mbar_wait(&ctl.acc_free[b], ((j >> 1) - 1) & 1);
           }
-          TR(10, j);
           tc_fence_after();
           const uint64_t dq_k = smem_desc_sw128(smem_u32(sm.q[s]), 16, 1024);
           const uint64_t ddo_k = smem_desc_sw128(smem_u32(sm.dout[s]), 16, 1024);
@@ -189,20 +177,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             umma_bf16_ss_w(tmem + b * 128 + 64, dv_k + oa, ddo_k + ob, id_s, kk > 0);
           }
           umma_commit_warp(&ctl.sdp_full[b]);
-          TR(1, j);
         }
       } else {
         for (int j = 0; j < n_pairs; ++j) {
           const int s = j % NS, b = j & 1;
           mbar_wait(&ctl.pds_ready, j & 1);
-          TR(2, j);
           tc_fence_after();
           const uint64_t dq_mn = smem_desc_sw128(smem_u32(sm.q[s]), kSlabQ * 2, 1024);
           const uint64_t ddo_mn = smem_desc_sw128(smem_u32(sm.dout[s]), kSlabQ * 2, 1024);
           // dQ^T = K^T dS^T into pair j's (consumed) dP^T columns (K = 128 keys)
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {
-            if (prm.dbg & 2) break;
             const uint32_t ok = (kk * 16 * 128) >> 4;
             umma_bf16_ss_w(tmem + b * 128 + 64, dk_mn + ok, dds_mn + ok, id_dq, kk > 0);
           }
@@ -219,7 +204,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           umma_commit_warp(&ctl.q_empty[s]);  // S/dP(j) of warp 1 completed before pds_ready(j)
           umma_commit_warp(&ctl.pds_free);
           umma_commit_warp(&ctl.acc_free[b]);
-          TR(3, j);
         }
         umma_commit_warp(&ctl.acc_done);
       }
@@ -238,13 +222,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     for (int j = 0; j < n_pairs; ++j) {
       const int s = j % NS, b = j & 1;
-      const bool tl = ctid == 0;
 
       const int qrow0 = pair_row(j);
       const bool need_mask = prm.causal && (key0 + BK - 1 - off > qrow0);
       mbar_wait(&ctl.q_full[s], (j / NS) & 1);
       mbar_wait(&ctl.sdp_full[b], (j >> 1) & 1);
-      if (tl) TR(5, j);
       tc_fence_after();
       float sv[32], dp[32];
       tmem_ld32(tmem + lane_off + b * 128 + c0, sv);
@@ -276,9 +258,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         pk[x / 2] = pack_bf16(p0, p1);
         dk[x / 2] = pack_bf16(dd.x, dd.y);
       }
-      if (tl) TR(6, j);
       if (j > 0) mbar_wait(&ctl.pds_free, (j - 1) & 1);
-      if (tl) TR(7, j);
       // P^T / dS^T (packed bf16) over this WG's own S^T columns: A operands of
       // the dV / dK TS-UMMAs; dS^T also to smem: B operand of dQ^T = K^T dS^T.
       tmem_st16(tmem + lane_off + b * 128 + wg * 32, pk);
@@ -290,7 +270,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       fence_async_smem();
       tc_fence_before();
       mbar_arrive(&ctl.pds_ready);
-      if (tl) TR(8, j);
 
     }
     if (n_pairs > 0) {
@@ -325,9 +304,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane_off = uint32_t(quarter * 32) << 16;
     for (int jj = 0; jj < n_pairs; ++jj) {
       const int bb = jj & 1;
-      const bool tl = tracing && dtid == 0;
       mbar_wait(&ctl.dq_full[bb], (jj >> 1) & 1);
-      if (tl) TR(4, jj);
       tc_fence_after();
       float a0[32], a1[32];
       tmem_ld32(tmem + lane_off + bb * 128 + 64, a0);
@@ -335,7 +312,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(&ctl.dq_free[bb]);
-      if (prm.dbg & 1) continue;
       if (dtid == 0) bulk_wait_read<0>();  // the previous reduce has read the stage
       named_bar_sync(1, kDrain);
       const uint32_t st = smem_u32(sm.stage[0]) + uint32_t(d) * 4u;
@@ -346,7 +322,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       fence_async_smem();
       named_bar_sync(2, kDrain);
-      if (tl) TR(9, jj);
       if (dtid == 0) {
         tma_reduce_add_2d(&tm_dq, sm.stage[0], pair_head(jj) * D, pair_row(jj));
         bulk_commit();
@@ -384,8 +359,6 @@ int attn_bwd_d128(const void* q, int64_t q_rows, int64_t q_stride, const void* k
   prm.dk = dk_acc;
   prm.dv = dv_acc;
   prm.acc_stride = int64_t(kv_heads) * D;
-  prm.trace = getenv("SP_BWD_TRACE") != nullptr;
-  prm.dbg = getenv("SP_BWD_DBG") ? atoi(getenv("SP_BWD_DBG")) : 0;
   for (int c = 0; c < n_chunks; ++c) {
     prm.chunk_row[c] = chunk_row[c];
     prm.acc_row[c] = acc_row[c];
@@ -398,21 +371,11 @@ int attn_bwd_d128(const void* q, int64_t q_rows, int64_t q_stride, const void* k
       !make_tmap_f32(&tdq, dq_acc, uint64_t(heads) * D, uint64_t(q_rows), uint64_t(heads) * D, D, BQ))
     return set_error(SP_ERR_CUDA, "attn_bwd_d128: cuTensorMapEncodeTiled failed (alignment?)");
   const size_t smem = sizeof(Smem) + 1024;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(attn_bwd_d128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return cuda_status(e, "attn_bwd_d128: set smem");
-    configured = true;
-  }
+  if (int rc = set_smem_once(reinterpret_cast<const void*>(attn_bwd_d128_kernel), smem, "attn_bwd_d128: set smem"))
+    return rc;
   attn_bwd_d128_kernel<<<dim3(prm.total_kv / BK, kv_heads), kThreads, smem, st>>>(tq, tdo, tk, tv, tdq, prm);
   count_launch(1);
   return cuda_status(cudaGetLastError(), "attn_bwd_d128 launch");
 }
 
-int bwd_trace_copy(long long* out) {
-  return cuda_status(cudaMemcpyFromSymbol(out, g_bwd_trace, sizeof(long long) * 12 * 512), "trace copy");
-}
-
 }  // namespace sp
-
-extern "C" int sp_debug_bwd_trace(long long* out) { return sp::bwd_trace_copy(out); }

@@ -24,7 +24,6 @@
 #include "sm100.cuh"
 #include "kernels.hpp"
 
-#include <cstdlib>
 
 namespace sp {
 namespace {
@@ -39,6 +38,9 @@ struct FwdParams {
   int chunk_len;
   int group;  // heads / kv_heads
   int causal;
+  int kv_valid;        // keys >= kv_valid are masked (padding)
+  int64_t causal_off;  // causal: query row r sees keys <= r + causal_off
+  float* row_max;      // optional true row max (natural log units of scaled scores)
   float scale_log2;
   __nv_bfloat16* o;
   int64_t o_stride;
@@ -75,8 +77,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int head = blockIdx.y;
   const int kv_head = head / prm.group;
   const int row0 = tile * kBM;
-  const int kv_end = prm.causal ? prm.total_kv - prm.q_rows + row0 + kBM : prm.total_kv;
-  const int n_tiles = kv_end / kBN;
+  int64_t kmax = prm.kv_valid - 1;  // last key visible to some row of the tile
+  if (prm.causal) kmax = min(kmax, int64_t(row0) + kBM - 1 + prm.causal_off);
+  const int n_tiles = kmax < 0 ? 0 : int(kmax / kBN + 1);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tm_q);
@@ -173,8 +176,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t p_addr = smem_u32(sm.p);
     const float sl2 = prm.scale_log2;
     float m_used = -INFINITY;  // running max, log2 units of scaled scores
-    float l = 0.f;
+    float l = 0.f, m_true = -INFINITY;
     float sv[kBN];
+    const int64_t qlim = prm.causal ? min(int64_t(prm.kv_valid) - 1, int64_t(row0 + r) + prm.causal_off)
+                                    : int64_t(prm.kv_valid) - 1;
     for (int j = 0; j < n_tiles; ++j) {
       mbar_wait(&sm.s_full[j & 1], (j >> 1) & 1);
       tc_fence_after();
@@ -182,14 +187,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int c = 0; c < kBN / 32; ++c)
         tmem_ld32(tmem + lane_off + (j & 1) * 128 + c * 32, *reinterpret_cast<float(*)[32]>(&sv[c * 32]));
       tmem_wait_ld();
-      if (prm.causal && j == n_tiles - 1) {
+      const int64_t lim = qlim - int64_t(j) * kBN;  // columns c > lim are masked
+      if (lim < kBN - 1) {
+        const int lm = lim < -1 ? -1 : int(lim);
 #pragma unroll
         for (int c = 0; c < kBN; ++c)
-          if (c > r) sv[c] = -INFINITY;
+          if (c > lm) sv[c] = -INFINITY;
       }
       float mx = -INFINITY;
 #pragma unroll
       for (int c = 0; c < kBN; ++c) mx = fmaxf(mx, sv[c]);
+      m_true = fmaxf(m_true, mx);
       const float cand = mx * sl2;
       const bool grow = cand > m_used + 8.0f;
       float corr = 1.f;
@@ -258,6 +266,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     prm.lse[int64_t(head) * prm.q_rows + grow_row] =
         l > 0.f ? (m_used + __log2f(l)) * 0.69314718055994530942f : -INFINITY;
+    if (prm.row_max)
+      prm.row_max[int64_t(head) * prm.q_rows + grow_row] =
+          l > 0.f ? m_true * prm.scale_log2 * 0.69314718055994530942f : -INFINITY;
     tc_fence_before();
   }
   __syncthreads();
@@ -272,12 +283,7 @@ int launch_fwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& 
                int heads, cudaStream_t stream) {
   auto kern = attn_fwd_kernel<D, NS>;
   const size_t smem = sizeof(FwdSmem<D, NS>) + 1024;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return cuda_status(e, "attn_fwd: set smem");
-    configured = true;
-  }
+  if (int rc = set_smem_once(reinterpret_cast<const void*>(kern), smem, "attn_fwd: set smem")) return rc;
   kern<<<dim3(q_tiles, heads), kThreads, smem, stream>>>(tq, tk, tv, prm);
   count_launch(1);
   return cuda_status(cudaGetLastError(), "attn_fwd launch");
@@ -286,11 +292,15 @@ int launch_fwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& 
 }  // namespace
 }  // namespace sp
 
-extern "C" int sp_attn_fwd(const void* q, int64_t q_rows, int64_t q_stride, const void* k_pool, const void* v_pool,
-                           int64_t pool_rows, int64_t kv_stride, const int32_t* chunk_row, int n_chunks,
-                           int chunk_len, int heads, int kv_heads, int head_dim, int causal, void* o,
-                           int64_t o_stride, float* lse, sp_stream_t stream) {
-  using namespace sp;
+namespace sp {
+namespace {
+
+// Shared by sp_attn_fwd and sp_attn_fwd_masked: validation, then the d=128
+// (attn_fwd_v4.cu) or d=64 kernel.
+int attn_fwd_dispatch(const void* q, int64_t q_rows, int64_t q_stride, const void* k_pool, const void* v_pool,
+                      int64_t pool_rows, int64_t kv_stride, const int32_t* chunk_row, int n_chunks, int chunk_len,
+                      int heads, int kv_heads, int head_dim, const FwdMask& mk, void* o, int64_t o_stride, float* lse,
+                      cudaStream_t st) {
   if (head_dim != 64 && head_dim != 128)
     return set_error(SP_ERR_UNSUPPORTED, "sp_attn_fwd: head_dim %d not in {64,128}", head_dim);
   if (q_rows <= 0 || q_rows % 128 || chunk_len <= 0 || chunk_len % 128 || n_chunks < 0 || n_chunks > SP_MAX_CHUNKS)
@@ -302,40 +312,68 @@ extern "C" int sp_attn_fwd(const void* q, int64_t q_rows, int64_t q_stride, cons
       kv_stride < int64_t(kv_heads) * head_dim)
     return set_error(SP_ERR_INVALID, "sp_attn_fwd: bad strides");
   const int64_t total_kv = int64_t(n_chunks) * chunk_len;
-  if (causal && total_kv < q_rows)
-    return set_error(SP_ERR_UNSUPPORTED, "sp_attn_fwd: causal needs total_kv >= q_rows");
+  if (total_kv > INT32_MAX || mk.kv_valid < 0 || mk.kv_valid > total_kv || !(mk.scale > 0.0))
+    return set_error(SP_ERR_INVALID, "sp_attn_fwd: bad key range or scale");
+  for (int c = 0; c < n_chunks; ++c)
+    if (chunk_row[c] < 0 || int64_t(chunk_row[c]) + chunk_len > pool_rows)
+      return set_error(SP_ERR_INVALID, "sp_attn_fwd: chunk %d outside the pool", c);
+  if (head_dim == 128)
+    return attn_fwd_d128_ps(q, q_rows, q_stride, k_pool, v_pool, pool_rows, kv_stride, chunk_row, n_chunks, chunk_len,
+                            heads, kv_heads, mk, o, o_stride, lse, st);
   FwdParams prm{};
   prm.q_rows = int(q_rows);
   prm.total_kv = int(total_kv);
   prm.chunk_len = chunk_len;
   prm.group = heads / kv_heads;
-  prm.causal = causal;
-  prm.scale_log2 = float(1.4426950408889634 / sqrt(double(head_dim)));
+  prm.causal = mk.causal;
+  prm.kv_valid = int(mk.kv_valid);
+  prm.causal_off = mk.causal_off;
+  prm.row_max = mk.row_max;
+  prm.scale_log2 = float(1.4426950408889634 * mk.scale);
   prm.o = static_cast<__nv_bfloat16*>(o);
   prm.o_stride = o_stride;
   prm.lse = lse;
-  for (int c = 0; c < n_chunks; ++c) {
-    if (chunk_row[c] < 0 || int64_t(chunk_row[c]) + chunk_len > pool_rows)
-      return set_error(SP_ERR_INVALID, "sp_attn_fwd: chunk %d outside the pool", c);
-    prm.chunk_row[c] = chunk_row[c];
-  }
+  for (int c = 0; c < n_chunks; ++c) prm.chunk_row[c] = chunk_row[c];
   CUtensorMap tq, tk, tv;
   if (!make_tmap_bf16(&tq, q, uint64_t(q_stride), uint64_t(q_rows), uint64_t(q_stride), 128) ||
       !make_tmap_bf16(&tk, k_pool, uint64_t(kv_stride), uint64_t(pool_rows), uint64_t(kv_stride), 128) ||
       !make_tmap_bf16(&tv, v_pool, uint64_t(kv_stride), uint64_t(pool_rows), uint64_t(kv_stride), 128))
     return set_error(SP_ERR_CUDA, "sp_attn_fwd: cuTensorMapEncodeTiled failed (alignment?)");
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int q_tiles = int(q_rows / 128);
-  // d=128: attn_fwd_v4.cu (production); SP_ATTN_FWD_V3 / SP_ATTN_FWD_V1 select
-  // the earlier designs for A/B measurements
-  static const bool v1 = getenv("SP_ATTN_FWD_V1") != nullptr;
-  static const bool v3 = getenv("SP_ATTN_FWD_V3") != nullptr;
-  if (head_dim == 128 && !v1 && !v3)
-    return attn_fwd_d128_ps(q, q_rows, q_stride, k_pool, v_pool, pool_rows, kv_stride, chunk_row, n_chunks, chunk_len,
-                            heads, kv_heads, causal, o, o_stride, lse, st);
-  if (head_dim == 128 && !v1)
-    return attn_fwd_d128_pp(q, q_rows, q_stride, k_pool, v_pool, pool_rows, kv_stride, chunk_row, n_chunks, chunk_len,
-                            heads, kv_heads, causal, o, o_stride, lse, st);
-  if (head_dim == 128) return launch_fwd<128, 2>(tq, tk, tv, prm, q_tiles, heads, st);
-  return launch_fwd<64, 3>(tq, tk, tv, prm, q_tiles, heads, st);
+  return launch_fwd<64, 3>(tq, tk, tv, prm, int(q_rows / 128), heads, st);
+}
+
+}  // namespace
+}  // namespace sp
+
+extern "C" int sp_attn_fwd(const void* q, int64_t q_rows, int64_t q_stride, const void* k_pool, const void* v_pool,
+                           int64_t pool_rows, int64_t kv_stride, const int32_t* chunk_row, int n_chunks,
+                           int chunk_len, int heads, int kv_heads, int head_dim, int causal, void* o,
+                           int64_t o_stride, float* lse, sp_stream_t stream) {
+  using namespace sp;
+  const int64_t total_kv = int64_t(n_chunks) * chunk_len;
+  if (causal && total_kv < q_rows)
+    return set_error(SP_ERR_UNSUPPORTED, "sp_attn_fwd: causal needs total_kv >= q_rows");
+  FwdMask mk;
+  mk.causal = causal;
+  mk.causal_off = total_kv - q_rows;  // bottom-right aligned, reference attention.cpp:34-35
+  mk.kv_valid = total_kv;
+  mk.scale = head_dim > 0 ? 1.0 / sqrt(double(head_dim)) : 0.0;  // attention.cpp:31
+  return attn_fwd_dispatch(q, q_rows, q_stride, k_pool, v_pool, pool_rows, kv_stride, chunk_row, n_chunks, chunk_len,
+                           heads, kv_heads, head_dim, mk, o, o_stride, lse, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int sp_attn_fwd_masked(const void* q, int64_t q_rows, int64_t q_stride, const void* k_pool,
+                                  const void* v_pool, int64_t pool_rows, int64_t kv_stride, const int32_t* chunk_row,
+                                  int n_chunks, int chunk_len, int heads, int kv_heads, int head_dim, int causal,
+                                  int64_t causal_off, int64_t kv_valid, double scale, void* o, int64_t o_stride,
+                                  float* lse, float* row_max, sp_stream_t stream) {
+  using namespace sp;
+  FwdMask mk;
+  mk.causal = causal;
+  mk.causal_off = causal_off;
+  mk.kv_valid = kv_valid;
+  mk.scale = scale;
+  mk.row_max = row_max;
+  return attn_fwd_dispatch(q, q_rows, q_stride, k_pool, v_pool, pool_rows, kv_stride, chunk_row, n_chunks, chunk_len,
+                           heads, kv_heads, head_dim, mk, o, o_stride, lse, static_cast<cudaStream_t>(stream));
 }

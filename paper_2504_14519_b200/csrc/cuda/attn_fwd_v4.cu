@@ -17,7 +17,6 @@
 // streams: S in the order A0 B0 A1 B1 ..., and PV_A / PV_B.
 #include <math.h>
 
-#include <cstdlib>
 
 #include "errors.hpp"
 #include "kernels.hpp"
@@ -39,12 +38,13 @@ constexpr int kSlab = 128 * 64;  // elements of one [128 rows][64] SW128 slab
 
 struct Params {
   int q_rows, total_kv, chunk_len, group, causal;
+  int kv_valid;         // keys >= kv_valid are masked (padding)
+  int64_t causal_off;   // causal: query row r sees keys <= r + causal_off
   float scale_log2;
-  int trace;  // diagnostics: per-tile timeline of CTA (0,0) into g_ps_trace
-  int turns;  // MUFU turn-taking between the two tiles (named barriers); off by default
   __nv_bfloat16* o;
   int64_t o_stride;
   float* lse;
+  float* row_max;       // optional [heads][q_rows]: true row max of the scaled scores (natural log units)
   int chunk_row[SP_MAX_CHUNKS];
 };
 
@@ -61,28 +61,6 @@ struct Ctl {
   float red_l[2][2][BM];     // [tile][half][row]: partial row sum (epilogue)
 };
 
-// 2^x on the FMA pipe (see attn_fwd_v2.cu): used for a fixed fraction of the
-// exponentials so that MUFU (16/clk/SM) is not the only exp2 unit.
-__device__ __forceinline__ float poly_exp2(float x) {
-  x = fmaxf(x, -126.f);
-  const float t = x + 12582912.f;
-  const int j = __float_as_int(t) - 0x4B400000;
-  const float f = x - (t - 12582912.f);
-  float p = fmaf(0.0096181291f, f, 0.0555041087f);
-  p = fmaf(p, f, 0.2402264923f);
-  p = fmaf(p, f, 0.6931471806f);
-  p = fmaf(p, f, 1.0f);
-  return __int_as_float(__float_as_int(p) + (j << 23));
-}
-
-__device__ long long g_ps_trace[16][1024];
-#define TRP(e, j)                                                     \
-  do {                                                                \
-    if (tracing && (j) < 1024) g_ps_trace[e][(j)] = clock64();       \
-  } while (0)
-
-// kPolyMask: bit x (of 8) set = element x of every group of 8 uses poly_exp2.
-template <int kPolyMask>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_ps_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                        const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ Params prm) {
@@ -95,13 +73,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int kvh = head / prm.group;
   const int row0 = pair * 2 * BM;
   const bool has_b = row0 + BM < prm.q_rows;
-  auto n_tiles = [&](int r0) {
-    return prm.causal ? (prm.total_kv - prm.q_rows + r0 + BM) / BN : prm.total_kv / BN;
+  auto n_tiles = [&](int r0) {  // KV tiles holding a key visible to some row of [r0, r0 + BM)
+    int64_t kmax = prm.kv_valid - 1;
+    if (prm.causal) kmax = min(kmax, int64_t(r0) + BM - 1 + prm.causal_off);
+    return kmax < 0 ? 0 : int(kmax / BN + 1);
   };
   const int n_a = n_tiles(row0);
   const int n_b = has_b ? n_tiles(row0 + BM) : 0;
   const int n = n_a > n_b ? n_a : n_b;  // K/V tiles the CTA streams
-  bool tracing = prm.trace && blockIdx.x == 0 && blockIdx.y == 0;
 
   if (warp == kProducerWarp && lane == 0) {
     tma_prefetch(&tm_q);
@@ -183,7 +162,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (k > 0) mbar_wait(&ctl.s_free, (k - 1) & 1);
         mbar_wait(&ctl.k_full[j % NK], (j / NK) & 1);
         tc_fence_after();
-        TRP(0, k);
         umma_bf16_ss_k128(tmem, smem_desc_sw128(smem_u32(sm.q[x]), 16, 1024),
                           smem_desc_sw128(smem_u32(sm.k[j % NK]), 16, 1024), id_s, 0u);
         umma_commit_warp(&ctl.s_full[x]);
@@ -197,7 +175,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (j >= (x ? n_b : n_a)) continue;
           mbar_wait(&ctl.p_full[x], j & 1);
           tc_fence_after();
-          TRP(2 + x, j);
           // keys [16kk, +16): P_X of half kk/4 at cols 128 + 64x + 32(kk/4) + 8(kk%4)
           umma_bf16_ts_k128(tmem + 256 + x * 128, tmem + 128 + x * 64, 32,
                             smem_desc_sw128(smem_u32(sm.v[j % NV]), kSlab * 2, 1024), id_o, j > 0 ? 1u : 0u);
@@ -220,13 +197,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t p_col = tmem + 128 + x * 64 + h * 32 + lane_off;  // own P
     const uint32_t o_col = tmem + 256 + x * 128 + h * 64 + lane_off;
     const float sl2 = prm.scale_log2;
-    float m_used = -INFINITY, l = 0.f;
-    tracing = tracing && (warp == 0 || warp == 8) && lane == 0;
+    float m_used = -INFINITY, l = 0.f, m_true = -INFINITY;
+    // last visible key of this thread's row, relative to its key half
+    const int64_t qlim = prm.causal ? min(int64_t(prm.kv_valid) - 1, int64_t(row0 + x * BM + r) + prm.causal_off)
+                                    : int64_t(prm.kv_valid) - 1;
     for (int j = 0; j < nt; ++j) {
       mbar_wait(&ctl.s_full[x], j & 1);
-      TRP(8 + 4 * x, j);
       tc_fence_after();
-      const bool diag = prm.causal && j == nt - 1;  // key column c visible iff c <= r
+      const int64_t lim = qlim - int64_t(j) * BN - h * 64;  // columns e > lim of this half are masked
       // S row half -> registers once (both loads in flight together)
       float sv[64];
       tmem_ld32(s_col, *reinterpret_cast<float(*)[32]>(&sv[0]));
@@ -234,10 +212,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(&ctl.s_free);  // S buffer may take the next tile's scores
-      if (diag) {
+      if (lim < 63) {  // the diagonal tile (or padding): per-element mask
+        const int lm = lim < -1 ? -1 : int(lim);
 #pragma unroll
         for (int e = 0; e < 64; ++e)
-          if (h * 64 + e > r) sv[e] = -INFINITY;
+          if (e > lm) sv[e] = -INFINITY;
       }
       float m8[8];
 #pragma unroll
@@ -253,7 +232,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       ctl.red_m[x][j & 1][h][r] = mh;
       named_bar_sync(1 + x, 256);
       const float mx = fmaxf(mh, ctl.red_m[x][j & 1][h ^ 1][r]);
-      TRP(9 + 4 * x, j);
+      m_true = fmaxf(m_true, mx);
       const float cand = mx * sl2;
       const bool grow = cand > m_used + 8.0f;  // identical decision in both halves
       float corr = 1.f;
@@ -283,10 +262,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_st16(o_col + c * 16, ow);
         }
       }
-      // MUFU turn: A(j), B(j), A(j+1), ... (named barrier 3 hands the turn to
-      // A, 4 to B; bar.arrive by the 256 giving threads, bar.sync by the 256
-      // taking ones)
-      if (prm.turns && (x == 0 ? (j >= 1 && j - 1 < n_b) : (j < n_a))) named_bar_sync(3 + x, 512);
       float2 rs[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
       const float2 sl2x2 = make_float2(sl2, sl2), nmx2 = make_float2(-msub, -msub);
       // exponentials from registers; bf16 P_X (keys [64h+16q, +16) -> columns
@@ -298,21 +273,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int e = 0; e < 8; ++e) {
           const int i = q * 16 + 2 * e;
           const float2 xx = ffma2(make_float2(sv[i], sv[i + 1]), sl2x2, nmx2);
-          const float a = ((kPolyMask >> (i & 7)) & 1) ? poly_exp2(xx.x) : fast_exp2(xx.x);
-          const float b = ((kPolyMask >> ((i + 1) & 7)) & 1) ? poly_exp2(xx.y) : fast_exp2(xx.y);
+          const float a = fast_exp2(xx.x);
+          const float b = fast_exp2(xx.y);
           rs[e & 3] = fadd2(rs[e & 3], make_float2(a, b));
           pk[e] = pack_bf16(a, b);
         }
         tmem_st8(p_col + q * 8, pk);
       }
-      if (prm.turns && (x == 0 ? (j < n_b) : (j + 1 < n_a))) named_bar_arrive(4 - x, 512);
-      TRP(10 + 4 * x, j);
       const float2 rr = fadd2(fadd2(rs[0], rs[1]), fadd2(rs[2], rs[3]));
       l = l * corr + (rr.x + rr.y);
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&ctl.p_full[x]);
-      TRP(11 + 4 * x, j);
     }
     // ------------------------------------------------------------- epilogue
     ctl.red_l[x][h][r] = l;
@@ -344,9 +316,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                                pack_bf16(ov[8 * q4 + 4] * inv, ov[8 * q4 + 5] * inv),
                                pack_bf16(ov[8 * q4 + 6] * inv, ov[8 * q4 + 7] * inv));
       }
-      if (h == 0)
+      if (h == 0) {
         prm.lse[int64_t(head) * prm.q_rows + qrow] =
             lt > 0.f ? (m_used + __log2f(lt)) * 0.69314718055994530942f : -INFINITY;
+        if (prm.row_max)
+          prm.row_max[int64_t(head) * prm.q_rows + qrow] =
+              lt > 0.f ? m_true * prm.scale_log2 * 0.69314718055994530942f : -INFINITY;
+      }
     }
     tc_fence_before();
   }
@@ -361,19 +337,21 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 int attn_fwd_d128_ps(const void* q, int64_t q_rows, int64_t q_stride, const void* k_pool, const void* v_pool,
                      int64_t pool_rows, int64_t kv_stride, const int32_t* chunk_row, int n_chunks, int chunk_len,
-                     int heads, int kv_heads, int causal, void* o, int64_t o_stride, float* lse, cudaStream_t st) {
+                     int heads, int kv_heads, const FwdMask& mk, void* o, int64_t o_stride, float* lse,
+                     cudaStream_t st) {
   Params prm{};
   prm.q_rows = int(q_rows);
   prm.total_kv = n_chunks * chunk_len;
   prm.chunk_len = chunk_len;
   prm.group = heads / kv_heads;
-  prm.causal = causal;
-  prm.scale_log2 = float(1.4426950408889634 / sqrt(double(D)));
-  prm.trace = getenv("SP_FWD_TRACE") != nullptr;
-  prm.turns = getenv("SP_FWD_TURNS") ? 1 : 0;  // measured: concurrent exponentials of both tiles win
+  prm.causal = mk.causal;
+  prm.kv_valid = int(mk.kv_valid);
+  prm.causal_off = mk.causal_off;
+  prm.scale_log2 = float(1.4426950408889634 * mk.scale);
   prm.o = static_cast<__nv_bfloat16*>(o);
   prm.o_stride = o_stride;
   prm.lse = lse;
+  prm.row_max = mk.row_max;
   for (int c = 0; c < n_chunks; ++c) prm.chunk_row[c] = chunk_row[c];
   CUtensorMap tq, tk, tv;
   if (!make_tmap_bf16(&tq, q, uint64_t(q_stride), uint64_t(q_rows), uint64_t(q_stride), BM) ||
@@ -381,20 +359,12 @@ int attn_fwd_d128_ps(const void* q, int64_t q_rows, int64_t q_stride, const void
       !make_tmap_bf16(&tv, v_pool, uint64_t(kv_stride), uint64_t(pool_rows), uint64_t(kv_stride), BN))
     return set_error(SP_ERR_CUDA, "attn_fwd_d128_ps: cuTensorMapEncodeTiled failed (alignment?)");
   const size_t smem = sizeof(Smem) + 1024;
-  // kPolyMask > 0 (some exponentials on the FMA pipe) measured slower on B200
-  auto kern = attn_fwd_ps_kernel<0>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  if (e != cudaSuccess) return cuda_status(e, "attn_fwd_d128_ps: set smem");
+  if (int rc = set_smem_once(reinterpret_cast<const void*>(attn_fwd_ps_kernel), smem, "attn_fwd_d128_ps: set smem"))
+    return rc;
   const unsigned pairs = unsigned((q_rows + 2 * BM - 1) / (2 * BM));
-  kern<<<dim3(pairs, heads), kThreads, smem, st>>>(tq, tk, tv, prm);
+  attn_fwd_ps_kernel<<<dim3(pairs, heads), kThreads, smem, st>>>(tq, tk, tv, prm);
   count_launch(1);
   return cuda_status(cudaGetLastError(), "attn_fwd_d128_ps launch");
 }
 
-int ps_trace_copy(long long* out) {
-  return cuda_status(cudaMemcpyFromSymbol(out, g_ps_trace, sizeof(long long) * 16 * 1024), "trace copy");
-}
-
 }  // namespace sp
-
-extern "C" int sp_debug_ps_trace(long long* out) { return sp::ps_trace_copy(out); }

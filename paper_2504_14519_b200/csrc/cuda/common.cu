@@ -6,6 +6,8 @@
 #include <cstdarg>
 #include <cstdio>
 #include <mutex>
+#include <set>
+#include <utility>
 
 #include "errors.hpp"
 #include "slimpipe.h"
@@ -34,6 +36,19 @@ int set_error(int code, const char* fmt, ...) {
 int cuda_status(cudaError_t e, const char* what) {
   if (e == cudaSuccess) return SP_OK;
   return set_error(SP_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+int set_smem_once(const void* fn, size_t smem, const char* what) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  if (cudaError_t e = cudaGetDevice(&dev)) return cuda_status(e, what);
+  std::lock_guard<std::mutex> g(mu);
+  if (done.count({fn, dev})) return SP_OK;
+  if (cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)))
+    return cuda_status(e, what);
+  done.insert({fn, dev});
+  return SP_OK;
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {

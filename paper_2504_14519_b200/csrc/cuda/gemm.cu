@@ -24,7 +24,9 @@ using Key = std::tuple<int, bool, bool, int64_t, int64_t, int64_t, int64_t, int6
 
 struct State {
   cublasLtHandle_t lt = nullptr;
-  void* ws = nullptr;
+  // one workspace per (device, stream): GEMMs on different streams (the
+  // vocabulary stream, loopback ranks) never share scratch memory
+  std::map<std::pair<int, cudaStream_t>, void*> ws;
   size_t ws_bytes = 64ull << 20;
   std::map<Key, Plan> plans;
   std::mutex mu;
@@ -49,10 +51,11 @@ int gemm(bool trans_a, bool trans_b, int64_t M, int64_t N, int64_t K, const void
   std::lock_guard<std::mutex> g(S.mu);
   int dev = 0;
   cudaGetDevice(&dev);
-  if (!S.lt) {
+  if (!S.lt)
     if (int rc = lt_status(cublasLtCreate(&S.lt), "create")) return rc;
-    if (int rc = cuda_status(cudaMalloc(&S.ws, S.ws_bytes), "gemm workspace")) return rc;
-  }
+  void*& ws = S.ws[{dev, st}];
+  if (!ws)
+    if (int rc = cuda_status(cudaMalloc(&ws, S.ws_bytes), "gemm workspace")) return rc;
   const Key key{dev, trans_a, trans_b, M, N, K, lda, ldb, ldc, c_f32};
   auto it = S.plans.find(key);
   if (it == S.plans.end()) {
@@ -82,7 +85,7 @@ int gemm(bool trans_a, bool trans_b, int64_t M, int64_t N, int64_t K, const void
   }
   const Plan& p = it->second;
   count_library_launch();
-  return lt_status(cublasLtMatmul(S.lt, p.op, &alpha, B, p.a, A, p.b, &beta, C, p.c, C, p.c, &p.algo, S.ws,
+  return lt_status(cublasLtMatmul(S.lt, p.op, &alpha, B, p.a, A, p.b, &beta, C, p.c, C, p.c, &p.algo, ws,
                                   S.ws_bytes, st),
                    "matmul");
 }

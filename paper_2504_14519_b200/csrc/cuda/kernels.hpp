@@ -43,13 +43,24 @@ int xent_shard_grad(const float* logits, const int32_t* tgt, int64_t rows, int V
                     const float* zt, float scale, void* dlogits, float* loss_sum, cudaStream_t st);
 int add_f32(float* dst, const float* src, int64_t n, cudaStream_t st);  // dst += src
 
-// attn_fwd_v2.cu — two-tile, P-in-TMEM d=128 forward (q_rows % 256 == 0)
-int attn_fwd_d128_pp(const void* q, int64_t q_rows, int64_t q_stride, const void* k_pool, const void* v_pool,
-                  int64_t pool_rows, int64_t kv_stride, const int32_t* chunk_row, int n_chunks, int chunk_len,
-                  int heads, int kv_heads, int causal, void* o, int64_t o_stride, float* lse, cudaStream_t st);
+// K1 masking / output options (sp_attn_fwd: causal_off = total - q_rows,
+// kv_valid = total, scale = 1/sqrt(d), no row_max).
+struct FwdMask {
+  int causal = 1;
+  int64_t causal_off = 0;  // causal: query row r sees keys <= r + causal_off
+  int64_t kv_valid = 0;    // keys >= kv_valid (padding) are masked
+  double scale = 0.0;      // softmax scale
+  float* row_max = nullptr;  // optional fp32 [heads][q_rows]: true row max of the scaled scores
+};
+
+// attn_fwd_v4.cu — d=128 forward (two 128-row tiles per CTA, shared S buffer)
 int attn_fwd_d128_ps(const void* q, int64_t q_rows, int64_t q_stride, const void* k_pool, const void* v_pool,
-                  int64_t pool_rows, int64_t kv_stride, const int32_t* chunk_row, int n_chunks, int chunk_len,
-                  int heads, int kv_heads, int causal, void* o, int64_t o_stride, float* lse, cudaStream_t st);
+                     int64_t pool_rows, int64_t kv_stride, const int32_t* chunk_row, int n_chunks, int chunk_len,
+                     int heads, int kv_heads, const FwdMask& mk, void* o, int64_t o_stride, float* lse,
+                     cudaStream_t st);
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize once per (kernel, device)
+int set_smem_once(const void* fn, size_t smem, const char* what);
 
 // attn_bwd_v2.cu — pipelined d=128 backward (lse2/delta prepared by the caller)
 int attn_bwd_d128(const void* q, int64_t q_rows, int64_t q_stride, const void* k_pool, const void* v_pool,

@@ -1,0 +1,320 @@
+// Transports behind sp::Link (csrc/host/transport.hpp): NCCL for one process
+// per GPU, and the single-GPU loopback that runs every rank as a host thread
+// of one process (tests and single-GPU boxes).
+#include <cuda.h>
+
+#include <algorithm>
+#include <atomic>
+#include <memory>
+#include <mutex>
+#include <vector>
+
+#include "kernels.hpp"
+#include "transport.hpp"
+
+namespace sp {
+
+int Link::broadcast(void*, int64_t, ncclDataType_t, int, cudaStream_t) {
+  return set_error(SP_ERR_UNSUPPORTED, "transport: collectives are not available on this link");
+}
+int Link::all_reduce(float*, int64_t, ncclRedOp_t, cudaStream_t) {
+  return set_error(SP_ERR_UNSUPPORTED, "transport: collectives are not available on this link");
+}
+int Link::reduce(float*, int64_t, int, cudaStream_t) {
+  return set_error(SP_ERR_UNSUPPORTED, "transport: collectives are not available on this link");
+}
+
+namespace {
+
+int nccl_rc(ncclResult_t r, const char* what) {
+  if (r == ncclSuccess) return SP_OK;
+  return set_error(SP_ERR_NCCL, "%s: %s", what, ncclGetErrorString(r));
+}
+
+class NcclLink final : public Link {
+ public:
+  explicit NcclLink(ncclComm_t c) : c_(c) {}
+  ~NcclLink() override {
+    if (c_) ncclCommDestroy(c_);
+  }
+  int send(const void* buf, int64_t count, ncclDataType_t dt, int peer, cudaStream_t st) override {
+    return nccl_rc(ncclSend(buf, size_t(count), dt, peer, c_, st), "ncclSend");
+  }
+  int recv(void* buf, int64_t count, ncclDataType_t dt, int peer, cudaStream_t st) override {
+    return nccl_rc(ncclRecv(buf, size_t(count), dt, peer, c_, st), "ncclRecv");
+  }
+  int group_start() override { return nccl_rc(ncclGroupStart(), "ncclGroupStart"); }
+  int group_end() override { return nccl_rc(ncclGroupEnd(), "ncclGroupEnd"); }
+  int broadcast(void* buf, int64_t count, ncclDataType_t dt, int root, cudaStream_t st) override {
+    return nccl_rc(ncclBroadcast(buf, buf, size_t(count), dt, root, c_, st), "ncclBroadcast");
+  }
+  int all_reduce(float* buf, int64_t count, ncclRedOp_t op, cudaStream_t st) override {
+    return nccl_rc(ncclAllReduce(buf, buf, size_t(count), ncclFloat32, op, c_, st), "ncclAllReduce");
+  }
+  int reduce(float* buf, int64_t count, int root, cudaStream_t st) override {
+    return nccl_rc(ncclReduce(buf, buf, size_t(count), ncclFloat32, ncclSum, root, c_, st), "ncclReduce");
+  }
+
+ private:
+  ncclComm_t c_;
+};
+
+// ------------------------------------------------------------------ loopback
+using WaitFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+using WriteFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+struct MemOps {
+  WaitFn wait = nullptr;
+  WriteFn write = nullptr;
+};
+
+const MemOps& memops() {
+  static MemOps m;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      m.wait = reinterpret_cast<WaitFn>(p);
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      m.write = reinterpret_cast<WriteFn>(p);
+  });
+  return m;
+}
+
+constexpr int kSlots = 4096;  // messages in flight per (communicator, sender, receiver)
+constexpr int kComms = 8;
+
+struct Mail {
+  void* dst;
+  int64_t bytes;
+};
+
+struct Channel {
+  uint32_t* ready = nullptr;  // device [kSlots]: seq+1 once receive `seq` is posted
+  uint32_t* done = nullptr;   // device [kSlots]: seq+1 once send `seq` landed
+  Mail* mail = nullptr;       // pinned, device-mapped [kSlots]: receive destinations
+  std::atomic<uint64_t> sseq{0}, rseq{0};
+};
+
+// The sender's copy: destination and size come from the receiver's mailbox
+// (published before the ready flag the sender's stream waited on).
+__global__ void loop_copy_kernel(const Mail* mail, const uint8_t* __restrict__ src, int64_t bytes, int* err) {
+  const volatile Mail* vm = mail;
+  uint8_t* dst = static_cast<uint8_t*>(vm->dst);
+  if (vm->bytes != bytes) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) atomicAdd(err, 1);
+    return;
+  }
+  const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x, nth = int64_t(gridDim.x) * blockDim.x;
+  if (((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0) {
+    const int64_t n16 = bytes >> 4;
+    const int4* s = reinterpret_cast<const int4*>(src);
+    int4* d = reinterpret_cast<int4*>(dst);
+    for (int64_t x = tid; x < n16; x += nth) d[x] = s[x];
+    for (int64_t x = (n16 << 4) + tid; x < bytes; x += nth) dst[x] = src[x];
+  } else {
+    for (int64_t x = tid; x < bytes; x += nth) dst[x] = src[x];
+  }
+}
+
+}  // namespace
+
+struct LoopWorld {
+  int n = 0;
+  std::vector<std::unique_ptr<Channel>> ch;  // [comm][src][dst]
+  uint32_t* flags = nullptr;
+  Mail* mail = nullptr;
+  int* err = nullptr;
+  Channel& at(int comm, int src, int dst) { return *ch[size_t((comm * n + src) * n + dst)]; }
+};
+
+LoopWorld* loop_world_create(int ranks) {
+  const MemOps& m = memops();
+  if (!m.wait || !m.write || ranks < 1) return nullptr;
+  auto w = std::make_unique<LoopWorld>();
+  w->n = ranks;
+  const size_t nch = size_t(kComms) * ranks * ranks;
+  if (cudaMalloc(&w->flags, nch * 2 * kSlots * sizeof(uint32_t)) != cudaSuccess) return nullptr;
+  if (cudaMemset(w->flags, 0, nch * 2 * kSlots * sizeof(uint32_t)) != cudaSuccess) return nullptr;
+  if (cudaHostAlloc(reinterpret_cast<void**>(&w->mail), nch * kSlots * sizeof(Mail),
+                    cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess)
+    return nullptr;
+  if (cudaMalloc(&w->err, sizeof(int)) != cudaSuccess || cudaMemset(w->err, 0, sizeof(int)) != cudaSuccess)
+    return nullptr;
+  for (size_t x = 0; x < nch; ++x) {
+    auto c = std::make_unique<Channel>();
+    c->ready = w->flags + x * 2 * kSlots;
+    c->done = c->ready + kSlots;
+    c->mail = w->mail + x * kSlots;
+    w->ch.push_back(std::move(c));
+  }
+  if (cudaDeviceSynchronize() != cudaSuccess) return nullptr;
+  return w.release();
+}
+
+void loop_world_destroy(LoopWorld* w) {
+  if (!w) return;
+  cudaDeviceSynchronize();
+  cudaFree(w->flags);
+  cudaFree(w->err);
+  cudaFreeHost(w->mail);
+  delete w;
+}
+
+int loop_world_size(const LoopWorld* w) { return w ? w->n : 0; }
+
+int loop_world_errors(const LoopWorld* w) {
+  int e = 0;
+  if (w) cudaMemcpy(&e, w->err, sizeof e, cudaMemcpyDeviceToHost);
+  return e;
+}
+
+namespace {
+
+int dt_bytes(ncclDataType_t dt) {
+  switch (dt) {
+    case ncclInt8: case ncclUint8: return 1;
+    case ncclFloat16: case ncclBfloat16: return 2;
+    case ncclInt32: case ncclUint32: case ncclFloat32: return 4;
+    default: return 8;
+  }
+}
+
+class LoopLink final : public Link {
+ public:
+  LoopLink(LoopWorld* w, int id, std::vector<int> members, int me) : w_(w), id_(id), mem_(std::move(members)), me_(me) {}
+
+  int send(const void* buf, int64_t count, ncclDataType_t dt, int peer, cudaStream_t st) override {
+    if (grouping_) {
+      ops_.push_back({true, buf, nullptr, count * dt_bytes(dt), peer, st});
+      return SP_OK;
+    }
+    return do_send(buf, count * dt_bytes(dt), peer, st);
+  }
+  int recv(void* buf, int64_t count, ncclDataType_t dt, int peer, cudaStream_t st) override {
+    if (grouping_) {
+      ops_.push_back({false, nullptr, buf, count * dt_bytes(dt), peer, st});
+      return SP_OK;
+    }
+    uint64_t seq = 0;
+    if (int rc = post(buf, count * dt_bytes(dt), peer, st, &seq)) return rc;
+    return wait_done(peer, seq, st);
+  }
+  int group_start() override {
+    grouping_ = true;
+    return SP_OK;
+  }
+  // Receives are posted first, then the sends run, then the receives wait:
+  // a group never waits on its own later members.
+  int group_end() override {
+    grouping_ = false;
+    std::vector<uint64_t> seqs(ops_.size());
+    for (size_t x = 0; x < ops_.size(); ++x)
+      if (!ops_[x].is_send)
+        if (int rc = post(ops_[x].rbuf, ops_[x].bytes, ops_[x].peer, ops_[x].st, &seqs[x])) return clear(rc);
+    for (const Op& o : ops_)
+      if (o.is_send)
+        if (int rc = do_send(o.sbuf, o.bytes, o.peer, o.st)) return clear(rc);
+    for (size_t x = 0; x < ops_.size(); ++x)
+      if (!ops_[x].is_send)
+        if (int rc = wait_done(ops_[x].peer, seqs[x], ops_[x].st)) return clear(rc);
+    return clear(SP_OK);
+  }
+
+ private:
+  struct Op {
+    bool is_send;
+    const void* sbuf;
+    void* rbuf;
+    int64_t bytes;
+    int peer;
+    cudaStream_t st;
+  };
+  int clear(int rc) {
+    ops_.clear();
+    return rc;
+  }
+  Channel& chan(int src_local, int dst_local) { return w_->at(id_, mem_[size_t(src_local)], mem_[size_t(dst_local)]); }
+
+  static int mem_rc(CUresult r, const char* what) {
+    return r == CUDA_SUCCESS ? SP_OK : set_error(SP_ERR_CUDA, "loopback %s failed (CUresult %d)", what, int(r));
+  }
+
+  int post(void* buf, int64_t bytes, int peer, cudaStream_t st, uint64_t* seq_out) {
+    Channel& c = chan(peer, me_);
+    const uint64_t seq = c.rseq++;
+    const int slot = int(seq % kSlots);
+    c.mail[slot].dst = buf;
+    c.mail[slot].bytes = bytes;
+    *seq_out = seq;
+    return mem_rc(memops().write(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(c.ready + slot),
+                                 cuuint32_t(seq + 1), CU_STREAM_WRITE_VALUE_DEFAULT),
+                  "write(ready)");
+  }
+  int wait_done(int peer, uint64_t seq, cudaStream_t st) {
+    Channel& c = chan(peer, me_);
+    return mem_rc(memops().wait(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(c.done + seq % kSlots),
+                                cuuint32_t(seq + 1), CU_STREAM_WAIT_VALUE_GEQ),
+                  "wait(done)");
+  }
+  int do_send(const void* buf, int64_t bytes, int peer, cudaStream_t st) {
+    Channel& c = chan(me_, peer);
+    const uint64_t seq = c.sseq++;
+    const int slot = int(seq % kSlots);
+    if (int rc = mem_rc(memops().wait(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(c.ready + slot),
+                                      cuuint32_t(seq + 1), CU_STREAM_WAIT_VALUE_GEQ),
+                        "wait(ready)"))
+      return rc;
+    if (bytes > 0) {
+      const int blocks = int(std::min<int64_t>(296, (bytes / 16 + 255) / 256 + 1));
+      loop_copy_kernel<<<blocks, 256, 0, st>>>(c.mail + slot, static_cast<const uint8_t*>(buf), bytes, w_->err);
+      count_launch();
+      if (int rc = cuda_status(cudaGetLastError(), "loopback copy")) return rc;
+    }
+    return mem_rc(memops().write(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(c.done + slot),
+                                 cuuint32_t(seq + 1), CU_STREAM_WRITE_VALUE_DEFAULT),
+                  "write(done)");
+  }
+
+  LoopWorld* w_;
+  int id_;
+  std::vector<int> mem_;
+  int me_;
+  bool grouping_ = false;
+  std::vector<Op> ops_;
+};
+
+}  // namespace
+
+std::unique_ptr<Link> make_nccl_link(ncclComm_t comm) { return std::make_unique<NcclLink>(comm); }
+
+std::unique_ptr<Link> make_loop_link(LoopWorld* w, int comm_id, std::vector<int> members, int me) {
+  if (!w || comm_id < 0 || comm_id >= kComms) return nullptr;
+  for (int m : members)
+    if (m < 0 || m >= w->n) return nullptr;
+  return std::make_unique<LoopLink>(w, comm_id, std::move(members), me);
+}
+
+}  // namespace sp
+
+extern "C" {
+
+int sp_loopback_create(int ranks, void** world) {
+  sp::LoopWorld* w = sp::loop_world_create(ranks);
+  if (!w)
+    return sp::set_error(SP_ERR_CUDA, "loopback world: stream memory operations or allocation unavailable");
+  *world = w;
+  return SP_OK;
+}
+
+int sp_loopback_destroy(void* world) {
+  sp::loop_world_destroy(static_cast<sp::LoopWorld*>(world));
+  return SP_OK;
+}
+
+int sp_loopback_errors(void* world) { return sp::loop_world_errors(static_cast<sp::LoopWorld*>(world)); }
+
+}  // extern "C"

@@ -48,65 +48,63 @@ struct DevBuf {  // RAII device allocation
   DevBuf& operator=(const DevBuf&) = delete;
 };
 
-void check_head_dim(int d) {
-  if (d != 64 && d != 128) throw std::invalid_argument("chunked attention (B200): head_dim must be 64 or 128");
-}
-
-// One K1 launch: query [rows][d] over `chunks` (keys concatenated in order),
-// bottom-right causal over their total when `causal`.  Returns the state
-// (O normalised, row_max = LSE, row_sumexp = 1; fully masked rows empty).
-AttnChunkState run_k1(const Mat& q, const std::vector<const KvChunk*>& chunks, bool causal) {
+// One K1 launch (sp_attn_fwd_masked) for a single head: query [rows][d] over
+// `chunks` (keys concatenated in order, key/value widths d / dv <= 128).
+// Rows, keys and both widths are zero-padded to the kernel tiles (128 rows /
+// keys, 64 or 128 columns); the padded keys are masked (kv_valid), the
+// softmax scale is the reference's 1/sqrt(d) (attention.cpp:31) and, when
+// `causal`, row r sees concatenated keys <= r + causal_off.  Returns the
+// reference state (attention.cpp:13-19 semantics): unnormalised partial
+// output, the true row max of the scaled scores, and the row sum of
+// exponentials relative to it; rows that see no key stay empty (-inf, 0).
+AttnChunkState run_k1(const Mat& q, const std::vector<const KvChunk*>& chunks, bool causal, int64_t causal_off) {
   const int rows = q.rows, d = q.cols;
-  check_head_dim(d);
-  if (rows % 128) throw std::invalid_argument("chunked attention (B200): query rows must be a multiple of 128");
+  const int dv = chunks.empty() ? d : chunks.front()->values.cols;
   int64_t total = 0;
-  bool equal = true;
-  for (const KvChunk* c : chunks) {
-    if (c->keys.rows != c->values.rows) throw std::invalid_argument("chunk_attention: key/value row mismatch");
-    if (c->keys.cols != d || c->values.cols != d) throw std::invalid_argument("chunk_attention: head_dim mismatch");
-    if (c->keys.rows % 128) throw std::invalid_argument("chunked attention (B200): chunk length must be a multiple of 128");
-    equal = equal && c->keys.rows == chunks.front()->keys.rows;
-    total += c->keys.rows;
-  }
-  AttnChunkState st = empty_state(rows, d);
+  for (const KvChunk* c : chunks) total += c->keys.rows;
+  AttnChunkState st = empty_state(rows, dv);
   if (total == 0 || rows == 0) return st;
-  if (causal && total < rows) throw std::invalid_argument("chunked attention (B200): causal needs total_kv >= rows");
-  // chunk table: the given chunks when equal-length, else 128-row pieces
-  const int chunk_len = equal ? chunks.front()->keys.rows : 128;
-  const int64_t n_tab = total / chunk_len;
-  if (n_tab > SP_MAX_CHUNKS) throw std::invalid_argument("chunked attention (B200): too many chunks");
-  std::vector<int32_t> chunk_row(static_cast<size_t>(n_tab));
-  for (int64_t c = 0; c < n_tab; ++c) chunk_row[size_t(c)] = int32_t(c * chunk_len);
-
-  std::vector<uint16_t> hq(size_t(rows) * d), hk(size_t(total) * d), hv(size_t(total) * d);
-  for (size_t x = 0; x < hq.size(); ++x) hq[x] = to_bf16(q.a[x]);
-  size_t off = 0;
-  for (const KvChunk* c : chunks) {
-    for (size_t x = 0; x < c->keys.a.size(); ++x) {
-      hk[off + x] = to_bf16(c->keys.a[x]);
-      hv[off + x] = to_bf16(c->values.a[x]);
+  if (d > 128 || dv > 128)
+    throw std::invalid_argument("chunked attention (B200): head_dim above 128 is not implemented by K1");
+  const int dp = (d <= 64 && dv <= 64) ? 64 : 128;
+  const int64_t rows_p = (rows + 127) / 128 * 128, total_p = (total + 127) / 128 * 128;
+  if (total_p > (int64_t(1) << 30)) throw std::invalid_argument("chunked attention (B200): too many keys");
+  std::vector<uint16_t> hq(size_t(rows_p) * dp, 0), hk(size_t(total_p) * dp, 0), hv(size_t(total_p) * dp, 0);
+  for (int r = 0; r < rows; ++r)
+    for (int c = 0; c < d; ++c) hq[size_t(r) * dp + c] = to_bf16(q.at(r, c));
+  int64_t pos = 0;
+  for (const KvChunk* ch : chunks) {
+    for (int r = 0; r < ch->keys.rows; ++r) {
+      for (int c = 0; c < d; ++c) hk[size_t(pos + r) * dp + c] = to_bf16(ch->keys.at(r, c));
+      for (int c = 0; c < dv; ++c) hv[size_t(pos + r) * dp + c] = to_bf16(ch->values.at(r, c));
     }
-    off += c->keys.a.size();
+    pos += ch->keys.rows;
   }
-  DevBuf dq(hq.size() * 2), dk(hk.size() * 2), dv(hv.size() * 2), dout(hq.size() * 2), dlse(size_t(rows) * 4);
+  DevBuf dq(hq.size() * 2), dk(hk.size() * 2), dvb(hv.size() * 2), dout(hq.size() * 2), dlse(size_t(rows_p) * 4),
+      dmax(size_t(rows_p) * 4);
   cuda_check(cudaMemcpy(dq.p, hq.data(), hq.size() * 2, cudaMemcpyHostToDevice), "copy q");
   cuda_check(cudaMemcpy(dk.p, hk.data(), hk.size() * 2, cudaMemcpyHostToDevice), "copy k");
-  cuda_check(cudaMemcpy(dv.p, hv.data(), hv.size() * 2, cudaMemcpyHostToDevice), "copy v");
-  const int rc = sp_attn_fwd(dq.p, rows, d, dk.p, dv.p, total, d, chunk_row.data(), int(n_tab), chunk_len, 1, 1, d,
-                             causal ? 1 : 0, dout.p, d, static_cast<float*>(dlse.p), nullptr);
+  cuda_check(cudaMemcpy(dvb.p, hv.data(), hv.size() * 2, cudaMemcpyHostToDevice), "copy v");
+  const int32_t chunk_row = 0;
+  const int rc = sp_attn_fwd_masked(dq.p, rows_p, dp, dk.p, dvb.p, total_p, dp, &chunk_row, 1, int(total_p), 1, 1, dp,
+                                    causal ? 1 : 0, causal_off, total, 1.0 / std::sqrt(double(d)), dout.p, dp,
+                                    static_cast<float*>(dlse.p), static_cast<float*>(dmax.p), nullptr);
   if (rc != SP_OK) {
     if (rc == SP_ERR_INVALID) throw std::invalid_argument(sp_last_error());
     throw std::runtime_error(sp_last_error());
   }
   std::vector<uint16_t> ho(hq.size());
-  std::vector<float> hl(static_cast<size_t>(rows));
+  std::vector<float> hl(static_cast<size_t>(rows_p)), hm(static_cast<size_t>(rows_p));
   cuda_check(cudaMemcpy(ho.data(), dout.p, ho.size() * 2, cudaMemcpyDeviceToHost), "copy o");
   cuda_check(cudaMemcpy(hl.data(), dlse.p, hl.size() * 4, cudaMemcpyDeviceToHost), "copy lse");
+  cuda_check(cudaMemcpy(hm.data(), dmax.p, hm.size() * 4, cudaMemcpyDeviceToHost), "copy row max");
   for (int r = 0; r < rows; ++r) {
-    if (std::isinf(hl[size_t(r)]) && hl[size_t(r)] < 0) continue;  // fully masked: stays empty
-    st.row_max[size_t(r)] = hl[size_t(r)];
-    st.row_sumexp[size_t(r)] = 1.0;
-    for (int c = 0; c < d; ++c) st.partial_output.at(r, c) = from_bf16(ho[size_t(r) * d + c]);
+    const double lse = hl[size_t(r)], m = hm[size_t(r)];
+    if (std::isinf(lse) || std::isinf(m)) continue;  // the row sees no key: stays empty
+    const double l = std::exp(lse - m);              // sum of exp(s - m), >= 1
+    st.row_max[size_t(r)] = m;
+    st.row_sumexp[size_t(r)] = l;
+    for (int c = 0; c < dv; ++c) st.partial_output.at(r, c) = from_bf16(ho[size_t(r) * dp + c]) * l;
   }
   return st;
 }
@@ -122,23 +120,16 @@ AttnChunkState empty_state(int rows, int head_dim) {
   return st;
 }
 
-// attention.cpp:21-61 — the two visibility cases of the sliced schedule
+// attention.cpp:21-61: one chunk at global key position chunk_pos folded into
+// the state; row r sees global keys <= total_kv - rows + r when causal.
 void accumulate_chunk(AttnChunkState& st, const Mat& query, const KvChunk& chunk, std::int64_t chunk_pos,
                       std::int64_t total_kv, bool causal) {
-  const int rows = query.rows, len = chunk.keys.rows;
-  if (st.empty()) st = empty_state(rows, query.cols);
-  if (st.partial_output.rows != rows || st.partial_output.cols != query.cols)
+  const Mat& k = chunk.keys;
+  const Mat& v = chunk.values;
+  if (k.cols != query.cols || v.rows != k.rows) throw std::invalid_argument("accumulate_chunk: dimension mismatch");
+  if (st.partial_output.rows != query.rows || st.partial_output.cols != v.cols)
     throw std::invalid_argument("accumulate_chunk: state shape mismatch");
-  const int64_t first_visible_limit = total_kv - rows;  // row 0 sees keys <= this
-  bool masked = false;
-  if (causal && chunk_pos + len - 1 > first_visible_limit) {
-    if (chunk_pos > total_kv - 1) return;  // no row sees any key of this chunk
-    if (!(len == rows && chunk_pos + len == total_kv))
-      throw std::invalid_argument(
-          "accumulate_chunk (B200): a partially visible chunk must be the slice's diagonal chunk");
-    masked = true;
-  }
-  st = merge_partials(st, run_k1(query, {&chunk}, masked));
+  st = merge_partials(st, run_k1(query, {&chunk}, causal, total_kv - query.rows - chunk_pos));
 }
 
 // attention.cpp:63-82
@@ -177,9 +168,16 @@ Mat finalize(const AttnChunkState& st) {
 
 // attention.cpp:94-111 — one K1 launch over the whole ordered chunk list
 std::pair<Mat, AttnChunkState> chunk_attention(const Mat& query, const std::vector<KvChunk>& chunks, bool causal) {
+  std::int64_t total_kv = 0;
   std::vector<const KvChunk*> ptrs;
-  for (const KvChunk& c : chunks) ptrs.push_back(&c);
-  AttnChunkState st = run_k1(query, ptrs, causal);
+  for (const KvChunk& c : chunks) {
+    if (c.keys.rows != c.values.rows) throw std::invalid_argument("chunk_attention: key/value row mismatch");
+    if (c.keys.cols != query.cols || c.values.cols != chunks.front().values.cols)
+      throw std::invalid_argument("accumulate_chunk: dimension mismatch");
+    total_kv += c.keys.rows;
+    ptrs.push_back(&c);
+  }
+  AttnChunkState st = run_k1(query, ptrs, causal, total_kv - query.rows);
   Mat o = finalize(st);
   return {std::move(o), std::move(st)};
 }
@@ -202,7 +200,7 @@ extern "C" int sp_host_chunk_attention(const double* q, int rows, int d, const d
       std::memcpy(chunks[size_t(c)].values.a.data(), v + pos * d, sizeof(double) * size_t(chunk_lens[c]) * d);
       pos += chunk_lens[c];
     }
-    pipelab::AttnChunkState st;
+    pipelab::AttnChunkState st = pipelab::empty_state(rows, d);
     pipelab::Mat o;
     if (streamed) {  // accumulate_chunk per chunk, then finalize (attention.cpp:94-111 loop)
       int64_t cp = 0;
@@ -210,7 +208,6 @@ extern "C" int sp_host_chunk_attention(const double* q, int rows, int d, const d
         pipelab::accumulate_chunk(st, qm, chunks[size_t(c)], cp, pos, causal != 0);
         cp += chunk_lens[c];
       }
-      if (st.empty()) st = pipelab::empty_state(rows, d);
       o = pipelab::finalize(st);
     } else {
       auto r = pipelab::chunk_attention(qm, chunks, causal != 0);

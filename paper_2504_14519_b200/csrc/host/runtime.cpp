@@ -42,6 +42,7 @@
 #include "pipelab/schedule.hpp"
 #include "pipelab/simulator.hpp"
 #include "slimpipe.h"
+#include "transport.hpp"
 
 namespace sp {
 namespace {
@@ -157,7 +158,9 @@ class Runtime {
   // direction), split from nc_fwd / nc_bwd, so a send to a busy neighbour
   // never blocks a receive from the other one (no head-of-line blocking).
   // Comm ranks inside a link: lower stage = 0, higher stage = 1.
-  ncclComm_t c_act_in = nullptr, c_act_out = nullptr, c_grad_in = nullptr, c_grad_out = nullptr;
+  std::unique_ptr<Link> l_act_in, l_act_out, l_grad_in, l_grad_out;
+  std::unique_ptr<Link> vlink;  // world communicator of the vocabulary collectives
+  LoopWorld* loop = nullptr;    // single-GPU loopback world (transport.hpp), or NCCL when null
   cudaStream_t s_act_in = nullptr, s_act_out = nullptr, s_grad_in = nullptr, s_grad_out = nullptr;
   bf16raw* ain_buf[2] = {nullptr, nullptr};  // activations received from s-1 (ring)
   cudaEvent_t ev_ain_free[2]{};
@@ -189,7 +192,7 @@ class Runtime {
   };
   std::map<int, PassX> xplan;
   pipelab::ExchangeAnnotation ann;
-  ncclComm_t nc_x[2] = {nullptr, nullptr};
+  std::unique_ptr<Link> lx[2];
   cudaStream_t cx[2] = {nullptr, nullptr}, rx[2] = {nullptr, nullptr};
   int x_tout = 0, x_cout = 0, x_tin = 0, x_cin = 0;  // per-class maxima (both classes)
   struct XBuf {
@@ -205,12 +208,7 @@ class Runtime {
   ~Runtime() {
     if (comp) cudaStreamSynchronize(comp);
     for (void* a : allocations) cudaFree(a);
-    for (ncclComm_t cm : {c_act_in, c_act_out, c_grad_in, c_grad_out})
-      if (cm) ncclCommDestroy(cm);
     if (nc_fwd) ncclCommDestroy(nc_fwd);
-    if (nc_bwd) ncclCommDestroy(nc_bwd);
-    for (int c = 0; c < 2; ++c)
-      if (nc_x[c]) ncclCommDestroy(nc_x[c]);
     for (auto& t : times) {
       cudaEventDestroy(t.start);
       cudaEventDestroy(t.end);
@@ -237,8 +235,9 @@ class Runtime {
   std::pair<int, int> sk(int k, int j) const { return {k, (cur << 20) | j}; }
   float* G(int64_t off) { return grad + off; }
 
-  int init(const sp_model_config& c, const void* ids) {
+  int init(const sp_model_config& c, const void* ids, LoopWorld* lw = nullptr) {
     cfg = c;
+    loop = lw;
     rank = c.rank;
     p = c.pp;
     stage = rank + 1;
@@ -339,59 +338,14 @@ class Runtime {
     SP_CUDA(cudaEventCreate(&step_start));
     SP_CUDA(cudaEventCreate(&step_end));
 
-    if (p > 1) {
-      ncclUniqueId id[SP_NCCL_IDS];
-      std::memcpy(id, ids, sizeof id);
-      // SP_NCCL_MAX_CTAS=N (diagnostics, default unset = NCCL's choice) caps
-      // the CTAs of every stage communicator's kernels
-      ncclConfig_t ccfg = NCCL_CONFIG_INITIALIZER;
-      ncclConfig_t* pcfg = nullptr;
-      if (const char* mc = std::getenv("SP_NCCL_MAX_CTAS")) {
-        ccfg.maxCTAs = std::max(1, std::atoi(mc));
-        ccfg.minCTAs = 1;
-        pcfg = &ccfg;
-      }
-      if (pcfg) {
-        SP_NCCL(ncclCommInitRankConfig(&nc_fwd, p, id[0], rank, pcfg));
-        SP_NCCL(ncclCommInitRankConfig(&nc_bwd, p, id[1], rank, pcfg));
-      } else {
-        SP_NCCL(ncclCommInitRank(&nc_fwd, p, id[0], rank));
-        SP_NCCL(ncclCommInitRank(&nc_bwd, p, id[1], rank));
-      }
-      // link (r, r+1) comes from split A when r is even, split B when r is odd
-      auto split = [&](ncclComm_t parent, int color, int key, ncclComm_t* out) -> int {
-        SP_NCCL(ncclCommSplit(parent, color, key, out, pcfg));
-        return SP_OK;
-      };
-      // v > 1 (even p): split B also carries the ring's wrap link (p-1, 0),
-      // where rank 0 is the receiving end and so takes link rank 1 (key p)
-      const bool ring = v > 1;
-      const int colA = rank / 2;  // {0,1} {2,3} ...
-      const int colB = ring ? (rank % 2 ? (rank + 1) / 2 : rank / 2) % (p / 2)
-                            : (rank == 0 ? NCCL_SPLIT_NOCOLOR : (rank + 1) / 2);  // {1,2} {3,4} ... [{p-1,0}]
-      const int keyB = ring && rank == 0 ? p : rank;
-      ncclComm_t fa = nullptr, fb = nullptr, ga = nullptr, gb = nullptr;
-      SP_TRY(split(nc_fwd, (rank == p - 1 && rank % 2 == 0) ? NCCL_SPLIT_NOCOLOR : colA, rank, &fa));
-      SP_TRY(split(nc_fwd, (!ring && rank == p - 1 && rank % 2 == 1) ? NCCL_SPLIT_NOCOLOR : colB, keyB, &fb));
-      SP_TRY(split(nc_bwd, (rank == p - 1 && rank % 2 == 0) ? NCCL_SPLIT_NOCOLOR : colA, rank, &ga));
-      SP_TRY(split(nc_bwd, (!ring && rank == p - 1 && rank % 2 == 1) ? NCCL_SPLIT_NOCOLOR : colB, keyB, &gb));
-      const bool even = rank % 2 == 0;
-      if (!last_dev || ring) {  // link to the next stage
-        c_act_out = even ? fa : fb;
-        c_grad_in = even ? ga : gb;
-      }
-      if (!first_dev || ring) {  // link to the previous stage (r-1, r): split A iff r-1 even
-        c_act_in = even ? fb : fa;
-        c_grad_out = even ? gb : ga;
-      }
-      if (!xplan.empty() || c.exchange_mode != 0) {
-        int lo = 0, hi = 0;
-        SP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-        for (int k = 0; k < 2; ++k) {
-          SP_NCCL(ncclCommInitRank(&nc_x[k], p, id[2 + k], rank));
-          SP_CUDA(cudaStreamCreateWithFlags(&cx[k], cudaStreamNonBlocking));
-          SP_CUDA(cudaStreamCreateWithPriority(&rx[k], cudaStreamNonBlocking, hi));
-        }
+    if (p > 1 && loop) SP_TRY(init_loop_links());
+    else if (p > 1) SP_TRY(init_nccl_links(ids));
+    if (!xplan.empty() || c.exchange_mode != 0) {
+      int lo = 0, hi = 0;
+      SP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      for (int k = 0; k < 2 && p > 1; ++k) {
+        SP_CUDA(cudaStreamCreateWithFlags(&cx[k], cudaStreamNonBlocking));
+        SP_CUDA(cudaStreamCreateWithPriority(&rx[k], cudaStreamNonBlocking, hi));
       }
     }
     if (vp) SP_CUDA(cudaStreamCreateWithFlags(&s_vocab, cudaStreamNonBlocking));
@@ -405,6 +359,90 @@ class Runtime {
     return SP_OK;
   }
 
+  // Stage links and exchange communicators over NCCL (one process per GPU).
+  int init_nccl_links(const void* ids) {
+    ncclUniqueId id[SP_NCCL_IDS];
+    std::memcpy(id, ids, sizeof id);
+    // SP_NCCL_MAX_CTAS=N (diagnostics, default unset = NCCL's choice) caps
+    // the CTAs of every stage communicator's kernels
+    ncclConfig_t ccfg = NCCL_CONFIG_INITIALIZER;
+    ncclConfig_t* pcfg = nullptr;
+    if (const char* mc = std::getenv("SP_NCCL_MAX_CTAS")) {
+      ccfg.maxCTAs = std::max(1, std::atoi(mc));
+      ccfg.minCTAs = 1;
+      pcfg = &ccfg;
+    }
+    if (pcfg) {
+      SP_NCCL(ncclCommInitRankConfig(&nc_fwd, p, id[0], rank, pcfg));
+      SP_NCCL(ncclCommInitRankConfig(&nc_bwd, p, id[1], rank, pcfg));
+    } else {
+      SP_NCCL(ncclCommInitRank(&nc_fwd, p, id[0], rank));
+      SP_NCCL(ncclCommInitRank(&nc_bwd, p, id[1], rank));
+    }
+    // link (r, r+1) comes from split A when r is even, split B when r is odd
+    auto split = [&](ncclComm_t parent, int color, int key, ncclComm_t* out) -> int {
+      SP_NCCL(ncclCommSplit(parent, color, key, out, pcfg));
+      return SP_OK;
+    };
+    // v > 1 (even p): split B also carries the ring's wrap link (p-1, 0),
+    // where rank 0 is the receiving end and so takes link rank 1 (key p)
+    const bool ring = v > 1;
+    const int colA = rank / 2;  // {0,1} {2,3} ...
+    const int colB = ring ? (rank % 2 ? (rank + 1) / 2 : rank / 2) % (p / 2)
+                          : (rank == 0 ? NCCL_SPLIT_NOCOLOR : (rank + 1) / 2);  // {1,2} {3,4} ... [{p-1,0}]
+    const int keyB = ring && rank == 0 ? p : rank;
+    ncclComm_t fa = nullptr, fb = nullptr, ga = nullptr, gb = nullptr;
+    SP_TRY(split(nc_fwd, (rank == p - 1 && rank % 2 == 0) ? NCCL_SPLIT_NOCOLOR : colA, rank, &fa));
+    SP_TRY(split(nc_fwd, (!ring && rank == p - 1 && rank % 2 == 1) ? NCCL_SPLIT_NOCOLOR : colB, keyB, &fb));
+    SP_TRY(split(nc_bwd, (rank == p - 1 && rank % 2 == 0) ? NCCL_SPLIT_NOCOLOR : colA, rank, &ga));
+    SP_TRY(split(nc_bwd, (!ring && rank == p - 1 && rank % 2 == 1) ? NCCL_SPLIT_NOCOLOR : colB, keyB, &gb));
+    const bool even = rank % 2 == 0;
+    if (!last_dev || ring) {  // link to the next stage
+      l_act_out = make_nccl_link(even ? fa : fb);
+      l_grad_in = make_nccl_link(even ? ga : gb);
+    }
+    if (!first_dev || ring) {  // link to the previous stage (r-1, r): split A iff r-1 even
+      l_act_in = make_nccl_link(even ? fb : fa);
+      l_grad_out = make_nccl_link(even ? gb : ga);
+    }
+    if (!xplan.empty() || cfg.exchange_mode != 0)
+      for (int k = 0; k < 2; ++k) {
+        ncclComm_t cm = nullptr;
+        SP_NCCL(ncclCommInitRank(&cm, p, id[2 + k], rank));
+        lx[k] = make_nccl_link(cm);
+      }
+    if (vp) {  // the vocabulary collectives run on the world communicator nc_bwd
+      vlink = make_nccl_link(nc_bwd);
+      nc_bwd = nullptr;
+    }
+    return SP_OK;
+  }
+
+  // The same links on the single-GPU loopback transport (every rank a thread
+  // of this process): communicator ids 0 activations, 1 gradients, 2/3 the
+  // two exchange classes.  Link ranks as in init_nccl_links: the lower stage
+  // of a stage link is link rank 0 (the ring's wrap link: device p-1).
+  int init_loop_links() {
+    if (loop_world_size(loop) != p) return set_error(SP_ERR_INVALID, "loopback world has %d ranks, pp = %d",
+                                                     loop_world_size(loop), p);
+    if (vp) return set_error(SP_ERR_UNSUPPORTED, "loopback transport: vocabulary parallelism needs collectives");
+    const bool ring = v > 1;
+    const int nx = (rank + 1) % p, pv = (rank + p - 1) % p;
+    if (!last_dev || ring) {
+      l_act_out = make_loop_link(loop, 0, {rank, nx}, 0);
+      l_grad_in = make_loop_link(loop, 1, {rank, nx}, 0);
+    }
+    if (!first_dev || ring) {
+      l_act_in = make_loop_link(loop, 0, {pv, rank}, 1);
+      l_grad_out = make_loop_link(loop, 1, {pv, rank}, 1);
+    }
+    std::vector<int> all(static_cast<size_t>(p));
+    for (int r = 0; r < p; ++r) all[size_t(r)] = r;
+    if (!xplan.empty() || cfg.exchange_mode != 0)
+      for (int k = 0; k < 2; ++k) lx[k] = make_loop_link(loop, 2 + k, all, rank);
+    return SP_OK;
+  }
+
   // Diagnostics for the open vocab-parallel stall: run each
   // vocab collective once at its real message size before the arena exists,
   // so NCCL's lazy connection setup happens here (same order on all ranks)
@@ -414,10 +452,10 @@ class Runtime {
     SP_CUDA(cudaMalloc(&buf, size_t(Ls) * size_t(h) * 4));
     SP_CUDA(cudaMemsetAsync(buf, 0, size_t(Ls) * size_t(h) * 4, s_vocab));
     float* f = static_cast<float*>(buf);
-    SP_NCCL(ncclBroadcast(buf, buf, Ls * h, ncclBfloat16, p - 1, nc_bwd, s_vocab));
-    SP_NCCL(ncclAllReduce(f, f, Ls, ncclFloat32, ncclMax, nc_bwd, s_vocab));
-    SP_NCCL(ncclAllReduce(f, f, 2 * Ls, ncclFloat32, ncclSum, nc_bwd, s_vocab));
-    SP_NCCL(ncclReduce(f, f, Ls * h, ncclFloat32, ncclSum, p - 1, nc_bwd, s_vocab));
+    SP_TRY(vlink->broadcast(buf, Ls * h, ncclBfloat16, p - 1, s_vocab));
+    SP_TRY(vlink->all_reduce(f, Ls, ncclMax, s_vocab));
+    SP_TRY(vlink->all_reduce(f, 2 * Ls, ncclSum, s_vocab));
+    SP_TRY(vlink->reduce(f, Ls * h, p - 1, s_vocab));
     SP_CUDA(cudaStreamSynchronize(s_vocab));
     SP_CUDA(cudaFree(buf));
     return SP_OK;
@@ -551,18 +589,16 @@ class Runtime {
   // their arena slots), landing contiguously at the transfer's pool rows.
   int recv_chunks(bf16raw* rk, bf16raw* rv, const XIn& xi, int c) {
     for (std::size_t x = 0; x < xi.chunks.size(); ++x)
-      SP_NCCL(ncclRecv(rk + int64_t(xi.base + x) * Ls * kvd, Ls * kvd, ncclBfloat16, xi.peer, nc_x[c], cx[c]));
+      SP_TRY(lx[c]->recv(rk + int64_t(xi.base + x) * Ls * kvd, Ls * kvd, ncclBfloat16, xi.peer, cx[c]));
     for (std::size_t x = 0; x < xi.chunks.size(); ++x)
-      SP_NCCL(ncclRecv(rv + int64_t(xi.base + x) * Ls * kvd, Ls * kvd, ncclBfloat16, xi.peer, nc_x[c], cx[c]));
+      SP_TRY(lx[c]->recv(rv + int64_t(xi.base + x) * Ls * kvd, Ls * kvd, ncclBfloat16, xi.peer, cx[c]));
     return SP_OK;
   }
   int send_chunks(int l, int k, const XOut& xo, int c) {
     for (int ch : xo.chunks)
-      SP_NCCL(ncclSend(k_pool[l] + int64_t(slot_of.at(sk(k, ch))) * Ls * kvd, Ls * kvd, ncclBfloat16, xo.peer, nc_x[c],
-                       cx[c]));
+      SP_TRY(lx[c]->send(k_pool[l] + int64_t(slot_of.at(sk(k, ch))) * Ls * kvd, Ls * kvd, ncclBfloat16, xo.peer, cx[c]));
     for (int ch : xo.chunks)
-      SP_NCCL(ncclSend(v_pool[l] + int64_t(slot_of.at(sk(k, ch))) * Ls * kvd, Ls * kvd, ncclBfloat16, xo.peer, nc_x[c],
-                       cx[c]));
+      SP_TRY(lx[c]->send(v_pool[l] + int64_t(slot_of.at(sk(k, ch))) * Ls * kvd, Ls * kvd, ncclBfloat16, xo.peer, cx[c]));
     x_bytes_sent += 2 * int64_t(xo.chunks.size()) * Ls * kvd * 2;
     return SP_OK;
   }
@@ -597,10 +633,10 @@ class Runtime {
       for (std::size_t t = 0; t < px.in.size(); ++t) {
         const XIn& xi = px.in[t];
         const int nc = int(xi.chunks.size());
-        SP_NCCL(ncclGroupStart());
-        SP_NCCL(ncclRecv(b.rq + t * Ls * qd, Ls * qd, ncclBfloat16, xi.peer, nc_x[c], cx[c]));
+        SP_TRY(lx[c]->group_start());
+        SP_TRY(lx[c]->recv(b.rq + t * Ls * qd, Ls * qd, ncclBfloat16, xi.peer, cx[c]));
         SP_TRY(recv_chunks(b.rk, b.rv, xi, c));
-        SP_NCCL(ncclGroupEnd());
+        SP_TRY(lx[c]->group_end());
         SP_TRY(link(cx[c], rx[c]));
         std::vector<int32_t> rows;
         for (int x = 0; x < nc; ++x) rows.push_back(int32_t((xi.base + x) * Ls));
@@ -609,10 +645,10 @@ class Runtime {
                            nc, int(Ls), cfg.heads, cfg.kv_heads, cfg.head_dim, causal, b.ro + t * Ls * qd, qd,
                            b.rlse + t * a * Ls, rx[c]));
         SP_TRY(link(rx[c], cx[c]));
-        SP_NCCL(ncclGroupStart());
-        SP_NCCL(ncclSend(b.ro + t * Ls * qd, Ls * qd, ncclBfloat16, xi.peer, nc_x[c], cx[c]));
-        SP_NCCL(ncclSend(b.rlse + t * a * Ls, a * Ls, ncclFloat32, xi.peer, nc_x[c], cx[c]));
-        SP_NCCL(ncclGroupEnd());
+        SP_TRY(lx[c]->group_start());
+        SP_TRY(lx[c]->send(b.ro + t * Ls * qd, Ls * qd, ncclBfloat16, xi.peer, cx[c]));
+        SP_TRY(lx[c]->send(b.rlse + t * a * Ls, a * Ls, ncclFloat32, xi.peer, cx[c]));
+        SP_TRY(lx[c]->group_end());
       }
       return SP_OK;
     };
@@ -620,12 +656,12 @@ class Runtime {
       for (std::size_t t = 0; t < px.in.size(); ++t) {
         const XIn& xi = px.in[t];
         const int nc = int(xi.chunks.size());
-        SP_NCCL(ncclGroupStart());
-        SP_NCCL(ncclRecv(b.rq + t * Ls * qd, Ls * qd, ncclBfloat16, xi.peer, nc_x[c], cx[c]));
-        SP_NCCL(ncclRecv(b.rdo + t * Ls * qd, Ls * qd, ncclBfloat16, xi.peer, nc_x[c], cx[c]));
-        SP_NCCL(ncclRecv(b.rstats + t * 2 * a * Ls, 2 * a * Ls, ncclFloat32, xi.peer, nc_x[c], cx[c]));
+        SP_TRY(lx[c]->group_start());
+        SP_TRY(lx[c]->recv(b.rq + t * Ls * qd, Ls * qd, ncclBfloat16, xi.peer, cx[c]));
+        SP_TRY(lx[c]->recv(b.rdo + t * Ls * qd, Ls * qd, ncclBfloat16, xi.peer, cx[c]));
+        SP_TRY(lx[c]->recv(b.rstats + t * 2 * a * Ls, 2 * a * Ls, ncclFloat32, xi.peer, cx[c]));
         SP_TRY(recv_chunks(b.rk, b.rv, xi, c));
-        SP_NCCL(ncclGroupEnd());
+        SP_TRY(lx[c]->group_end());
         SP_TRY(link(cx[c], rx[c]));
         std::vector<int32_t> rows;
         for (int x = 0; x < nc; ++x) rows.push_back(int32_t((xi.base + x) * Ls));
@@ -641,11 +677,11 @@ class Runtime {
                                 b.rdo + t * Ls * qd, qd, b.rstats + t * 2 * a * Ls, dq, b.rdk, b.rdv,
                                 int64_t(std::max(1, x_cin)) * Ls, rows.data(), rx[c]));
         SP_TRY(link(rx[c], cx[c]));
-        SP_NCCL(ncclGroupStart());
-        SP_NCCL(ncclSend(dq, Ls * qd, ncclFloat32, xi.peer, nc_x[c], cx[c]));
-        SP_NCCL(ncclSend(dk, nc * Ls * kvd, ncclFloat32, xi.peer, nc_x[c], cx[c]));
-        SP_NCCL(ncclSend(dv, nc * Ls * kvd, ncclFloat32, xi.peer, nc_x[c], cx[c]));
-        SP_NCCL(ncclGroupEnd());
+        SP_TRY(lx[c]->group_start());
+        SP_TRY(lx[c]->send(dq, Ls * qd, ncclFloat32, xi.peer, cx[c]));
+        SP_TRY(lx[c]->send(dk, nc * Ls * kvd, ncclFloat32, xi.peer, cx[c]));
+        SP_TRY(lx[c]->send(dv, nc * Ls * kvd, ncclFloat32, xi.peer, cx[c]));
+        SP_TRY(lx[c]->group_end());
       }
       return SP_OK;
     };
@@ -852,10 +888,10 @@ class Runtime {
     if (out) {
       SP_TRY(link(comp, cx[c]));
       for (const XOut& xo : px->out) {
-        SP_NCCL(ncclGroupStart());
-        SP_NCCL(ncclSend(x.q, Ls * qd, ncclBfloat16, xo.peer, nc_x[c], cx[c]));
+        SP_TRY(lx[c]->group_start());
+        SP_TRY(lx[c]->send(x.q, Ls * qd, ncclBfloat16, xo.peer, cx[c]));
         SP_TRY(send_chunks(l, k, xo, c));
-        SP_NCCL(ncclGroupEnd());
+        SP_TRY(lx[c]->group_end());
         x_bytes_sent += Ls * qd * 2;
       }
     }
@@ -863,10 +899,10 @@ class Runtime {
     if (out) {
       XBuf& b = xb[c];
       for (std::size_t t = 0; t < px->out.size(); ++t) {
-        SP_NCCL(ncclGroupStart());
-        SP_NCCL(ncclRecv(b.o_rem + t * Ls * qd, Ls * qd, ncclBfloat16, px->out[t].peer, nc_x[c], cx[c]));
-        SP_NCCL(ncclRecv(b.lse_rem + t * a * Ls, a * Ls, ncclFloat32, px->out[t].peer, nc_x[c], cx[c]));
-        SP_NCCL(ncclGroupEnd());
+        SP_TRY(lx[c]->group_start());
+        SP_TRY(lx[c]->recv(b.o_rem + t * Ls * qd, Ls * qd, ncclBfloat16, px->out[t].peer, cx[c]));
+        SP_TRY(lx[c]->recv(b.lse_rem + t * a * Ls, a * Ls, ncclFloat32, px->out[t].peer, cx[c]));
+        SP_TRY(lx[c]->group_end());
       }
       SP_TRY(link(cx[c], comp));
       for (std::size_t t = 0; t < px->out.size(); ++t)
@@ -930,7 +966,7 @@ class Runtime {
       ain_idx ^= 1;
       SP_CUDA(cudaStreamWaitEvent(s_act_in, ev_ain_free[b], 0));
       if (jit_recv) SP_TRY(link(comp, s_act_in));  // post the receive only when this pass starts
-      SP_NCCL(ncclRecv(ain_buf[b], Ls * h, ncclBfloat16, 0, c_act_in, s_act_in));
+      SP_TRY(l_act_in->recv(ain_buf[b], Ls * h, ncclBfloat16, 0, s_act_in));
       SP_TRY(link(s_act_in, comp));
       SP_CUDA(cudaEventRecord(t0, comp));  // busy time starts once the input is here
       SP_CUDA(cudaMemcpyAsync(xs, ain_buf[b], Ls * h * 2, cudaMemcpyDeviceToDevice, comp));
@@ -946,7 +982,7 @@ class Runtime {
       SP_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
       SP_CUDA(cudaEventRecord(done, comp));
       SP_CUDA(cudaStreamWaitEvent(s_act_out, done, 0));
-      SP_NCCL(ncclSend(out_buf[b], Ls * h, ncclBfloat16, 1, c_act_out, s_act_out));
+      SP_TRY(l_act_out->send(out_buf[b], Ls * h, ncclBfloat16, 1, s_act_out));
       SP_CUDA(cudaEventRecord(ev_out_free[b], s_act_out));
       cudaEventDestroy(done);
     } else {
@@ -1002,12 +1038,12 @@ class Runtime {
     if (out) {
       SP_TRY(link(comp, cx[c]));
       for (const XOut& xo : px->out) {
-        SP_NCCL(ncclGroupStart());
-        SP_NCCL(ncclSend(x.q, Ls * qd, ncclBfloat16, xo.peer, nc_x[c], cx[c]));
-        SP_NCCL(ncclSend(tmp_h, Ls * qd, ncclBfloat16, xo.peer, nc_x[c], cx[c]));
-        SP_NCCL(ncclSend(delta_ws, 2 * a * Ls, ncclFloat32, xo.peer, nc_x[c], cx[c]));
+        SP_TRY(lx[c]->group_start());
+        SP_TRY(lx[c]->send(x.q, Ls * qd, ncclBfloat16, xo.peer, cx[c]));
+        SP_TRY(lx[c]->send(tmp_h, Ls * qd, ncclBfloat16, xo.peer, cx[c]));
+        SP_TRY(lx[c]->send(delta_ws, 2 * a * Ls, ncclFloat32, xo.peer, cx[c]));
         SP_TRY(send_chunks(l, k, xo, c));
-        SP_NCCL(ncclGroupEnd());
+        SP_TRY(lx[c]->group_end());
         x_bytes_sent += 2 * Ls * qd * 2 + 2 * a * Ls * 4;
       }
     }
@@ -1027,11 +1063,11 @@ class Runtime {
       for (std::size_t tt = 0; tt < px->out.size(); ++tt) {
         const XOut& xo = px->out[tt];
         const int64_t nc = int64_t(xo.chunks.size());
-        SP_NCCL(ncclGroupStart());
-        SP_NCCL(ncclRecv(b.dq_rem + tt * Ls * qd, Ls * qd, ncclFloat32, xo.peer, nc_x[c], cx[c]));
-        SP_NCCL(ncclRecv(b.dk_rem + int64_t(xo.base) * Ls * kvd, nc * Ls * kvd, ncclFloat32, xo.peer, nc_x[c], cx[c]));
-        SP_NCCL(ncclRecv(b.dv_rem + int64_t(xo.base) * Ls * kvd, nc * Ls * kvd, ncclFloat32, xo.peer, nc_x[c], cx[c]));
-        SP_NCCL(ncclGroupEnd());
+        SP_TRY(lx[c]->group_start());
+        SP_TRY(lx[c]->recv(b.dq_rem + tt * Ls * qd, Ls * qd, ncclFloat32, xo.peer, cx[c]));
+        SP_TRY(lx[c]->recv(b.dk_rem + int64_t(xo.base) * Ls * kvd, nc * Ls * kvd, ncclFloat32, xo.peer, cx[c]));
+        SP_TRY(lx[c]->recv(b.dv_rem + int64_t(xo.base) * Ls * kvd, nc * Ls * kvd, ncclFloat32, xo.peer, cx[c]));
+        SP_TRY(lx[c]->group_end());
       }
       SP_TRY(link(cx[c], comp));
       for (std::size_t tt = 0; tt < px->out.size(); ++tt) {
@@ -1062,7 +1098,7 @@ class Runtime {
     VSlot& vs = *vsp;
     const int64_t tok0 = int64_t(k - 1) * cfg.seq_len + int64_t(i - 1) * Ls;
     SP_TRY(link(comp, s_vocab));
-    SP_NCCL(ncclBroadcast(vs.xf, vs.xf, Ls * h, ncclBfloat16, p - 1, nc_bwd, s_vocab));
+    SP_TRY(vlink->broadcast(vs.xf, Ls * h, ncclBfloat16, p - 1, s_vocab));
     SP_TRY(link(s_vocab, comp));
     SP_TRY(gemm(false, true, Ls, Vs, h, vs.xf, h, W(head), h, vlogits, Vs, true, 1.f, 0.f, comp));
     float* m_loc = vs.st;
@@ -1070,11 +1106,11 @@ class Runtime {
     float* zt = vs.st + 2 * Ls;
     SP_TRY(xent_shard_stats(vlogits, targets + tok0, Ls, int(Vs), int(v0), m_loc, m_glob, zt, comp));
     SP_TRY(link(comp, s_vocab));
-    SP_NCCL(ncclAllReduce(m_glob, m_glob, Ls, ncclFloat32, ncclMax, nc_bwd, s_vocab));
+    SP_TRY(vlink->all_reduce(m_glob, Ls, ncclMax, s_vocab));
     SP_TRY(link(s_vocab, comp));
     SP_TRY(xent_shard_rescale(m_loc, m_glob, zt, Ls, comp));
     SP_TRY(link(comp, s_vocab));
-    SP_NCCL(ncclAllReduce(zt, zt, 2 * Ls, ncclFloat32, ncclSum, nc_bwd, s_vocab));
+    SP_TRY(vlink->all_reduce(zt, 2 * Ls, ncclSum, s_vocab));
     SP_TRY(link(s_vocab, comp));
     return SP_OK;
   }
@@ -1093,7 +1129,7 @@ class Runtime {
     SP_TRY(gemm(false, false, Ls, h, Vs, vdlog, Vs, W(head), h, vdxf, h, true, 1.f, 0.f, comp));  // partial dX
     SP_TRY(gemm(true, false, Vs, h, Ls, vdlog, Vs, vs.xf, h, G(head), h, true, 1.f, 1.f, comp));    // dW shard
     SP_TRY(link(comp, s_vocab));
-    SP_NCCL(ncclReduce(vdxf, vdxf, Ls * h, ncclFloat32, ncclSum, p - 1, nc_bwd, s_vocab));
+    SP_TRY(vlink->reduce(vdxf, Ls * h, p - 1, s_vocab));
     SP_TRY(link(s_vocab, comp));
     vfree.push_back(vs_i);
     vslot_of.erase({k, i});
@@ -1115,7 +1151,7 @@ class Runtime {
       dx = gin_buf[gb];
       SP_CUDA(cudaStreamWaitEvent(s_grad_in, ev_gin_free[gb], 0));
       if (jit_recv) SP_TRY(link(comp, s_grad_in));
-      SP_NCCL(ncclRecv(dx, Ls * h, ncclBfloat16, 1, c_grad_in, s_grad_in));
+      SP_TRY(l_grad_in->recv(dx, Ls * h, ncclBfloat16, 1, s_grad_in));
       cudaEvent_t got;
       SP_CUDA(cudaEventCreateWithFlags(&got, cudaEventDisableTiming));
       SP_CUDA(cudaEventRecord(got, s_grad_in));
@@ -1161,7 +1197,7 @@ class Runtime {
       SP_CUDA(cudaEventRecord(done, comp));
       SP_CUDA(cudaStreamWaitEvent(s_grad_out, done, 0));
       cudaEventDestroy(done);
-      SP_NCCL(ncclSend(dx, Ls * h, ncclBfloat16, 0, c_grad_out, s_grad_out));
+      SP_TRY(l_grad_out->send(dx, Ls * h, ncclBfloat16, 0, s_grad_out));
       if (gb >= 0) {  // middle stage: dx lives in the receive buffer
         SP_CUDA(cudaEventRecord(ev_gin_free[gb], s_grad_out));
       } else {        // last stage: dx lives in gout_buf[gout_idx]
@@ -1261,6 +1297,15 @@ int sp_nccl_unique_id(void* out128) {
 int sp_runtime_create(const sp_model_config* cfg, const void* nccl_ids, void** handle) {
   auto rt = std::make_unique<Runtime>();
   const int rc = rt->init(*cfg, nccl_ids);
+  if (rc != SP_OK) return rc;
+  *handle = rt.release();
+  return SP_OK;
+}
+
+int sp_runtime_create_loopback(const sp_model_config* cfg, void* world, void** handle) {
+  if (!world) return sp::set_error(SP_ERR_INVALID, "loopback world is null");
+  auto rt = std::make_unique<Runtime>();
+  const int rc = rt->init(*cfg, nullptr, static_cast<sp::LoopWorld*>(world));
   if (rc != SP_OK) return rc;
   *handle = rt.release();
   return SP_OK;

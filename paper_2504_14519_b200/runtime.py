@@ -133,6 +133,10 @@ def _lib():
     lib = N.lib()
     lib.sp_nccl_unique_id.argtypes = [C.c_void_p]
     lib.sp_runtime_create.argtypes = [C.POINTER(_Cfg), C.c_void_p, C.POINTER(C.c_void_p)]
+    lib.sp_runtime_create_loopback.argtypes = [C.POINTER(_Cfg), C.c_void_p, C.POINTER(C.c_void_p)]
+    lib.sp_loopback_create.argtypes = [C.c_int, C.POINTER(C.c_void_p)]
+    lib.sp_loopback_destroy.argtypes = [C.c_void_p]
+    lib.sp_loopback_errors.argtypes = [C.c_void_p]
     lib.sp_runtime_exchange_stats.argtypes = [C.c_void_p, C.POINTER(C.c_int64)]
     lib.sp_runtime_destroy.argtypes = [C.c_void_p]
     lib.sp_runtime_step.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_float)]
@@ -171,20 +175,77 @@ def nccl_ids(rank: int, world: int):
     return C.create_string_buffer(ids[0], 128 * N_NCCL_IDS)
 
 
+class LoopbackWorld:
+    """All pp ranks of a step as threads of this process on ONE GPU
+    (csrc/host/transport.hpp loopback): the stage links and exchange
+    transfers run through device flags and copy kernels instead of NCCL,
+    with the executor's own send/recv program.  For single-GPU boxes/tests:
+
+        world = LoopbackWorld(cfg.pp)
+        steps = [SlimPipeStep(cfg, r, cfg.pp, loopback=world) for r in range(cfg.pp)]
+        losses = world.run(lambda r: steps[r].step(tok, tgt, optimizer=False))
+    """
+
+    def __init__(self, ranks: int):
+        self.ranks = ranks
+        h = C.c_void_p()
+        N.check(_lib().sp_loopback_create(ranks, C.byref(h)), "sp_loopback_create")
+        self._h = h
+
+    @property
+    def handle(self):
+        return self._h
+
+    def errors(self) -> int:
+        return int(_lib().sp_loopback_errors(self._h))
+
+    def run(self, fn):
+        """fn(rank) on one host thread per rank (concurrently, as the ranks'
+        enqueues must be); returns the per-rank results, re-raising the
+        first exception."""
+        import threading
+        out, err = [None] * self.ranks, [None] * self.ranks
+
+        def body(r):
+            try:
+                out[r] = fn(r)
+            except BaseException as e:  # noqa: BLE001 - re-raised below
+                err[r] = e
+        ths = [threading.Thread(target=body, args=(r,)) for r in range(self.ranks)]
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+        for e in err:
+            if e is not None:
+                raise e
+        return out
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib().sp_loopback_destroy(self._h)
+            self._h = None
+
+
 class SlimPipeStep:
     """One pipeline stage of the sliced-1F1B step on this process's GPU."""
 
-    def __init__(self, cfg: StepConfig, rank: int | None = None, world: int | None = None):
+    def __init__(self, cfg: StepConfig, rank: int | None = None, world: int | None = None,
+                 loopback: LoopbackWorld | None = None):
         self.cfg = cfg
         self.rank = int(os.environ.get("RANK", 0)) if rank is None else rank
         self.world = int(os.environ.get("WORLD_SIZE", 1)) if world is None else world
         if cfg.pp != self.world:
             raise ValueError(f"pp ({cfg.pp}) must equal the number of ranks ({self.world})")
         lib = _lib()
-        ids = nccl_ids(self.rank, self.world)
         h = C.c_void_p()
         c = cfg.to_c(self.rank)
-        N.check(lib.sp_runtime_create(C.byref(c), ids, C.byref(h)), "sp_runtime_create")
+        if loopback is not None:
+            N.check(lib.sp_runtime_create_loopback(C.byref(c), loopback.handle, C.byref(h)),
+                    "sp_runtime_create_loopback")
+        else:
+            ids = nccl_ids(self.rank, self.world)
+            N.check(lib.sp_runtime_create(C.byref(c), ids, C.byref(h)), "sp_runtime_create")
         self._h = h
         self.stage = self.rank + 1
         self.is_first = self.stage == 1

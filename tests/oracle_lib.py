@@ -170,3 +170,57 @@ def port_mha_bwd(q, k, v, dout, lse, causal, threads=8):
 
 def parse(text: str):
     return json.loads(text)
+
+
+def _port_sampled():
+    p = port()
+    if not getattr(p, "_sampled_typed", False):
+        p.orc_fwd_rows.argtypes = [_fp, C.c_int, C.c_int, C.c_int, _fp, _fp, C.c_int, C.c_int64, C.c_int, _ip,
+                                   C.c_int, _dp, _dp, C.c_int]
+        p.orc_bwd_rows.argtypes = [_fp, C.c_int, C.c_int, C.c_int, _fp, _fp, C.c_int, C.c_int64, C.c_int, _fp,
+                                   C.c_int, _fp, C.c_int, _dp, _ip, C.c_int, _dp, C.c_int]
+        p.orc_bwd_keys.argtypes = [_fp, C.c_int, C.c_int, C.c_int, _fp, _fp, C.c_int, C.c_int64, C.c_int, _fp,
+                                   C.c_int, _fp, C.c_int, _dp, _ip, C.c_int, _dp, _dp, C.c_int]
+        p._sampled_typed = True
+    return p
+
+
+def _f32(a):
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+def port_fwd_rows(q, k, v, causal, sel, threads=8):
+    """One head: q [rows,d], k/v [total,d] -> (o [len(sel),d], lse [len(sel)]) of rows `sel`."""
+    q, k, v = _f32(q), _f32(k), _f32(v)
+    rows, d = q.shape
+    sel = np.ascontiguousarray(sel, dtype=np.int32)
+    o = np.zeros((len(sel), d))
+    lse = np.zeros(len(sel))
+    _port_sampled().orc_fwd_rows(_f(q), d, rows, d, _f(k), _f(v), d, k.shape[0], int(causal),
+                                 sel.ctypes.data_as(_ip), len(sel), _d(o), _d(lse), threads)
+    return o, lse
+
+
+def port_bwd_rows(q, k, v, o, dout, lse, causal, sel, threads=8):
+    """dQ of rows `sel` for the backward as a function of (Q, K, V, O, dO, LSE)."""
+    q, k, v, o, dout = _f32(q), _f32(k), _f32(v), _f32(o), _f32(dout)
+    lse = np.ascontiguousarray(lse, dtype=np.float64)
+    rows, d = q.shape
+    sel = np.ascontiguousarray(sel, dtype=np.int32)
+    dq = np.zeros((len(sel), d))
+    _port_sampled().orc_bwd_rows(_f(q), d, rows, d, _f(k), _f(v), d, k.shape[0], int(causal), _f(o), d, _f(dout), d,
+                                 _d(lse), sel.ctypes.data_as(_ip), len(sel), _d(dq), threads)
+    return dq
+
+
+def port_bwd_keys(q, k, v, o, dout, lse, causal, sel, threads=8):
+    """dK/dV of key rows `sel`."""
+    q, k, v, o, dout = _f32(q), _f32(k), _f32(v), _f32(o), _f32(dout)
+    lse = np.ascontiguousarray(lse, dtype=np.float64)
+    rows, d = q.shape
+    sel = np.ascontiguousarray(sel, dtype=np.int32)
+    dk = np.zeros((len(sel), d))
+    dv = np.zeros((len(sel), d))
+    _port_sampled().orc_bwd_keys(_f(q), d, rows, d, _f(k), _f(v), d, k.shape[0], int(causal), _f(o), d, _f(dout), d,
+                                 _d(lse), sel.ctypes.data_as(_ip), len(sel), _d(dk), _d(dv), threads)
+    return dk, dv

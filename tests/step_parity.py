@@ -1,0 +1,101 @@
+"""Shared parity logic of the multi-stage step (PP > 1): what each rank
+reports and how rank 0 compares the assembled model with the float64 oracle
+(oracle/model_oracle.py).  Used by tests/mp_step_check.py (NCCL, one process
+per GPU) and tests/test_loopback_gpu.py (every rank a thread on one GPU).
+
+Tolerances: loss rel 1e-2; every parameter gradient max|g - ref| <=
+GRAD_TOL * max|ref| per tensor (bf16 activations through the whole stack;
+the measured worst case is printed).
+"""
+from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT / "oracle"))
+
+NAMES = ["attn_norm", "wqkv", "wo", "mlp_norm", "wgu", "wd"]
+GRAD_TOL = 5e-2
+LOSS_TOL = 1e-2
+
+
+def inputs(cfg, seed=0):
+    rng = np.random.default_rng(seed)
+    tok = rng.integers(0, cfg.vocab, (cfg.microbatches, cfg.seq_len), dtype=np.int32)
+    tgt = np.roll(tok, -1, axis=1).astype(np.int32)
+    tgt[:, -1] = -1
+    return tok, tgt
+
+
+def gather_rank(step, cfg, loss):
+    """Everything rank `step.rank` contributes to the comparison."""
+    lps = cfg.layers // cfg.pp
+    mine = {"loss": loss, "params": {}, "grads": {}}
+    for l in range(lps):  # lps local layers: v chunks of layers/(pp v)
+        for k in NAMES:
+            mine["params"][(step.global_layer(l), k)] = step.get_param(l, k)
+            mine["grads"][(step.global_layer(l), k)] = step.get_grad(l, k)
+    if step.is_first:
+        mine["params"][(None, "embedding")] = step.get_param(0, "embedding")
+        mine["grads"][(None, "embedding")] = step.get_grad(0, "embedding")
+    if step.is_last:
+        mine["params"][(None, "final_norm")] = step.get_param(0, "final_norm")
+        mine["grads"][(None, "final_norm")] = step.get_grad(0, "final_norm")
+    if cfg.vocab_parallel:  # every stage holds a vocabulary shard of the head
+        mine["head_shard"] = (step.get_param(0, "head"), step.get_grad(0, "head"))
+    elif step.is_last:
+        mine["params"][(None, "head")] = step.get_param(0, "head")
+        mine["grads"][(None, "head")] = step.get_grad(0, "head")
+    mine["mem"] = step.memory()
+    mine["x"] = step.exchange_stats()
+    return mine
+
+
+def compare(cfg, allv, tok, tgt, log=print):
+    """Rank-0 check of the gathered stages against the oracle.  Returns
+    (ok, worst relative gradient error, per-tensor errors)."""
+    import torch
+    import model_oracle as MO
+    world, n, m = cfg.pp, cfg.slices, cfg.microbatches
+    P, G = {}, {}
+    for d in allv:
+        P.update(d["params"])
+        G.update(d["grads"])
+    if cfg.vocab_parallel:
+        P[(None, "head")] = np.concatenate([d["head_shard"][0] for d in allv], axis=0)
+        G[(None, "head")] = np.concatenate([d["head_shard"][1] for d in allv], axis=0)
+    rnd = lambda x: torch.from_numpy(x).bfloat16().double().numpy()
+    W = {k: [rnd(P[(l, k)]) for l in range(cfg.layers)] for k in NAMES}
+    for k in ("embedding", "final_norm", "head"):
+        W[k] = rnd(P[(None, k)])
+    ref_loss, ref_g = MO.Model(W, cfg.heads, cfg.kv_heads, cfg.rope_theta, cfg.norm_eps).step(tok, tgt, n)
+    gpu_loss = allv[-1]["loss"]
+    log(f"pp={world} v={cfg.interleave} m={m} n={n} exchange={cfg.exchange} recompute={cfg.recompute} "
+        f"kv_heads={cfg.kv_heads} vocab_parallel={cfg.vocab_parallel} loss gpu {gpu_loss:.6f} oracle {ref_loss:.6f}")
+    xs = [d["x"] for d in allv]
+    log(f"exchange stats per rank: {xs}")
+    ok = True
+    if cfg.exchange != "off":
+        ok &= sum(x["passes_out"] for x in xs) > 0 and sum(x["bytes_sent"] for x in xs) > 0
+    ok &= abs(gpu_loss - ref_loss) / abs(ref_loss) < LOSS_TOL
+    worst, errs = 0.0, {}
+    for (l, k), g in G.items():
+        r = ref_g[k][l] if l is not None else ref_g[k]
+        e = float(np.max(np.abs(g - r)) / max(1e-30, np.max(np.abs(r))))
+        errs[f"{k}{'' if l is None else l}"] = e
+        worst = max(worst, e)
+        if e > GRAD_TOL:
+            log(f"grad mismatch {l} {k} {e}")
+            ok = False
+    log("per-tensor grad err: " + " ".join(f"{k}={v:.2e}" for k, v in sorted(errs.items())))
+    for r_, d in enumerate(allv):
+        mm = d["mem"]
+        expect = n + 2 * (world - 1 - r_) if m * n >= n + 2 * (world - 1) and cfg.interleave == 1 else None
+        log(f"rank {r_}: slots {mm['slots']} high-water {mm['slots_high_water']} ledger {mm['ledger_peak_units']}"
+            f" (n+2(p-d) = {expect})")
+        ok &= mm["slots_high_water"] == mm["ledger_peak_units"]
+    log(f"worst grad err {worst} {'PASS' if ok else 'FAIL'}")
+    return ok, worst, errs

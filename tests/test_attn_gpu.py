@@ -182,9 +182,13 @@ def test_pipelab_attention_api_matches_oracle(d, rows, chunks, causal, streamed)
            out.ctypes.data_as(dp), mx.ctypes.data_as(dp), sm.ctypes.data_as(dp))
     assert rc == 0, N.lib().sp_last_error()
     assert max_rel_err(out, ref_o) < TOL_BF16
-    lse = mx + np.log(sm)  # the state's log-sum-exp, whatever stabiliser it carries
+    lse = mx + np.log(sm)  # the state's log-sum-exp
     assert np.max(np.abs(lse - ref_lse)) < TOL_LSE
-    # unsupported shapes fail loudly (no CPU fallback)
-    rc = f(arr(q[:100]), 100, d, arr(k), arr(v), (C.c_int * len(chunks))(*chunks), len(chunks), int(causal), 0,
-           out.ctypes.data_as(dp), mx.ctypes.data_as(dp), sm.ctypes.data_as(dp))
+    _, _, ref_mx, ref_sm = O.port_chunk_attention(q, k, v, chunks, causal)  # reference state semantics
+    assert np.max(np.abs(mx - ref_mx)) < TOL_LSE and np.max(np.abs(sm - ref_sm) / ref_sm) < TOL_BF16
+    # head widths above the kernel's 128 fail loudly (no CPU fallback)
+    wide = np.zeros((rows, 160))
+    kw = np.zeros((total, 160))
+    rc = f(arr(wide), rows, 160, arr(kw), arr(kw), (C.c_int * len(chunks))(*chunks), len(chunks), int(causal), 0,
+           np.zeros((rows, 160)).ctypes.data_as(dp), mx.ctypes.data_as(dp), sm.ctypes.data_as(dp))
     assert rc == 1

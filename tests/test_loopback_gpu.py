@@ -1,0 +1,79 @@
+"""PP > 1 step parity on ONE GPU: every pipeline rank runs as a host thread
+of this process (LoopbackWorld, csrc/host/transport.hpp), so the executor's
+multi-stage program — stage sends/receives (reference schedule.cpp:102-130
+cross-device edges), the exchange transfers of every tick plan of
+apply_exchange (simulator.cpp:56-108: Q/K/V out, attention partials back,
+K3 merge, dQ/dK/dV adds), slot arena, recompute — runs on a single-GPU box
+exactly as under NCCL, and the assembled model is compared with the float64
+oracle (tests/step_parity.py tolerances)."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import step_parity as SP
+from test_attn_gpu import _need_gpu
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(pp, m, n, exchange, recompute, kv_heads=4, interleave=1):
+    from paper_2504_14519_b200.runtime import LoopbackWorld, SlimPipeStep, StepConfig
+    cfg = StepConfig.c1(pp=pp, microbatches=m, slices=n, layers=2 * pp * interleave, exchange=exchange,
+                        seq_len=1024 * n, recompute=recompute, kv_heads=kv_heads, interleave=interleave)
+    world = LoopbackWorld(pp)
+    steps = [SlimPipeStep(cfg, r, pp, loopback=world) for r in range(pp)]
+    try:
+        tok, tgt = SP.inputs(cfg)
+        torch.cuda.synchronize()
+        losses = world.run(lambda r: steps[r].step(tok, tgt, optimizer=False))
+        assert world.errors() == 0, "loopback transport saw mismatched message sizes"
+        allv = [SP.gather_rank(steps[r], cfg, losses[r]) for r in range(pp)]
+        ok, worst, _ = SP.compare(cfg, allv, tok, tgt)
+        return ok, worst, [s.exchange_stats() for s in steps]
+    finally:
+        for s in steps:
+            s.close()
+        world.close()
+
+
+@pytest.mark.parametrize("pp,m,n,x,rc", [
+    (2, 2, 4, "off", "selective"), (2, 1, 2, "off", "full"),
+    (2, 2, 4, "on", "selective"), (2, 2, 4, "on", "full"),
+    (2, 2, 8, "early", "selective"), (2, 3, 4, "on", "selective"),
+    (4, 2, 4, "off", "selective"), (4, 2, 8, "on", "selective"), (4, 2, 8, "on", "full"),
+    (4, 2, 8, "early", "selective"), (4, 2, 8, "early", "full"),
+])
+def test_loopback_step_matches_oracle(pp, m, n, x, rc):
+    _need_gpu()
+    ok, worst, xs = _run(pp, m, n, x, rc)
+    assert ok, worst
+    if x != "off":  # the tick plans really moved attention work
+        assert sum(s["passes_out"] for s in xs) > 0 and sum(s["bytes_sent"] for s in xs) > 0
+
+
+def test_loopback_gqa_through_the_exchange():
+    _need_gpu()
+    ok, worst, _ = _run(2, 2, 4, "on", "selective", kv_heads=2)
+    assert ok, worst
+
+
+@pytest.mark.parametrize("pp,m,n,rc", [(2, 2, 4, "selective"), (2, 1, 4, "full"), (4, 2, 8, "selective")])
+def test_loopback_interleaved_v2(pp, m, n, rc):
+    """Interleaved SlimPipe (v = 2): the stage links form a ring."""
+    _need_gpu()
+    ok, worst, _ = _run(pp, m, n, "off", rc, interleave=2)
+    assert ok, worst
+
+
+def test_loopback_rejects_vocab_parallel():
+    _need_gpu()
+    from paper_2504_14519_b200.runtime import LoopbackWorld, SlimPipeStep, StepConfig
+    cfg = StepConfig.c1(pp=2, layers=4, vocab=1024, vocab_parallel=True)
+    world = LoopbackWorld(2)
+    try:
+        with pytest.raises(RuntimeError, match="vocabulary"):
+            SlimPipeStep(cfg, 0, 2, loopback=world)
+    finally:
+        world.close()
