@@ -246,7 +246,10 @@ int sp_runtime_recompute(void* handle);
 /* Diagnostics: position in this rank's pass order of the first pass not yet
  * finished on the compute stream (-1: all done); out4 = kind, microbatch,
  * slice, stage of that pass.  Non-blocking. */
-int sp_runtime_progress(void* handle, int32_t* out4); /* policy in effect: 0 selective, 1 full */
+int sp_runtime_progress(void* handle, int32_t* out4);
+/* Diagnostics (any thread): index in this rank's pass order of the pass the
+ * host is enqueuing inside sp_runtime_step, -1 when it is not in a step. */
+int sp_runtime_enqueue_position(void* handle);
 int sp_runtime_param(void* handle, int layer, int which, float* host, int64_t count, int dir);
 /* {passes with outgoing transfers, passes with incoming transfers, bytes sent
  *  by this rank through the exchange in the last step} */

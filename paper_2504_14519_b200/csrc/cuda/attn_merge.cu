@@ -15,8 +15,9 @@ namespace sp {
 namespace {
 
 template <int D>
-__global__ void __launch_bounds__(256) attn_merge_kernel(const __nv_bfloat16* __restrict__ oa,
-                                                          const float* __restrict__ la,
+// oa/la may alias oo/lo (in-place merge, runtime.cpp): no __restrict__ on
+// them; each element is read before it is written by the same thread.
+__global__ void __launch_bounds__(256) attn_merge_kernel(const __nv_bfloat16* oa, const float* la,
                                                           const __nv_bfloat16* __restrict__ ob,
                                                           const float* __restrict__ lb, int64_t rows, int heads,
                                                           int64_t stride, __nv_bfloat16* oo, float* lo) {

@@ -27,6 +27,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -202,6 +203,7 @@ class Runtime {
   } xb[2];
   int64_t x_bytes_sent = 0;
   cudaEvent_t step_start = nullptr, step_end = nullptr;
+  std::atomic<int> enq_pos{-1};  // diagnostics: pass (index in order) the host is enqueuing, -1 idle
   size_t bytes_allocated = 0;
   std::vector<void*> allocations;
 
@@ -262,6 +264,8 @@ class Runtime {
     kvd = int64_t(c.kv_heads) * c.head_dim;
     qkv_w = qd + 2 * kvd;
     if (Ls % 128) return set_error(SP_ERR_UNSUPPORTED, "slice length must be a multiple of 128");
+    if (c.slices > SP_MAX_CHUNKS)  // the attention kernels carry one chunk-table entry per slice
+      return set_error(SP_ERR_UNSUPPORTED, "slices (%d) above SP_MAX_CHUNKS (%d)", c.slices, SP_MAX_CHUNKS);
 
     pipelab::GenConfig gc;
     gc.p = p;
@@ -349,11 +353,12 @@ class Runtime {
       }
     }
     if (vp) SP_CUDA(cudaStreamCreateWithFlags(&s_vocab, cudaStreamNonBlocking));
-    if (vp && std::getenv("SP_VOCAB_WARMUP")) SP_TRY(vocab_warmup());  // diagnostics
     SP_TRY(alloc_params());
-    SP_TRY(alloc_arena());
+    // everything but the arena first, so recompute=auto sizes the O/LSE stash
+    // against what is really left
     SP_TRY(alloc_workspace());
     SP_TRY(alloc_exchange());
+    SP_TRY(alloc_arena());
     SP_TRY(init_weights(c.seed));
     SP_CUDA(cudaStreamSynchronize(comp));
     return SP_OK;
@@ -415,7 +420,7 @@ class Runtime {
       vlink = make_nccl_link(nc_bwd);
       nc_bwd = nullptr;
     }
-    return SP_OK;
+    return warm_links();
   }
 
   // The same links on the single-GPU loopback transport (every rank a thread
@@ -443,20 +448,66 @@ class Runtime {
     return SP_OK;
   }
 
-  // Diagnostics for the open vocab-parallel stall: run each
-  // vocab collective once at its real message size before the arena exists,
-  // so NCCL's lazy connection setup happens here (same order on all ranks)
-  // instead of inside the asynchronously enqueued step.
-  int vocab_warmup() {
+  // NCCL connects peers lazily, at the first send/recv (or collective
+  // algorithm) of a communicator, with a host-side handshake that blocks
+  // until the peer's host reaches the same communicator.  The step enqueues
+  // asynchronously in each rank's own pass order, so first uses would meet in
+  // rank-dependent orders — a host-level cycle (the round-1 vocab-parallel /
+  // interleaved stall: both ranks blocked inside step enqueue).  Every
+  // communicator is therefore exercised here, in one global order:
+  //   1. stage links in increasing link index (link (a, a+1) = a; the ring's
+  //      wrap link = p-1), activations then gradients — per rank increasing,
+  //      so the waits form a chain, never a cycle;
+  //   2. the two exchange communicators: one group with every peer;
+  //   3. the vocabulary collectives at their real message sizes (the
+  //      algorithm, hence the connection, depends on the size).
+  int warm_links() {
+    cudaStream_t st = comp;
     void* buf = nullptr;
-    SP_CUDA(cudaMalloc(&buf, size_t(Ls) * size_t(h) * 4));
-    SP_CUDA(cudaMemsetAsync(buf, 0, size_t(Ls) * size_t(h) * 4, s_vocab));
-    float* f = static_cast<float*>(buf);
-    SP_TRY(vlink->broadcast(buf, Ls * h, ncclBfloat16, p - 1, s_vocab));
-    SP_TRY(vlink->all_reduce(f, Ls, ncclMax, s_vocab));
-    SP_TRY(vlink->all_reduce(f, 2 * Ls, ncclSum, s_vocab));
-    SP_TRY(vlink->reduce(f, Ls * h, p - 1, s_vocab));
-    SP_CUDA(cudaStreamSynchronize(s_vocab));
+    const size_t big = vp ? size_t(Ls) * size_t(h) * 4 : 4096;
+    SP_CUDA(cudaMalloc(&buf, big));
+    SP_CUDA(cudaMemsetAsync(buf, 0, big, st));
+    char* b = static_cast<char*>(buf);
+    auto pair = [&](Link* l, int peer) -> int {
+      SP_TRY(l->group_start());
+      SP_TRY(l->send(b, 4, ncclUint8, peer, st));
+      SP_TRY(l->recv(b + 64, 4, ncclUint8, peer, st));
+      return l->group_end();
+    };
+    const bool ring = v > 1;
+    const int prev_link = first_dev ? (ring ? p - 1 : -1) : rank - 1;  // link index of (prev, me)
+    const int next_link = (!last_dev || ring) ? rank : -1;              // link index of (me, next)
+    std::vector<std::pair<int, int>> mine;  // (link index, 0 = to prev / 1 = to next)
+    if (prev_link >= 0) mine.emplace_back(prev_link, 0);
+    if (next_link >= 0) mine.emplace_back(next_link, 1);
+    std::sort(mine.begin(), mine.end());
+    for (const auto& lk : mine) {
+      if (lk.second == 0) {
+        SP_TRY(pair(l_act_in.get(), 0));
+        SP_TRY(pair(l_grad_out.get(), 0));
+      } else {
+        SP_TRY(pair(l_act_out.get(), 1));
+        SP_TRY(pair(l_grad_in.get(), 1));
+      }
+    }
+    for (int k = 0; k < 2; ++k) {
+      if (!lx[k]) continue;
+      SP_TRY(lx[k]->group_start());
+      for (int q = 0; q < p; ++q)
+        if (q != rank) {
+          SP_TRY(lx[k]->send(b, 4, ncclUint8, q, st));
+          SP_TRY(lx[k]->recv(b + 64 + 8 * q, 4, ncclUint8, q, st));
+        }
+      SP_TRY(lx[k]->group_end());
+    }
+    if (vp) {
+      float* f = static_cast<float*>(buf);
+      SP_TRY(vlink->broadcast(buf, Ls * h, ncclBfloat16, p - 1, st));
+      SP_TRY(vlink->all_reduce(f, Ls, ncclMax, st));
+      SP_TRY(vlink->all_reduce(f, 2 * Ls, ncclSum, st));
+      SP_TRY(vlink->reduce(f, Ls * h, p - 1, st));
+    }
+    SP_CUDA(cudaStreamSynchronize(st));
     SP_CUDA(cudaFree(buf));
     return SP_OK;
   }
@@ -747,27 +798,7 @@ class Runtime {
 
   int alloc_arena() {
     const int64_t rows = int64_t(slots) * Ls;
-    if (cfg.recompute == 2) {  // auto: stash O/LSE only if it leaves room for everything else
-      size_t free_b = 0, total_b = 0;
-      SP_CUDA(cudaMemGetInfo(&free_b, &total_b));
-      const double stash_b = double(Lps) * rows * (qd * 2 + double(cfg.heads) * 4);
-      const double rest_b = double(rows) * h * 2 + double(Lps) * rows * kvd * 4 +                 // x, K/V
-                            double(v) * Lps * cfg.slices * Ls * kvd * 8 +                           // dK/dV acc
-                            double(Lps) * Ls * (6.0 * h + 3.0 * H) * 2 +                          // layer workspace
-                            (vp ? double(Ls) * double(Vs) * 6 + double(vslots.size()) * Ls * h * 2
-                                : last_dev ? double(Ls) * cfg.vocab * 4 * 2 : 0.0) +
-                            4.0 * double(1 << 30);  // logits (or the vocab shard's) + margin
-      stash = stash_b + rest_b < double(free_b);
-    }
     SP_TRY(alloc(&x_pool, rows * h));
-    if (stash) {
-      o_pool.assign(Lps, nullptr);
-      lse_pool.assign(Lps, nullptr);
-      for (int l = 0; l < Lps; ++l) {
-        SP_TRY(alloc(&o_pool[l], rows * qd));
-        SP_TRY(alloc(&lse_pool[l], rows * cfg.heads));
-      }
-    }
     k_pool.assign(Lps, nullptr);
     v_pool.assign(Lps, nullptr);
     dk_acc.assign(size_t(v) * Lps, nullptr);  // per local chunk and layer
@@ -782,6 +813,35 @@ class Runtime {
       SP_TRY(alloc(&dv_acc[l], acc_rows * kvd));
       SP_CUDA(cudaMemsetAsync(dk_acc[l], 0, acc_rows * kvd * 4, comp));
       SP_CUDA(cudaMemsetAsync(dv_acc[l], 0, acc_rows * kvd * 4, comp));
+    }
+    if (cfg.recompute == 2) {  // auto: stash O/LSE only if it fits beside everything allocated so far
+      size_t free_b = 0, total_b = 0;
+      SP_CUDA(cudaMemGetInfo(&free_b, &total_b));
+      const double stash_b = double(Lps) * rows * (qd * 2 + double(cfg.heads) * 4);
+      const double margin = 2.0 * double(1 << 30);  // cuBLASLt workspaces, NCCL buffers, allocator slack
+      stash = stash_b + margin < double(free_b);
+    }
+    if (stash) {
+      o_pool.assign(Lps, nullptr);
+      lse_pool.assign(Lps, nullptr);
+      const size_t n_before = allocations.size();
+      int rc = SP_OK;
+      for (int l = 0; l < Lps && rc == SP_OK; ++l) {
+        rc = alloc(&o_pool[l], rows * qd);
+        if (rc == SP_OK) rc = alloc(&lse_pool[l], rows * cfg.heads);
+      }
+      if (rc != SP_OK) {
+        if (cfg.recompute != 2) return rc;
+        // auto: the estimate was optimistic -> full recompute instead of failing
+        cudaGetLastError();
+        while (allocations.size() > n_before) {
+          cudaFree(allocations.back());
+          allocations.pop_back();
+        }
+        o_pool.clear();
+        lse_pool.clear();
+        stash = false;
+      }
     }
     free_slots.clear();
     for (int s = slots - 1; s >= 0; --s) free_slots.push_back(s);  // pop_back -> lowest first
@@ -1232,6 +1292,7 @@ class Runtime {
     SP_CUDA(cudaMemsetAsync(loss_dev, 0, 4, comp));
     for (pipelab::PassId id : order) {
       const pipelab::Pass& ps = sched.passes[id];
+      enq_pos = int(times.size());
       PassTime t{id, nullptr, nullptr};
       if (ps.kind == pipelab::PassKind::Forward || ps.kind == pipelab::PassKind::BackwardFused) {
         stage = ps.stage;
@@ -1252,6 +1313,7 @@ class Runtime {
       SP_TRY(adamw(master, w, grad, adam_m, adam_v, n_params, cfg.lr, 0.9f, 0.95f, 1e-8f, 0.1f, opt_step, comp));
       SP_CUDA(cudaMemsetAsync(grad, 0, n_params * 4, comp));
     }
+    enq_pos = -1;
     // drain comm streams into the compute stream so step_end covers them
     cudaEvent_t e1, e2;
     SP_CUDA(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
@@ -1335,6 +1397,8 @@ int sp_runtime_progress(void* handle, int32_t* out4) {
   }
   return -1;
 }
+
+int sp_runtime_enqueue_position(void* handle) { return static_cast<Runtime*>(handle)->enq_pos.load(); }
 
 int sp_runtime_sync(void* handle) {
   return sp::cuda_status(cudaStreamSynchronize(static_cast<Runtime*>(handle)->comp), "sync");
