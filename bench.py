@@ -74,6 +74,9 @@ def parse():
                     help="reference scenario JSON (scenario.cpp schema) for the model/run shape; overrides --model etc.")
     ap.add_argument("--gantt", default=None,
                     help="write the measured last-step timeline in the reference's Gantt JSON format (rank 0)")
+    ap.add_argument("--calibrate", default=None,
+                    help="fit the reference CostModel to the measured last step and write the calibrated "
+                         "simulate() prediction (exchange off/on/early) next to the measurement (rank 0)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -307,12 +310,19 @@ def main():
 
     # last timed step: per-pass busy (bubble) and attention kernel timings
     step_ms, passes = step.timeline()
+    per_dev = [passes]
+    if world > 1 and (args.gantt or args.calibrate):
+        per_dev = [None] * world
+        dist.all_gather_object(per_dev, passes)
+    calib = None
+    if args.calibrate and rank == 0 and not cfg.vocab_parallel:
+        from paper_2504_14519_b200 import calibrate as CAL
+        calib = CAL.predict(world, cfg.interleave, cfg.microbatches, cfg.slices, cfg.seq_len, per_dev)
+        calib["workload"] = workload_name(cfg, args.model)
+        with open(args.calibrate, "w") as f:
+            json.dump(calib, f, indent=1)
     if args.gantt:  # measured timeline in the reference's Gantt schema (gantt.cpp:52-106)
         from paper_2504_14519_b200 import plan as P
-        per_dev = [passes]
-        if world > 1:
-            per_dev = [None] * world
-            dist.all_gather_object(per_dev, passes)
         if rank == 0:
             with open(args.gantt, "w") as f:
                 f.write(P.gantt_measured_text(world, cfg.interleave, cfg.microbatches, cfg.slices, per_dev,
@@ -393,6 +403,8 @@ def main():
                        "l2": "inputs larger than L2 (per-step working set tens of GB)"},
             "mfu": mfu, "mfu_nominal": mfu_nominal, "mfu_peak_tflops": peak_tf,
             "bubble_fraction": bubble,
+            "bubble_simulated_calibrated": ({k: v["bubble"] for k, v in calib["simulated"].items()}
+                                            if calib else None),
             "peak_act_gb_per_gpu": arena_gb, "dkv_accum_gb_per_gpu": dkv_gb, "ledger_pred_gb_per_gpu": ledger_gb,
             "arena_slots": mem["slots"], "arena_high_water": mem["slots_high_water"],
             "roofline": {"kernel": f"sp_attn_{kind} (sm_100a tcgen05)", "bound": "tensor", "achieved": achieved,
