@@ -335,9 +335,21 @@ def main():
     busy_all = sum_over_ranks(busy)
     bubble = (world * makespan - busy_all) / busy_all if busy_all > 0 else 0.0
     at = step.attn_stats()
+    cs = step.comm_stats()
     mem = step.memory()
     at_tot = {k: sum_over_ranks(float(v)) for k, v in at.items()}
     launches_all = int(sum_over_ranks(float(launches)))
+    # stage P2P over NVLink: fastest message of any rank (link rate once the
+    # receive is posted) and the mean over all stage sends of the last step
+    link = None
+    if world > 1:
+        msg_b = cfg.slice_len * cfg.hidden * 2
+        fastest = -max_over_ranks(-cs["fastest_ms"] if cs["messages"] else -1e30)
+        n_msg, sum_ms = sum_over_ranks(cs["messages"]), sum_over_ranks(cs["send_ms"])
+        link = {"message_bytes": msg_b, "messages_per_step": int(n_msg),
+                "fastest_gbs": msg_b / (fastest / 1e3) / 1e9 if fastest > 0 else None,
+                "mean_gbs": n_msg * msg_b / (sum_ms / 1e3) / 1e9 if sum_ms > 0 else None,
+                "peak_gbs": 900.0, "timer": "CUDA events around each stage send on its stream (incl. waits)"}
 
     # ---- e2e through the public API: pinned host inputs, loss read back every step
     e2e = None
@@ -413,6 +425,7 @@ def main():
                          "attn_fwd_tflops": (at_tot["fwd_flops"] / max(1e-9, at_tot["fwd_ms"] / 1e3)) / 1e12,
                          "attn_bwd_tflops": (at_tot["bwd_flops"] / max(1e-9, at_tot["bwd_ms"] / 1e3)) / 1e12,
                          "attn_share_of_step": (at_tot["fwd_ms"] + at_tot["bwd_ms"]) / world / step_ms},
+            "stage_p2p": link,
             "gpu_launches": launches_all,
             "clocks": clk,
             "e2e": e2e,

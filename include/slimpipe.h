@@ -254,6 +254,10 @@ int sp_runtime_param(void* handle, int layer, int which, float* host, int64_t co
 /* {passes with outgoing transfers, passes with incoming transfers, bytes sent
  *  by this rank through the exchange in the last step} */
 int sp_runtime_exchange_stats(void* handle, int64_t* out3);
+/* Stage sends (activations / gradients) of the last step, timed with CUDA
+ * events on their streams: out4 = {messages, bytes, sum of send spans in ms,
+ * fastest send in ms}. */
+int sp_runtime_comm_stats(void* handle, double* out4);
 
 #ifdef __cplusplus
 }

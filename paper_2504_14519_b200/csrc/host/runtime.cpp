@@ -170,6 +170,19 @@ class Runtime {
   int out_idx = 0, gin_idx = 0, gout_idx = 0;
   std::vector<PassTime> times;
   std::vector<AttnTimer> attn_times;
+  // Event pools, created once and re-recorded every step: timing events
+  // (pass spans, attention and stage-send timers) in `tpool`, handed out in
+  // order from index 0 each step; `xev` is the one sync-only event behind
+  // link() and the stream hand-offs (a wait captures the event's state when
+  // it is enqueued, so re-recording it at once is safe).
+  std::vector<cudaEvent_t> tpool;
+  size_t tpool_i = 0;
+  cudaEvent_t xev = nullptr;
+  struct CommTimer {
+    cudaEvent_t a, b;
+    int64_t bytes;
+  };
+  std::vector<CommTimer> comm_times;  // stage sends of the last step
 
   // ---- attention workload redistribution (reference exchange.cpp /
   // simulator.cpp:56-108): per-pass transfer lists of this rank, two classes
@@ -211,14 +224,24 @@ class Runtime {
     if (comp) cudaStreamSynchronize(comp);
     for (void* a : allocations) cudaFree(a);
     if (nc_fwd) ncclCommDestroy(nc_fwd);
-    for (auto& t : times) {
-      cudaEventDestroy(t.start);
-      cudaEventDestroy(t.end);
+    for (cudaEvent_t e : tpool) cudaEventDestroy(e);
+    if (xev) cudaEventDestroy(xev);
+  }
+
+  int timing_event(cudaEvent_t* e) {
+    if (tpool_i == tpool.size()) {
+      cudaEvent_t ne;
+      SP_CUDA(cudaEventCreate(&ne));
+      tpool.push_back(ne);
     }
-    for (auto& t : attn_times) {
-      cudaEventDestroy(t.a);
-      cudaEventDestroy(t.b);
-    }
+    *e = tpool[tpool_i++];
+    return SP_OK;
+  }
+  // `to` waits for everything enqueued on `from` so far
+  int hand_off(cudaStream_t from, cudaStream_t to) {
+    SP_CUDA(cudaEventRecord(xev, from));
+    SP_CUDA(cudaStreamWaitEvent(to, xev, 0));
+    return SP_OK;
   }
 
   template <class T>
@@ -341,6 +364,7 @@ class Runtime {
     }
     SP_CUDA(cudaEventCreate(&step_start));
     SP_CUDA(cudaEventCreate(&step_end));
+    SP_CUDA(cudaEventCreateWithFlags(&xev, cudaEventDisableTiming));
 
     if (p > 1 && loop) SP_TRY(init_loop_links());
     else if (p > 1) SP_TRY(init_nccl_links(ids));
@@ -626,13 +650,19 @@ class Runtime {
     return it == xplan.end() ? nullptr : &it->second;
   }
 
-  // Event from `from` stream that `to` waits on (created / destroyed here).
-  int link(cudaStream_t from, cudaStream_t to) {
-    cudaEvent_t e;
-    SP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    SP_CUDA(cudaEventRecord(e, from));
-    SP_CUDA(cudaStreamWaitEvent(to, e, 0));
-    cudaEventDestroy(e);
+  int link(cudaStream_t from, cudaStream_t to) { return hand_off(from, to); }
+
+  // A stage message (one [Ls, h] bf16 slice) with CUDA events around the
+  // send on its stream: bytes / span is the link rate once the receiver's
+  // matching receive is posted (reported by sp_runtime_comm_stats).
+  int timed_send(Link* l, const void* buf, int peer, cudaStream_t st) {
+    CommTimer t{nullptr, nullptr, Ls * h * 2};
+    SP_TRY(timing_event(&t.a));
+    SP_TRY(timing_event(&t.b));
+    SP_CUDA(cudaEventRecord(t.a, st));
+    SP_TRY(l->send(buf, Ls * h, ncclBfloat16, peer, st));
+    SP_CUDA(cudaEventRecord(t.b, st));
+    comm_times.push_back(t);
     return SP_OK;
   }
 
@@ -922,8 +952,8 @@ class Runtime {
 
   int attn_fwd_timed(int l, const std::vector<int32_t>& rows, int causal, LayerWs& x) {
     AttnTimer t{};
-    SP_CUDA(cudaEventCreate(&t.a));
-    SP_CUDA(cudaEventCreate(&t.b));
+    SP_TRY(timing_event(&t.a));
+    SP_TRY(timing_event(&t.b));
     const int nch = int(rows.size());
     t.flops = attn_flops(nch, causal);
     t.kind = 0;
@@ -1038,13 +1068,9 @@ class Runtime {
       out_idx ^= 1;
       SP_CUDA(cudaStreamWaitEvent(comp, ev_out_free[b], 0));
       SP_TRY(stage_forward(k, i, out_buf[b], px, false));
-      cudaEvent_t done;
-      SP_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
-      SP_CUDA(cudaEventRecord(done, comp));
-      SP_CUDA(cudaStreamWaitEvent(s_act_out, done, 0));
-      SP_TRY(l_act_out->send(out_buf[b], Ls * h, ncclBfloat16, 1, s_act_out));
+      SP_TRY(hand_off(comp, s_act_out));
+      SP_TRY(timed_send(l_act_out.get(), out_buf[b], 1, s_act_out));
       SP_CUDA(cudaEventRecord(ev_out_free[b], s_act_out));
-      cudaEventDestroy(done);
     } else {
       SP_TRY(stage_forward(k, i, x_final, px, false));
       if (vp) {  // x_final is overwritten by later passes: normalise into the slice's vocab slot now
@@ -1108,8 +1134,8 @@ class Runtime {
       }
     }
     AttnTimer t{};
-    SP_CUDA(cudaEventCreate(&t.a));
-    SP_CUDA(cudaEventCreate(&t.b));
+    SP_TRY(timing_event(&t.a));
+    SP_TRY(timing_event(&t.b));
     t.flops = 2.5 * attn_flops(int(rows.size()), causal);
     t.kind = 1;
     SP_CUDA(cudaEventRecord(t.a, comp));
@@ -1212,11 +1238,7 @@ class Runtime {
       SP_CUDA(cudaStreamWaitEvent(s_grad_in, ev_gin_free[gb], 0));
       if (jit_recv) SP_TRY(link(comp, s_grad_in));
       SP_TRY(l_grad_in->recv(dx, Ls * h, ncclBfloat16, 1, s_grad_in));
-      cudaEvent_t got;
-      SP_CUDA(cudaEventCreateWithFlags(&got, cudaEventDisableTiming));
-      SP_CUDA(cudaEventRecord(got, s_grad_in));
-      SP_CUDA(cudaStreamWaitEvent(comp, got, 0));
-      cudaEventDestroy(got);
+      SP_TRY(hand_off(s_grad_in, comp));
       SP_CUDA(cudaEventRecord(t0, comp));
     } else {
       SP_CUDA(cudaEventRecord(t0, comp));
@@ -1252,12 +1274,8 @@ class Runtime {
       SP_TRY(embed_bwd(tokens + tok0, dx, G(emb), Ls, int(h), comp));
       if (gb >= 0) SP_CUDA(cudaEventRecord(ev_gin_free[gb], comp));
     } else {
-      cudaEvent_t done;
-      SP_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
-      SP_CUDA(cudaEventRecord(done, comp));
-      SP_CUDA(cudaStreamWaitEvent(s_grad_out, done, 0));
-      cudaEventDestroy(done);
-      SP_TRY(l_grad_out->send(dx, Ls * h, ncclBfloat16, 0, s_grad_out));
+      SP_TRY(hand_off(comp, s_grad_out));
+      SP_TRY(timed_send(l_grad_out.get(), dx, 0, s_grad_out));
       if (gb >= 0) {  // middle stage: dx lives in the receive buffer
         SP_CUDA(cudaEventRecord(ev_gin_free[gb], s_grad_out));
       } else {        // last stage: dx lives in gout_buf[gout_idx]
@@ -1272,16 +1290,10 @@ class Runtime {
   }
 
   int step(const int32_t* tok, const int32_t* tgt, int on_device, int flags, float* loss_out) {
-    for (auto& t : times) {
-      cudaEventDestroy(t.start);
-      cudaEventDestroy(t.end);
-    }
     times.clear();
-    for (auto& t : attn_times) {
-      cudaEventDestroy(t.a);
-      cudaEventDestroy(t.b);
-    }
     attn_times.clear();
+    comm_times.clear();
+    tpool_i = 0;
     slots_high_water = 0;
     x_bytes_sent = 0;
     const int64_t ntok = int64_t(cfg.microbatches) * cfg.seq_len;
@@ -1299,8 +1311,8 @@ class Runtime {
         cur = (stage - 1) / p;
         lbase = cur * Lps;
       }
-      SP_CUDA(cudaEventCreate(&t.start));
-      SP_CUDA(cudaEventCreate(&t.end));
+      SP_TRY(timing_event(&t.start));
+      SP_TRY(timing_event(&t.end));
       if (ps.kind == pipelab::PassKind::Forward) SP_TRY(run_forward(id, ps.microbatch, ps.slice, t.start));
       else if (ps.kind == pipelab::PassKind::VocabForward) SP_TRY(run_vocab_fwd(ps.microbatch, ps.slice, t.start));
       else if (ps.kind == pipelab::PassKind::VocabBackward) SP_TRY(run_vocab_bwd(ps.microbatch, ps.slice, t.start));
@@ -1315,21 +1327,13 @@ class Runtime {
     }
     enq_pos = -1;
     // drain comm streams into the compute stream so step_end covers them
-    cudaEvent_t e1, e2;
-    SP_CUDA(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
-    SP_CUDA(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming));
-    for (cudaStream_t st : {s_act_in, s_act_out, s_grad_in, s_grad_out}) {
-      SP_CUDA(cudaEventRecord(e1, st));
-      SP_CUDA(cudaStreamWaitEvent(comp, e1, 0));
-    }
+    for (cudaStream_t st : {s_act_in, s_act_out, s_grad_in, s_grad_out}) SP_TRY(hand_off(st, comp));
     for (int c = 0; c < 2; ++c)
       if (cx[c]) {
         SP_TRY(link(cx[c], comp));
         SP_TRY(link(rx[c], comp));
       }
     if (s_vocab) SP_TRY(link(s_vocab, comp));
-    cudaEventDestroy(e1);
-    cudaEventDestroy(e2);
     SP_CUDA(cudaEventRecord(step_end, comp));
     if (loss_out) {
       float l = 0.f;
@@ -1441,6 +1445,25 @@ int sp_runtime_attn_stats(void* handle, double* out6) {
     out6[3 * t.kind + 1] += t.flops;
     out6[3 * t.kind + 2] += 1;
   }
+  return SP_OK;
+}
+
+// Stage sends of the last step: out4 = {messages, bytes, total ms, fastest
+// message ms} (CUDA events on the send streams).
+int sp_runtime_comm_stats(void* handle, double* out4) {
+  Runtime* rt = static_cast<Runtime*>(handle);
+  double n = 0, bytes = 0, ms = 0, best = 0;
+  for (const auto& t : rt->comm_times) {
+    float x = 0.f;
+    cudaError_t e = cudaEventSynchronize(t.b);
+    if (e != cudaSuccess) return sp::cuda_status(e, "comm stats");
+    cudaEventElapsedTime(&x, t.a, t.b);
+    n += 1;
+    bytes += double(t.bytes);
+    ms += x;
+    best = (best == 0 || x < best) ? x : best;
+  }
+  out4[0] = n, out4[1] = bytes, out4[2] = ms, out4[3] = best;
   return SP_OK;
 }
 

@@ -138,6 +138,8 @@ def _lib():
     lib.sp_loopback_destroy.argtypes = [C.c_void_p]
     lib.sp_loopback_errors.argtypes = [C.c_void_p]
     lib.sp_runtime_exchange_stats.argtypes = [C.c_void_p, C.POINTER(C.c_int64)]
+    lib.sp_runtime_comm_stats.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
+    lib.sp_runtime_enqueue_position.argtypes = [C.c_void_p]
     lib.sp_runtime_destroy.argtypes = [C.c_void_p]
     lib.sp_runtime_step.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_float)]
     lib.sp_runtime_sync.argtypes = [C.c_void_p]
@@ -336,6 +338,12 @@ class SlimPipeStep:
         b = (C.c_int64 * 3)()
         N.check(_lib().sp_runtime_exchange_stats(self._h, b), "sp_runtime_exchange_stats")
         return {"passes_out": b[0], "passes_in": b[1], "bytes_sent": b[2]}
+
+    def comm_stats(self) -> dict:
+        """Stage sends of the last step (CUDA events on the send streams)."""
+        b = (C.c_double * 4)()
+        N.check(_lib().sp_runtime_comm_stats(self._h, b), "sp_runtime_comm_stats")
+        return {"messages": int(b[0]), "bytes": b[1], "send_ms": b[2], "fastest_ms": b[3]}
 
     # ---- parameter access (tests) ----
     def _param_shape(self, which: str):
