@@ -23,11 +23,13 @@
 #include "kernels.hpp"
 #include "sm100.cuh"
 
+#include <cstdlib>
+
 
 namespace sp {
 namespace {
 
-constexpr int D = 128, BQ = 64, BK = 128, NS = 3;
+constexpr int D = 128, BQ = 64, BK = 128;
 constexpr int kThreads = 480;
 constexpr int kCompute = 256;
 constexpr int kDrain = 128;
@@ -45,16 +47,19 @@ struct Params {
   int acc_row[SP_MAX_CHUNKS];
 };
 
+// NS: Q/dO ring depth; NDS: dS^T tiles (2 = element math of pair j never
+// waits for the dQ MMA of pair j-1 to finish reading the previous tile)
+template <int NS, int NDS>
 struct alignas(1024) Smem {
   __nv_bfloat16 k[BK * D];
   __nv_bfloat16 v[BK * D];
   __nv_bfloat16 q[NS][BQ * D];
   __nv_bfloat16 dout[NS][BQ * D];
-  __nv_bfloat16 ds[BK * BQ];
+  __nv_bfloat16 ds[NDS][BK * BQ];
   float stage[1][BQ * D];  // dQ tile [q][d] on their way to the TMA reduce
 };
-static_assert(sizeof(Smem) % 1024 == 0, "operand tiles stay 1024-aligned");
 
+template <int NS>
 struct Ctl {  // static shared memory: statistics and barriers
   float lse2[NS][BQ];
   float delta[NS][BQ];
@@ -70,13 +75,15 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
                : "memory");
 }
 
+template <int NS, int NDS>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_bwd_d128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
                          const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                          const __grid_constant__ CUtensorMap tm_dq, const __grid_constant__ Params prm) {
   extern __shared__ uint8_t smem_raw[];
-  Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ __align__(16) Ctl ctl;
+  static_assert(sizeof(Smem<NS, NDS>) % 1024 == 0, "operand tiles stay 1024-aligned");
+  auto& sm = *reinterpret_cast<Smem<NS, NDS>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(16) Ctl<NS> ctl;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int kt = blockIdx.x, kvh = blockIdx.y;
   const int key0 = kt * BK;
@@ -153,10 +160,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr uint32_t id_s = idesc_bf16_f32(BK, BQ, false, false);  // K Q^T, V dO^T
       constexpr uint32_t id_acc = idesc_bf16_f32(BK, D, false, true);  // P^T dO, dS^T Q
       constexpr uint32_t id_dq = idesc_bf16_f32(D, BQ, true, true);    // K^T dS^T
-      const uint32_t k_a = smem_u32(sm.k), v_a = smem_u32(sm.v), ds_a = smem_u32(sm.ds);
+      const uint32_t k_a = smem_u32(sm.k), v_a = smem_u32(sm.v);
       // descriptor bases; per-step offsets are added to the low word (address >> 4)
       const uint64_t dk_k = smem_desc_sw128(k_a, 16, 1024), dv_k = smem_desc_sw128(v_a, 16, 1024);
-      const uint64_t dk_mn = smem_desc_sw128(k_a, kSlabK * 2, 1024), dds_mn = smem_desc_sw128(ds_a, kSlabK * 2, 1024);
+      const uint64_t dk_mn = smem_desc_sw128(k_a, kSlabK * 2, 1024);
       mbar_wait(&ctl.kv_full, 0);
       if (warp == 1) {
         for (int j = 0; j < n_pairs; ++j) {
@@ -184,6 +191,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&ctl.pds_ready, j & 1);
           tc_fence_after();
           const uint64_t dq_mn = smem_desc_sw128(smem_u32(sm.q[s]), kSlabQ * 2, 1024);
+          const uint64_t dds_mn = smem_desc_sw128(smem_u32(sm.ds[NDS == 1 ? 0 : b]), kSlabK * 2, 1024);
           const uint64_t ddo_mn = smem_desc_sw128(smem_u32(sm.dout[s]), kSlabQ * 2, 1024);
           // dQ^T = K^T dS^T into pair j's (consumed) dP^T columns (K = 128 keys)
 #pragma unroll
@@ -216,7 +224,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int r = quarter * 32 + lane;
     const int ctid = cw * 32 + lane;  // 0..255
     const uint32_t lane_off = uint32_t(quarter * 32) << 16;
-    const uint32_t ds_a = smem_u32(sm.ds);
     const int key_rel = key0 - off + r;
     const int c0 = wg * 32;
 
@@ -258,7 +265,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         pk[x / 2] = pack_bf16(p0, p1);
         dk[x / 2] = pack_bf16(dd.x, dd.y);
       }
-      if (j > 0) mbar_wait(&ctl.pds_free, (j - 1) & 1);
+      if (NDS == 1 && j > 0) mbar_wait(&ctl.pds_free, (j - 1) & 1);
+      const uint32_t ds_a = smem_u32(sm.ds[NDS == 1 ? 0 : b]);
       // P^T / dS^T (packed bf16) over this WG's own S^T columns: A operands of
       // the dV / dK TS-UMMAs; dS^T also to smem: B operand of dQ^T = K^T dS^T.
       tmem_st16(tmem + lane_off + b * 128 + wg * 32, pk);
@@ -370,11 +378,24 @@ int attn_bwd_d128(const void* q, int64_t q_rows, int64_t q_stride, const void* k
       !make_tmap_bf16(&tv, v_pool, uint64_t(kv_stride), uint64_t(pool_rows), uint64_t(kv_stride), BK) ||
       !make_tmap_f32(&tdq, dq_acc, uint64_t(heads) * D, uint64_t(q_rows), uint64_t(heads) * D, D, BQ))
     return set_error(SP_ERR_CUDA, "attn_bwd_d128: cuTensorMapEncodeTiled failed (alignment?)");
-  const size_t smem = sizeof(Smem) + 1024;
-  if (int rc = set_smem_once(reinterpret_cast<const void*>(attn_bwd_d128_kernel), smem, "attn_bwd_d128: set smem"))
-    return rc;
-  attn_bwd_d128_kernel<<<dim3(prm.total_kv / BK, kv_heads), kThreads, smem, st>>>(tq, tdo, tk, tv, tdq, prm);
-  count_launch(1);
+  // SP_BWD_VARIANT (A/B measurement only, read once): 0 = NS 3 / one dS
+  // tile, 1 = NS 2 / one dS tile, 2 = NS 2 / two dS tiles (NS 3 / two tiles
+  // exceeds the 227 KB per-CTA shared memory)
+  static const int variant = [] {
+    const char* e = std::getenv("SP_BWD_VARIANT");
+    return e ? std::atoi(e) : 0;
+  }();
+  auto launch = [&](auto kern, size_t smem) -> int {
+    if (int rc = set_smem_once(reinterpret_cast<const void*>(kern), smem, "attn_bwd_d128: set smem")) return rc;
+    kern<<<dim3(prm.total_kv / BK, kv_heads), kThreads, smem, st>>>(tq, tdo, tk, tv, tdq, prm);
+    count_launch(1);
+    return SP_OK;
+  };
+  int rc = SP_OK;
+  if (variant == 1) rc = launch(attn_bwd_d128_kernel<2, 1>, sizeof(Smem<2, 1>) + 1024);
+  else if (variant == 2) rc = launch(attn_bwd_d128_kernel<2, 2>, sizeof(Smem<2, 2>) + 1024);
+  else rc = launch(attn_bwd_d128_kernel<3, 1>, sizeof(Smem<3, 1>) + 1024);
+  if (rc) return rc;
   return cuda_status(cudaGetLastError(), "attn_bwd_d128 launch");
 }
 

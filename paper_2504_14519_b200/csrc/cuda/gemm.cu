@@ -45,7 +45,7 @@ int lt_status(cublasStatus_t s, const char* what) {
 }  // namespace
 
 int gemm(bool trans_a, bool trans_b, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, const void* B,
-         int64_t ldb, void* C, int64_t ldc, bool c_f32, float alpha, float beta, cudaStream_t st) {
+         int64_t ldb, void* C, int64_t ldc, bool c_f32, float alpha, float beta, cudaStream_t st, const void* c_in) {
   if (M <= 0 || N <= 0 || K <= 0) return SP_OK;
   State& S = state();
   std::lock_guard<std::mutex> g(S.mu);
@@ -85,7 +85,9 @@ int gemm(bool trans_a, bool trans_b, int64_t M, int64_t N, int64_t K, const void
   }
   const Plan& p = it->second;
   count_library_launch();
-  return lt_status(cublasLtMatmul(S.lt, p.op, &alpha, B, p.a, A, p.b, &beta, C, p.c, C, p.c, &p.algo, ws,
+  // D = alpha op(A) op(B) + beta C_in: the residual input is read in place
+  // (no separate copy into the output first)
+  return lt_status(cublasLtMatmul(S.lt, p.op, &alpha, B, p.a, A, p.b, &beta, c_in ? c_in : C, p.c, C, p.c, &p.algo, ws,
                                   S.ws_bytes, st),
                    "matmul");
 }

@@ -73,7 +73,9 @@ int attn_bwd_d128(const void* q, int64_t q_rows, int64_t q_stride, const void* k
 //   C[M,N] = alpha * op(A) op(B) + beta * C
 //   A is [M,K] (or [K,M] when trans_a), B is [K,N] (or [N,K] when trans_b),
 //   lda/ldb/ldc are row pitches in elements.  c_f32 selects an fp32 C/D.
+//   c_in (optional): read the beta term from c_in instead of C (same layout).
 int gemm(bool trans_a, bool trans_b, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, const void* B,
-         int64_t ldb, void* C, int64_t ldc, bool c_f32, float alpha, float beta, cudaStream_t st);
+         int64_t ldb, void* C, int64_t ldc, bool c_f32, float alpha, float beta, cudaStream_t st,
+         const void* c_in = nullptr);
 
 }  // namespace sp

@@ -99,9 +99,30 @@ struct Channel {
   std::atomic<uint64_t> sseq{0}, rseq{0};
 };
 
-// The sender's copy: destination and size come from the receiver's mailbox
-// (published before the ready flag the sender's stream waited on).
-__global__ void loop_copy_kernel(const Mail* mail, const uint8_t* __restrict__ src, int64_t bytes, int* err) {
+__device__ __forceinline__ void spin_until(const uint32_t* flag, uint32_t value) {
+  uint32_t v;
+  while (true) {
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    if (int32_t(v - value) >= 0) break;
+    __nanosleep(256);
+  }
+}
+
+// A stream-ordered wait that occupies one small CTA (like an NCCL kernel)
+// rather than a hardware channel: a front-end stream wait would also stall
+// every other stream that shares its channel (CUDA_DEVICE_MAX_CONNECTIONS),
+// which with a dozen streams per rank can close a cycle between ranks.
+__global__ void loop_wait_kernel(const uint32_t* flag, uint32_t value) {
+  if (threadIdx.x == 0) spin_until(flag, value);
+}
+
+// The sender's copy: waits for the receive to be posted (ready flag), then
+// takes destination and size from the receiver's mailbox (published before
+// that flag was raised).
+__global__ void loop_copy_kernel(const uint32_t* ready, uint32_t value, const Mail* mail,
+                                 const uint8_t* __restrict__ src, int64_t bytes, int* err) {
+  if (threadIdx.x == 0) spin_until(ready, value);
+  __syncthreads();
   const volatile Mail* vm = mail;
   uint8_t* dst = static_cast<uint8_t*>(vm->dst);
   if (vm->bytes != bytes) {
@@ -256,24 +277,19 @@ class LoopLink final : public Link {
   }
   int wait_done(int peer, uint64_t seq, cudaStream_t st) {
     Channel& c = chan(peer, me_);
-    return mem_rc(memops().wait(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(c.done + seq % kSlots),
-                                cuuint32_t(seq + 1), CU_STREAM_WAIT_VALUE_GEQ),
-                  "wait(done)");
+    loop_wait_kernel<<<1, 32, 0, st>>>(c.done + seq % kSlots, uint32_t(seq + 1));
+    count_launch();
+    return cuda_status(cudaGetLastError(), "loopback wait");
   }
   int do_send(const void* buf, int64_t bytes, int peer, cudaStream_t st) {
     Channel& c = chan(me_, peer);
     const uint64_t seq = c.sseq++;
     const int slot = int(seq % kSlots);
-    if (int rc = mem_rc(memops().wait(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(c.ready + slot),
-                                      cuuint32_t(seq + 1), CU_STREAM_WAIT_VALUE_GEQ),
-                        "wait(ready)"))
-      return rc;
-    if (bytes > 0) {
-      const int blocks = int(std::min<int64_t>(296, (bytes / 16 + 255) / 256 + 1));
-      loop_copy_kernel<<<blocks, 256, 0, st>>>(c.mail + slot, static_cast<const uint8_t*>(buf), bytes, w_->err);
-      count_launch();
-      if (int rc = cuda_status(cudaGetLastError(), "loopback copy")) return rc;
-    }
+    const int blocks = int(std::min<int64_t>(296, (bytes / 16 + 255) / 256 + 1));
+    loop_copy_kernel<<<blocks, 256, 0, st>>>(c.ready + slot, uint32_t(seq + 1), c.mail + slot,
+                                             static_cast<const uint8_t*>(buf), bytes, w_->err);
+    count_launch();
+    if (int rc = cuda_status(cudaGetLastError(), "loopback copy")) return rc;
     return mem_rc(memops().write(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(c.done + slot),
                                  cuuint32_t(seq + 1), CU_STREAM_WRITE_VALUE_DEFAULT),
                   "write(done)");

@@ -1020,13 +1020,11 @@ class Runtime {
     SP_TRY(rope_qkv_fwd(qkv, Ls, cfg.heads, cfg.kv_heads, cfg.head_dim, pos0, rope_cos, rope_sin, x.q, qd,
                         k_pool[l] + int64_t(slot) * Ls * kvd, v_pool[l] + int64_t(slot) * Ls * kvd, kvd, comp));
     if (!(recompute && stash)) SP_TRY(attention_forward(l, k, i, x, px));
-    SP_CUDA(cudaMemcpyAsync(x.x_mid, x.x_in, Ls * h * 2, cudaMemcpyDeviceToDevice, comp));
-    SP_TRY(gemm(false, true, Ls, h, qd, x.o, qd, W(P.wo), qd, x.x_mid, h, false, 1.f, 1.f, comp));
+    SP_TRY(gemm(false, true, Ls, h, qd, x.o, qd, W(P.wo), qd, x.x_mid, h, false, 1.f, 1.f, comp, x.x_in));
     SP_TRY(rmsnorm_fwd(x.x_mid, W(P.mlp_norm), x.xn2, x.rstd2, Ls, int(h), cfg.norm_eps, comp));
     SP_TRY(gemm(false, true, Ls, 2 * H, h, x.xn2, h, W(P.wgu), h, x.gu, 2 * H, false, 1.f, 0.f, comp));
     SP_TRY(swiglu_fwd(x.gu, x.act, Ls, int(H), comp));
-    SP_CUDA(cudaMemcpyAsync(x_out, x.x_mid, Ls * h * 2, cudaMemcpyDeviceToDevice, comp));
-    SP_TRY(gemm(false, true, Ls, h, H, x.act, H, W(P.wd), H, x_out, h, false, 1.f, 1.f, comp));
+    SP_TRY(gemm(false, true, Ls, h, H, x.act, H, W(P.wd), H, x_out, h, false, 1.f, 1.f, comp, x.x_mid));
     return SP_OK;
   }
 

@@ -12,9 +12,11 @@
 //   * NCCL (one process per GPU, NVLink/NVSwitch) — the production path;
 //   * loopback (every rank a host thread of ONE process on ONE GPU): a
 //     receive publishes its destination and raises a device flag (stream
-//     memory op); the matching send waits for that flag on its own stream,
-//     copies straight into the destination and raises a "done" flag that the
-//     receive's stream waits on.  No host-side rendezvous, so the host enqueue
+//     memory write); the matching send's copy kernel waits for that flag,
+//     copies straight into the destination, and a "done" flag is raised that
+//     a one-CTA wait kernel on the receive's stream spins on (kernels, like
+//     NCCL's, not front-end stream waits: those would block every stream
+//     sharing the hardware channel).  No host-side rendezvous, so the host enqueue
 //     never blocks on a peer — the same progress semantics as NCCL.  It lets
 //     a single-GPU box run (and test) the multi-stage protocol bit for bit.
 #pragma once
