@@ -225,8 +225,8 @@ int sp_runtime_create(const sp_model_config* cfg, const void* nccl_ids, void** h
  * its rank's runtime with sp_runtime_create_loopback on a shared world and
  * calls sp_runtime_step concurrently.  Stage links and exchange transfers
  * then move through device-side flags + copy kernels instead of NCCL, with
- * the same send/recv order and group semantics (csrc/host/transport.hpp).
- * Vocabulary parallelism (collectives) is not offered on it. */
+ * the same send/recv order and group semantics (csrc/host/transport.hpp);
+ * the vocabulary collectives run as gathers/broadcasts over it. */
 int sp_loopback_create(int ranks, void** world);
 int sp_loopback_destroy(void* world);
 int sp_loopback_errors(void* world); /* message size mismatches seen so far (0 = none) */

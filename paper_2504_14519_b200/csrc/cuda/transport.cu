@@ -141,6 +141,13 @@ __global__ void loop_copy_kernel(const uint32_t* ready, uint32_t value, const Ma
   }
 }
 
+// out[i] = op(out[i], in[i]) (op 0 sum, 1 max) — the combine step of the
+// loopback collectives
+__global__ void loop_combine_kernel(float* out, const float* in, int64_t n, int op) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    out[i] = op ? fmaxf(out[i], in[i]) : out[i] + in[i];
+}
+
 }  // namespace
 
 struct LoopWorld {
@@ -203,6 +210,11 @@ int dt_bytes(ncclDataType_t dt) {
     default: return 8;
   }
 }
+
+#define SP_LOOP_TRY(x)        \
+  do {                        \
+    if (int rc_ = (x)) return rc_; \
+  } while (0)
 
 class LoopLink final : public Link {
  public:
@@ -301,6 +313,66 @@ class LoopLink final : public Link {
   int me_;
   bool grouping_ = false;
   std::vector<Op> ops_;
+  float* scratch_ = nullptr;  // collectives: peers' contributions at the root
+  int64_t scratch_n_ = 0;
+
+ public:
+  ~LoopLink() override {
+    if (scratch_) cudaFree(scratch_);
+  }
+  // Collectives over point-to-point messages (vocabulary parallelism on one
+  // GPU): the root gathers every peer's buffer, combines, and (all-reduce /
+  // broadcast) sends the result back.  Same arithmetic as a reduction tree
+  // up to the fp32 summation order.
+  int broadcast(void* buf, int64_t count, ncclDataType_t dt, int root, cudaStream_t st) override {
+    const int n = int(mem_.size());
+    if (me_ == root) {
+      SP_LOOP_TRY(group_start());
+      for (int q = 0; q < n; ++q)
+        if (q != root) SP_LOOP_TRY(send(buf, count, dt, q, st));
+      return group_end();
+    }
+    return recv(buf, count, dt, root, st);
+  }
+  int reduce(float* buf, int64_t count, int root, cudaStream_t st) override {
+    return gather_combine(buf, count, 0, root, st, false);
+  }
+  int all_reduce(float* buf, int64_t count, ncclRedOp_t op, cudaStream_t st) override {
+    if (op != ncclSum && op != ncclMax) return set_error(SP_ERR_UNSUPPORTED, "loopback all_reduce: sum or max only");
+    return gather_combine(buf, count, op == ncclMax ? 1 : 0, 0, st, true);
+  }
+
+ private:
+  int gather_combine(float* buf, int64_t count, int op, int root, cudaStream_t st, bool back) {
+    const int n = int(mem_.size());
+    if (me_ != root) {
+      SP_LOOP_TRY(send(buf, count, ncclFloat32, root, st));
+      return back ? recv(buf, count, ncclFloat32, root, st) : SP_OK;
+    }
+    const int64_t need = int64_t(n - 1) * count;
+    if (need > scratch_n_) {
+      if (scratch_) cudaFree(scratch_);
+      scratch_ = nullptr;
+      if (cudaError_t e = cudaMalloc(&scratch_, size_t(std::max<int64_t>(need, 1)) * 4))
+        return cuda_status(e, "loopback collective scratch");
+      scratch_n_ = need;
+    }
+    SP_LOOP_TRY(group_start());
+    for (int q = 0, x = 0; q < n; ++q)
+      if (q != root) SP_LOOP_TRY(recv(scratch_ + int64_t(x++) * count, count, ncclFloat32, q, st));
+    SP_LOOP_TRY(group_end());
+    const int blocks = int(std::min<int64_t>(592, (count + 255) / 256 + 1));
+    for (int x = 0; x < n - 1; ++x) {
+      loop_combine_kernel<<<blocks, 256, 0, st>>>(buf, scratch_ + int64_t(x) * count, count, op);
+      count_launch();
+    }
+    SP_LOOP_TRY(cuda_status(cudaGetLastError(), "loopback combine"));
+    if (!back) return SP_OK;
+    SP_LOOP_TRY(group_start());
+    for (int q = 0; q < n; ++q)
+      if (q != root) SP_LOOP_TRY(send(buf, count, ncclFloat32, q, st));
+    return group_end();
+  }
 };
 
 }  // namespace

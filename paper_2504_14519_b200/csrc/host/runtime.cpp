@@ -454,7 +454,6 @@ class Runtime {
   int init_loop_links() {
     if (loop_world_size(loop) != p) return set_error(SP_ERR_INVALID, "loopback world has %d ranks, pp = %d",
                                                      loop_world_size(loop), p);
-    if (vp) return set_error(SP_ERR_UNSUPPORTED, "loopback transport: vocabulary parallelism needs collectives");
     const bool ring = v > 1;
     const int nx = (rank + 1) % p, pv = (rank + p - 1) % p;
     if (!last_dev || ring) {
@@ -469,6 +468,7 @@ class Runtime {
     for (int r = 0; r < p; ++r) all[size_t(r)] = r;
     if (!xplan.empty() || cfg.exchange_mode != 0)
       for (int k = 0; k < 2; ++k) lx[k] = make_loop_link(loop, 2 + k, all, rank);
+    if (vp) vlink = make_loop_link(loop, 4, all, rank);  // collectives over p2p (transport.cu)
     return SP_OK;
   }
 

@@ -18,10 +18,10 @@ from test_attn_gpu import _need_gpu
 pytestmark = pytest.mark.gpu
 
 
-def _run(pp, m, n, exchange, recompute, kv_heads=4, interleave=1):
+def _run(pp, m, n, exchange, recompute, kv_heads=4, interleave=1, **kw):
     from paper_2504_14519_b200.runtime import LoopbackWorld, SlimPipeStep, StepConfig
     cfg = StepConfig.c1(pp=pp, microbatches=m, slices=n, layers=2 * pp * interleave, exchange=exchange,
-                        seq_len=1024 * n, recompute=recompute, kv_heads=kv_heads, interleave=interleave)
+                        seq_len=1024 * n, recompute=recompute, kv_heads=kv_heads, interleave=interleave, **kw)
     world = LoopbackWorld(pp)
     steps = [SlimPipeStep(cfg, r, pp, loopback=world) for r in range(pp)]
     try:
@@ -67,13 +67,11 @@ def test_loopback_interleaved_v2(pp, m, n, rc):
     assert ok, worst
 
 
-def test_loopback_rejects_vocab_parallel():
+@pytest.mark.parametrize("pp,m,n,rc", [(2, 2, 4, "selective"), (4, 2, 8, "full")])
+def test_loopback_vocab_parallel(pp, m, n, rc):
+    """Vocabulary parallelism (reference place_vocab distribute=true,
+    simulator.cpp:414-522): LM head and cross entropy split over all stages;
+    the collectives run as gathers/broadcasts over the loopback links."""
     _need_gpu()
-    from paper_2504_14519_b200.runtime import LoopbackWorld, SlimPipeStep, StepConfig
-    cfg = StepConfig.c1(pp=2, layers=4, vocab=1024, vocab_parallel=True)
-    world = LoopbackWorld(2)
-    try:
-        with pytest.raises(RuntimeError, match="vocabulary"):
-            SlimPipeStep(cfg, 0, 2, loopback=world)
-    finally:
-        world.close()
+    ok, worst, _ = _run(pp, m, n, "off", rc, vocab=1024, vocab_parallel=True)
+    assert ok, worst
