@@ -116,13 +116,12 @@ __global__ void loop_wait_kernel(const uint32_t* flag, uint32_t value) {
   if (threadIdx.x == 0) spin_until(flag, value);
 }
 
-// The sender's copy: waits for the receive to be posted (ready flag), then
-// takes destination and size from the receiver's mailbox (published before
-// that flag was raised).
-__global__ void loop_copy_kernel(const uint32_t* ready, uint32_t value, const Mail* mail,
-                                 const uint8_t* __restrict__ src, int64_t bytes, int* err) {
-  if (threadIdx.x == 0) spin_until(ready, value);
-  __syncthreads();
+// The sender's copy, launched behind a loop_wait_kernel on the receive's
+// ready flag (one spinning CTA per waiting stream, never a grid of them: a
+// grid of spinners could fill every SM and starve the kernel it waits for);
+// destination and size come from the receiver's mailbox, published before
+// that flag was raised.
+__global__ void loop_copy_kernel(const Mail* mail, const uint8_t* __restrict__ src, int64_t bytes, int* err) {
   const volatile Mail* vm = mail;
   uint8_t* dst = static_cast<uint8_t*>(vm->dst);
   if (vm->bytes != bytes) {
@@ -298,9 +297,9 @@ class LoopLink final : public Link {
     const uint64_t seq = c.sseq++;
     const int slot = int(seq % kSlots);
     const int blocks = int(std::min<int64_t>(296, (bytes / 16 + 255) / 256 + 1));
-    loop_copy_kernel<<<blocks, 256, 0, st>>>(c.ready + slot, uint32_t(seq + 1), c.mail + slot,
-                                             static_cast<const uint8_t*>(buf), bytes, w_->err);
-    count_launch();
+    loop_wait_kernel<<<1, 32, 0, st>>>(c.ready + slot, uint32_t(seq + 1));
+    loop_copy_kernel<<<blocks, 256, 0, st>>>(c.mail + slot, static_cast<const uint8_t*>(buf), bytes, w_->err);
+    count_launch(2);
     if (int rc = cuda_status(cudaGetLastError(), "loopback copy")) return rc;
     return mem_rc(memops().write(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(c.done + slot),
                                  cuuint32_t(seq + 1), CU_STREAM_WRITE_VALUE_DEFAULT),

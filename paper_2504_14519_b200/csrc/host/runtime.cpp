@@ -153,6 +153,7 @@ class Runtime {
   float *dq_acc = nullptr, *delta_ws = nullptr, *logits = nullptr, *rstd_f = nullptr, *loss_dev = nullptr;
   int32_t *tokens = nullptr, *targets = nullptr;
 
+  int device = 0;  // the runtime's GPU: every entry point makes it current (callers may be other threads)
   cudaStream_t comp = nullptr;
   ncclComm_t nc_fwd = nullptr, nc_bwd = nullptr;
   // Stage links: one 2-rank communicator and one stream per (neighbour,
@@ -349,6 +350,7 @@ class Runtime {
       return set_error(SP_ERR_INVALID, "vocab_parallel must be 0 or 1");
     }
 
+    SP_CUDA(cudaGetDevice(&device));  // host-side validation above runs without a GPU
     SP_CUDA(cudaStreamCreateWithFlags(&comp, cudaStreamNonBlocking));
     for (cudaStream_t* st : {&s_act_in, &s_act_out, &s_grad_in, &s_grad_out})
       SP_CUDA(cudaStreamCreateWithFlags(st, cudaStreamNonBlocking));
@@ -1288,6 +1290,7 @@ class Runtime {
   }
 
   int step(const int32_t* tok, const int32_t* tgt, int on_device, int flags, float* loss_out) {
+    SP_CUDA(cudaSetDevice(device));
     times.clear();
     attn_times.clear();
     comm_times.clear();
@@ -1376,6 +1379,7 @@ int sp_runtime_create_loopback(const sp_model_config* cfg, void* world, void** h
 }
 
 int sp_runtime_destroy(void* handle) {
+  if (handle) cudaSetDevice(static_cast<Runtime*>(handle)->device);
   delete static_cast<Runtime*>(handle);
   return SP_OK;
 }
@@ -1389,6 +1393,7 @@ int sp_runtime_step(void* handle, const int32_t* tokens, const int32_t* targets,
 // not completed on the compute stream, or -1 when all have; writes that
 // pass's (kind, microbatch, slice, stage) to out4.
 int sp_runtime_progress(void* handle, int32_t* out4) {
+  if (handle) cudaSetDevice(static_cast<Runtime*>(handle)->device);
   Runtime* rt = static_cast<Runtime*>(handle);
   for (std::size_t x = 0; x < rt->times.size(); ++x) {
     if (cudaEventQuery(rt->times[x].end) == cudaErrorNotReady) {
@@ -1403,6 +1408,7 @@ int sp_runtime_progress(void* handle, int32_t* out4) {
 int sp_runtime_enqueue_position(void* handle) { return static_cast<Runtime*>(handle)->enq_pos.load(); }
 
 int sp_runtime_sync(void* handle) {
+  if (handle) cudaSetDevice(static_cast<Runtime*>(handle)->device);
   return sp::cuda_status(cudaStreamSynchronize(static_cast<Runtime*>(handle)->comp), "sync");
 }
 
@@ -1411,6 +1417,7 @@ void* sp_runtime_stream(void* handle) { return static_cast<Runtime*>(handle)->co
 // Step time (ms between step_start and step_end) and per-pass busy times.
 // out: [0] step ms, then per pass of device_order: pass id, start ms, end ms.
 int sp_runtime_timeline(void* handle, double* out, int cap) {
+  if (handle) cudaSetDevice(static_cast<Runtime*>(handle)->device);
   Runtime* rt = static_cast<Runtime*>(handle);
   cudaError_t e = cudaEventSynchronize(rt->step_end);
   if (e != cudaSuccess) return sp::cuda_status(e, "timeline");
@@ -1433,6 +1440,7 @@ int sp_runtime_timeline(void* handle, double* out, int cap) {
 // Attention kernel timing of the last step: out = {fwd_ms, fwd_flops, fwd_launches,
 // bwd_ms, bwd_flops, bwd_launches}.
 int sp_runtime_attn_stats(void* handle, double* out6) {
+  if (handle) cudaSetDevice(static_cast<Runtime*>(handle)->device);
   Runtime* rt = static_cast<Runtime*>(handle);
   for (int x = 0; x < 6; ++x) out6[x] = 0.0;
   for (const auto& t : rt->attn_times) {
@@ -1449,6 +1457,7 @@ int sp_runtime_attn_stats(void* handle, double* out6) {
 // Stage sends of the last step: out4 = {messages, bytes, total ms, fastest
 // message ms} (CUDA events on the send streams).
 int sp_runtime_comm_stats(void* handle, double* out4) {
+  if (handle) cudaSetDevice(static_cast<Runtime*>(handle)->device);
   Runtime* rt = static_cast<Runtime*>(handle);
   double n = 0, bytes = 0, ms = 0, best = 0;
   for (const auto& t : rt->comm_times) {
@@ -1498,6 +1507,7 @@ int sp_runtime_memory(void* handle, int64_t* out7) {
 // which: 0 attn_norm 1 wqkv 2 wo 3 mlp_norm 4 wgu 5 wd 6 embedding 7 final_norm 8 head
 // dir: 0 device->host (master weights), 1 host->device (sets master + bf16), 2 grads device->host
 int sp_runtime_param(void* handle, int layer, int which, float* host, int64_t count, int dir) {
+  if (handle) cudaSetDevice(static_cast<Runtime*>(handle)->device);
   Runtime* rt = static_cast<Runtime*>(handle);
   int64_t off = -1, n = 0;
   const int64_t h = rt->h, H = rt->H;

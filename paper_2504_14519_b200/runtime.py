@@ -201,11 +201,14 @@ class LoopbackWorld:
     def errors(self) -> int:
         return int(_lib().sp_loopback_errors(self._h))
 
-    def run(self, fn):
+    def run(self, fn, timeout: float | None = None, steps=None):
         """fn(rank) on one host thread per rank (concurrently, as the ranks'
         enqueues must be); returns the per-rank results, re-raising the
-        first exception."""
+        first exception.  With `timeout` (seconds) a stuck step raises
+        TimeoutError naming, per rank of `steps`, the pass the host is
+        enqueuing and the first pass not finished on the device."""
         import threading
+        import time
         out, err = [None] * self.ranks, [None] * self.ranks
 
         def body(r):
@@ -213,11 +216,17 @@ class LoopbackWorld:
                 out[r] = fn(r)
             except BaseException as e:  # noqa: BLE001 - re-raised below
                 err[r] = e
-        ths = [threading.Thread(target=body, args=(r,)) for r in range(self.ranks)]
+        ths = [threading.Thread(target=body, args=(r,), daemon=True) for r in range(self.ranks)]
         for t in ths:
             t.start()
+        t_end = None if timeout is None else time.monotonic() + timeout
         for t in ths:
-            t.join()
+            t.join(None if t_end is None else max(0.0, t_end - time.monotonic()))
+        if any(t.is_alive() for t in ths):
+            where = [] if steps is None else [
+                f"rank {r}: host enqueuing pass #{_lib().sp_runtime_enqueue_position(s._h)}, device at {s.progress()}"
+                for r, s in enumerate(steps)]
+            raise TimeoutError(f"loopback step did not finish in {timeout} s; " + "; ".join(where))
         for e in err:
             if e is not None:
                 raise e

@@ -27,7 +27,7 @@ def _run(pp, m, n, exchange, recompute, kv_heads=4, interleave=1, **kw):
     try:
         tok, tgt = SP.inputs(cfg)
         torch.cuda.synchronize()
-        losses = world.run(lambda r: steps[r].step(tok, tgt, optimizer=False))
+        losses = world.run(lambda r: steps[r].step(tok, tgt, optimizer=False), timeout=120, steps=steps)
         assert world.errors() == 0, "loopback transport saw mismatched message sizes"
         allv = [SP.gather_rank(steps[r], cfg, losses[r]) for r in range(pp)]
         ok, worst, _ = SP.compare(cfg, allv, tok, tgt)
