@@ -18,8 +18,11 @@ void count_library_launch(int n = 1);  // cuBLASLt calls
 int embed_fwd(const int32_t* tok, const void* table, void* out, int64_t rows, int dim, cudaStream_t st);
 int embed_bwd(const int32_t* tok, const void* dy, float* dtable, int64_t rows, int dim, cudaStream_t st);
 int rmsnorm_fwd(const void* x, const void* w, void* y, float* rstd, int64_t rows, int dim, float eps, cudaStream_t st);
+// dw (may be null) += the weight gradient: with dw_ws (rmsnorm_dw_ws_floats
+// floats) in a fixed block order (bitwise reproducible), else by atomics
 int rmsnorm_bwd(const void* dy, const void* x, const void* w, const float* rstd, const void* dx_in, void* dx_out,
-                float* dw, int64_t rows, int dim, cudaStream_t st);
+                float* dw, int64_t rows, int dim, cudaStream_t st, float* dw_ws = nullptr);
+int64_t rmsnorm_dw_ws_floats(int64_t rows, int dim);
 int rope_table(float* cs, float* sn, int64_t positions, int d, double theta, cudaStream_t st);
 int rope_qkv_fwd(const void* qkv, int64_t rows, int heads, int kv_heads, int d, int64_t pos0, const float* cs,
                  const float* sn, void* q_out, int64_t q_stride, void* k_out, void* v_out, int64_t kv_stride,

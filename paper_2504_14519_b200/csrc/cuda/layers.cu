@@ -112,7 +112,7 @@ __global__ void rmsnorm_fwd_k(const bf16* __restrict__ x, const bf16* __restrict
 template <int kMaxVec>
 __global__ void rmsnorm_bwd_k(const bf16* __restrict__ dy, const bf16* __restrict__ x, const bf16* __restrict__ w,
                               const float* __restrict__ rstd, const bf16* dx_in, bf16* dx_out, float* __restrict__ dw,
-                              int64_t rows, int dim, int rows_per_block) {
+                              float* __restrict__ dw_part, int64_t rows, int dim, int rows_per_block) {
   float dwp[kMaxVec][8];
 #pragma unroll
   for (int i = 0; i < kMaxVec; ++i)
@@ -162,10 +162,27 @@ __global__ void rmsnorm_bwd_k(const bf16* __restrict__ dy, const bf16* __restric
 #pragma unroll
   for (int i = 0; i < kMaxVec; ++i) {
     const int c = (threadIdx.x + i * blockDim.x) * 8;
-    if (c < dim)
+    if (c < dim) {
+      if (dw_part) {  // deterministic: this block's partial row, summed in block order by rmsnorm_dw_sum_k
+        float* dst = dw_part + int64_t(blockIdx.x) * dim + c;
+        reinterpret_cast<float4*>(dst)[0] = make_float4(dwp[i][0], dwp[i][1], dwp[i][2], dwp[i][3]);
+        reinterpret_cast<float4*>(dst)[1] = make_float4(dwp[i][4], dwp[i][5], dwp[i][6], dwp[i][7]);
+      } else {
 #pragma unroll
-      for (int e = 0; e < 8; ++e) atomicAdd(dw + c + e, dwp[i][e]);
+        for (int e = 0; e < 8; ++e) atomicAdd(dw + c + e, dwp[i][e]);
+      }
+    }
   }
+}
+
+// dw[c] += sum over blocks b (in order) of part[b][c]: a fixed summation order,
+// so the weight gradient is bitwise reproducible run to run.
+__global__ void rmsnorm_dw_sum_k(const float* __restrict__ part, float* __restrict__ dw, int blocks, int dim) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= dim) return;
+  float acc = 0.f;
+  for (int b = 0; b < blocks; ++b) acc += part[int64_t(b) * dim + c];
+  dw[c] += acc;
 }
 
 // ---- RoPE (rotate-half convention over head_dim) ---------------------------------
@@ -531,15 +548,23 @@ int rmsnorm_fwd(const void* x, const void* w, void* y, float* rstd, int64_t rows
 }
 
 int rmsnorm_bwd(const void* dy, const void* x, const void* w, const float* rstd, const void* dx_in, void* dx_out,
-                float* dw, int64_t rows, int dim, cudaStream_t st) {
+                float* dw, int64_t rows, int dim, cudaStream_t st, float* dw_ws) {
   int threads = ((dim / 8 + 3) / 4 + 31) / 32 * 32;
   if (threads < 32) threads = 32;
   const int rpb = 32;
-  rmsnorm_bwd_k<4><<<unsigned((rows + rpb - 1) / rpb), threads, 0, st>>>(
-      (const bf16*)dy, (const bf16*)x, (const bf16*)w, rstd, (const bf16*)dx_in, (bf16*)dx_out, dw, rows, dim, rpb);
+  const unsigned blocks = unsigned((rows + rpb - 1) / rpb);
+  float* part = dw ? dw_ws : nullptr;
+  rmsnorm_bwd_k<4><<<blocks, threads, 0, st>>>((const bf16*)dy, (const bf16*)x, (const bf16*)w, rstd,
+                                               (const bf16*)dx_in, (bf16*)dx_out, dw, part, rows, dim, rpb);
   count_launch();
+  if (part) {
+    rmsnorm_dw_sum_k<<<unsigned((dim + 255) / 256), 256, 0, st>>>(part, dw, int(blocks), dim);
+    count_launch();
+  }
   return cuda_status(cudaGetLastError(), "rmsnorm_bwd");
 }
+
+int64_t rmsnorm_dw_ws_floats(int64_t rows, int dim) { return (rows + 31) / 32 * int64_t(dim); }
 
 int rope_table(float* cs, float* sn, int64_t positions, int d, double theta, cudaStream_t st) {
   rope_table_k<<<grid_for(positions * (d / 2), 256), 256, 0, st>>>(cs, sn, positions, d / 2, theta);

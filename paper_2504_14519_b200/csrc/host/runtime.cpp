@@ -150,6 +150,7 @@ class Runtime {
   bf16raw* gin_buf[2] = {nullptr, nullptr};  // gradients received from s+1
   bf16raw* gout_buf[2] = {nullptr, nullptr}; // gradients sent to s-1 (dx)
   float *rope_cos = nullptr, *rope_sin = nullptr;  // [seq_len][d/2]
+  float* norm_ws = nullptr;  // per-block RMSNorm dW partials (deterministic weight gradient)
   float *dq_acc = nullptr, *delta_ws = nullptr, *logits = nullptr, *rstd_f = nullptr, *loss_dev = nullptr;
   int32_t *tokens = nullptr, *targets = nullptr;
 
@@ -914,6 +915,7 @@ class Runtime {
     SP_TRY(alloc(&rope_sin, cfg.seq_len * (cfg.head_dim / 2)));
     SP_TRY(rope_table(rope_cos, rope_sin, cfg.seq_len, cfg.head_dim, double(cfg.rope_theta), comp));
     SP_TRY(alloc(&dq_acc, Ls * qd));
+    SP_TRY(alloc(&norm_ws, rmsnorm_dw_ws_floats(Ls, int(h))));
     SP_TRY(alloc(&delta_ws, 2 * int64_t(cfg.heads) * Ls));
     SP_TRY(alloc(&loss_dev, 1));
     SP_TRY(alloc(&tokens, int64_t(cfg.microbatches) * cfg.seq_len));
@@ -1107,7 +1109,7 @@ class Runtime {
     SP_TRY(swiglu_bwd(tmp_H, x.gu, tmp_2H, Ls, int(H), comp));                                      // d_gu
     SP_TRY(gemm(false, false, Ls, h, 2 * H, tmp_2H, 2 * H, W(P.wgu), h, tmp_h, h, false, 1.f, 0.f, comp));  // dxn2
     SP_TRY(gemm(true, false, 2 * H, h, Ls, tmp_2H, 2 * H, x.xn2, h, G(P.wgu), h, true, 1.f, 1.f, comp));    // dWgu
-    SP_TRY(rmsnorm_bwd(tmp_h, x.x_mid, W(P.mlp_norm), x.rstd2, dx, dx, G(P.mlp_norm), Ls, int(h), comp));
+    SP_TRY(rmsnorm_bwd(tmp_h, x.x_mid, W(P.mlp_norm), x.rstd2, dx, dx, G(P.mlp_norm), Ls, int(h), comp, norm_ws));
     // attention output projection
     SP_TRY(gemm(false, false, Ls, qd, h, dx, h, W(P.wo), qd, tmp_h, qd, false, 1.f, 0.f, comp));   // d_o
     SP_TRY(gemm(true, false, h, qd, Ls, dx, h, x.o, qd, G(P.wo), qd, true, 1.f, 1.f, comp));         // dWo
@@ -1171,7 +1173,7 @@ class Runtime {
                         cfg.head_dim, pos0, rope_cos, rope_sin, dqkv, 1, comp));
     SP_TRY(gemm(false, false, Ls, h, qkv_w, dqkv, qkv_w, W(P.wqkv), h, tmp_h, h, false, 1.f, 0.f, comp));   // dxn
     SP_TRY(gemm(true, false, qkv_w, h, Ls, dqkv, qkv_w, x.xn, h, G(P.wqkv), h, true, 1.f, 1.f, comp));      // dWqkv
-    SP_TRY(rmsnorm_bwd(tmp_h, x.x_in, W(P.attn_norm), x.rstd1, dx, dx, G(P.attn_norm), Ls, int(h), comp));
+    SP_TRY(rmsnorm_bwd(tmp_h, x.x_in, W(P.attn_norm), x.rstd1, dx, dx, G(P.attn_norm), Ls, int(h), comp, norm_ws));
     return SP_OK;
   }
 
@@ -1253,7 +1255,7 @@ class Runtime {
       if (vp) {  // dX of the final hidden state = sum of the shards' partials (VocabBackward, just before)
         SP_TRY(rmsnorm_fwd(x_final, W(final_norm), xf, rstd_f, Ls, int(h), cfg.norm_eps, comp));
         SP_TRY(f32_to_bf16(vdxf, tmp_h, Ls * h, comp));
-        SP_TRY(rmsnorm_bwd(tmp_h, x_final, W(final_norm), rstd_f, nullptr, dx, G(final_norm), Ls, int(h), comp));
+        SP_TRY(rmsnorm_bwd(tmp_h, x_final, W(final_norm), rstd_f, nullptr, dx, G(final_norm), Ls, int(h), comp, norm_ws));
       }
     }
     if (stage == nst && !vp) {
@@ -1265,7 +1267,7 @@ class Runtime {
       SP_TRY(cross_entropy(logits, targets + tok0, Ls, int(V), scale, dlogits, loss_dev, comp));
       SP_TRY(gemm(false, false, Ls, h, V, dlogits, V, W(head), h, tmp_h, h, false, 1.f, 0.f, comp));  // dxf
       SP_TRY(gemm(true, false, V, h, Ls, dlogits, V, xf, h, G(head), h, true, 1.f, 1.f, comp));        // dWhead
-      SP_TRY(rmsnorm_bwd(tmp_h, x_final, W(final_norm), rstd_f, nullptr, dx, G(final_norm), Ls, int(h), comp));
+      SP_TRY(rmsnorm_bwd(tmp_h, x_final, W(final_norm), rstd_f, nullptr, dx, G(final_norm), Ls, int(h), comp, norm_ws));
     } else if (stage < nst) {
       SP_TRY(stage_forward(k, i, top, px, true));
     }
