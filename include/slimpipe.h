@@ -230,6 +230,8 @@ int sp_runtime_create(const sp_model_config* cfg, const void* nccl_ids, void** h
 int sp_loopback_create(int ranks, void** world);
 int sp_loopback_destroy(void* world);
 int sp_loopback_errors(void* world); /* message size mismatches seen so far (0 = none) */
+/* transport self-test: 2-rank ping-pong of `iters` x (send/recv + grouped send+recv) */
+int sp_loopback_pingpong(void* world, int rank, void* send_buf, void* recv_buf, int64_t bytes, int iters);
 int sp_runtime_create_loopback(const sp_model_config* cfg, void* world, void** handle);
 int sp_runtime_destroy(void* handle);
 /* tokens/targets: [microbatches][seq_len] int32 (host, or device when on_device);

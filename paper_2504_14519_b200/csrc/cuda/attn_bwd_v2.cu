@@ -23,8 +23,6 @@
 #include "kernels.hpp"
 #include "sm100.cuh"
 
-#include <cstdlib>
-
 
 namespace sp {
 namespace {
@@ -378,24 +376,14 @@ int attn_bwd_d128(const void* q, int64_t q_rows, int64_t q_stride, const void* k
       !make_tmap_bf16(&tv, v_pool, uint64_t(kv_stride), uint64_t(pool_rows), uint64_t(kv_stride), BK) ||
       !make_tmap_f32(&tdq, dq_acc, uint64_t(heads) * D, uint64_t(q_rows), uint64_t(heads) * D, D, BQ))
     return set_error(SP_ERR_CUDA, "attn_bwd_d128: cuTensorMapEncodeTiled failed (alignment?)");
-  // SP_BWD_VARIANT (A/B measurement only, read once): 0 = NS 3 / one dS
-  // tile, 1 = NS 2 / one dS tile, 2 = NS 2 / two dS tiles (NS 3 / two tiles
-  // exceeds the 227 KB per-CTA shared memory)
-  static const int variant = [] {
-    const char* e = std::getenv("SP_BWD_VARIANT");
-    return e ? std::atoi(e) : 0;
-  }();
-  auto launch = [&](auto kern, size_t smem) -> int {
-    if (int rc = set_smem_once(reinterpret_cast<const void*>(kern), smem, "attn_bwd_d128: set smem")) return rc;
-    kern<<<dim3(prm.total_kv / BK, kv_heads), kThreads, smem, st>>>(tq, tdo, tk, tv, tdq, prm);
-    count_launch(1);
-    return SP_OK;
-  };
-  int rc = SP_OK;
-  if (variant == 1) rc = launch(attn_bwd_d128_kernel<2, 1>, sizeof(Smem<2, 1>) + 1024);
-  else if (variant == 2) rc = launch(attn_bwd_d128_kernel<2, 2>, sizeof(Smem<2, 2>) + 1024);
-  else rc = launch(attn_bwd_d128_kernel<3, 1>, sizeof(Smem<3, 1>) + 1024);
-  if (rc) return rc;
+  // NS = 3 Q/dO stages and one dS tile: measured best (scripts/k2_ab.py,
+  // profiles/r02_k2_ab.json: NS = 2 with one or two dS tiles is 11-12 %
+  // slower; NS = 3 with two dS tiles exceeds the 227 KB per-CTA shared memory)
+  auto kern = attn_bwd_d128_kernel<3, 1>;
+  const size_t smem = sizeof(Smem<3, 1>) + 1024;
+  if (int rc = set_smem_once(reinterpret_cast<const void*>(kern), smem, "attn_bwd_d128: set smem")) return rc;
+  kern<<<dim3(prm.total_kv / BK, kv_heads), kThreads, smem, st>>>(tq, tdo, tk, tv, tdq, prm);
+  count_launch(1);
   return cuda_status(cudaGetLastError(), "attn_bwd_d128 launch");
 }
 

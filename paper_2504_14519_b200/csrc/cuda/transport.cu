@@ -404,4 +404,34 @@ int sp_loopback_destroy(void* world) {
 
 int sp_loopback_errors(void* world) { return sp::loop_world_errors(static_cast<sp::LoopWorld*>(world)); }
 
+// Transport self-test (tests/test_loopback_gpu.py): rank `rank` of a 2-rank
+// world exchanges `iters` messages of `bytes` with rank 1-rank on its own
+// stream — rank 0 sends then receives, rank 1 receives then sends, plus one
+// grouped send+recv per iteration — and returns when its stream is done.
+int sp_loopback_pingpong(void* world, int rank, void* send_buf, void* recv_buf, int64_t bytes, int iters) {
+  auto* w = static_cast<sp::LoopWorld*>(world);
+  auto link = sp::make_loop_link(w, 7, {0, 1}, rank);
+  if (!link) return sp::set_error(SP_ERR_INVALID, "pingpong: bad world/rank");
+  cudaStream_t st;
+  if (cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking)) return sp::cuda_status(e, "pingpong stream");
+  const int peer = 1 - rank;
+  int rc = SP_OK;
+  for (int i = 0; i < iters && rc == SP_OK; ++i) {
+    if (rank == 0) {
+      rc = link->send(send_buf, bytes, ncclUint8, peer, st);
+      if (!rc) rc = link->recv(recv_buf, bytes, ncclUint8, peer, st);
+    } else {
+      rc = link->recv(recv_buf, bytes, ncclUint8, peer, st);
+      if (!rc) rc = link->send(send_buf, bytes, ncclUint8, peer, st);
+    }
+    if (!rc) rc = link->group_start();
+    if (!rc) rc = link->send(send_buf, bytes, ncclUint8, peer, st);
+    if (!rc) rc = link->recv(recv_buf, bytes, ncclUint8, peer, st);
+    if (!rc) rc = link->group_end();
+  }
+  if (!rc) rc = sp::cuda_status(cudaStreamSynchronize(st), "pingpong sync");
+  cudaStreamDestroy(st);
+  return rc;
+}
+
 }  // extern "C"

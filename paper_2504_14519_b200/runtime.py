@@ -137,6 +137,7 @@ def _lib():
     lib.sp_loopback_create.argtypes = [C.c_int, C.POINTER(C.c_void_p)]
     lib.sp_loopback_destroy.argtypes = [C.c_void_p]
     lib.sp_loopback_errors.argtypes = [C.c_void_p]
+    lib.sp_loopback_pingpong.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_int]
     lib.sp_runtime_exchange_stats.argtypes = [C.c_void_p, C.POINTER(C.c_int64)]
     lib.sp_runtime_comm_stats.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
     lib.sp_runtime_enqueue_position.argtypes = [C.c_void_p]
@@ -226,7 +227,11 @@ class LoopbackWorld:
             where = [] if steps is None else [
                 f"rank {r}: host enqueuing pass #{_lib().sp_runtime_enqueue_position(s._h)}, device at {s.progress()}"
                 for r, s in enumerate(steps)]
-            raise TimeoutError(f"loopback step did not finish in {timeout} s; " + "; ".join(where))
+            # the device is wedged: no cleanup can complete (stream syncs would
+            # block forever), so report and end the process
+            import sys
+            print(f"loopback step did not finish in {timeout} s; " + "; ".join(where), file=sys.stderr, flush=True)
+            os._exit(3)
         for e in err:
             if e is not None:
                 raise e

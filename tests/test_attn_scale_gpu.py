@@ -89,7 +89,9 @@ def test_attention_at_bench_scale_matches_oracle(name, Ls, heads, kv, n, L, hs):
         lse_h = lse[h].double().cpu().numpy()
         # forward: sampled rows
         ro, rl = O.port_fwd_rows(qh, kh, vh, True, rsel)
-        e_o = float(np.max(np.abs(oh[rsel] - ro) / np.maximum(1.0, np.abs(ro))))
+        # O: the reference's max(1,|x|) metric is near-vacuous when a row
+        # averages 1M random values (|O| ~ 1e-3), so also row-relative
+        e_o = max(float(np.max(np.abs(oh[rsel] - ro) / np.maximum(1.0, np.abs(ro)))), _rowwise_err(oh[rsel], ro))
         e_l = float(np.max(np.abs(lse_h[rsel] - rl)))
         # backward: dQ rows (this head) and dK/dV keys (this head's share)
         rdq = O.port_bwd_rows(qh, kh, vh, oh, doh, lse_h, True, rsel)
