@@ -232,6 +232,9 @@ int sp_loopback_destroy(void* world);
 int sp_loopback_errors(void* world); /* message size mismatches seen so far (0 = none) */
 /* transport self-test: 2-rank ping-pong of `iters` x (send/recv + grouped send+recv) */
 int sp_loopback_pingpong(void* world, int rank, void* send_buf, void* recv_buf, int64_t bytes, int iters);
+/* the same protocol with both ranks enqueued from one host thread */
+int sp_loopback_pingpong_1thread(void* world, void* buf0, void* buf1, void* rbuf0, void* rbuf1, int64_t bytes,
+                                 int iters);
 int sp_runtime_create_loopback(const sp_model_config* cfg, void* world, void** handle);
 int sp_runtime_destroy(void* handle);
 /* tokens/targets: [microbatches][seq_len] int32 (host, or device when on_device);

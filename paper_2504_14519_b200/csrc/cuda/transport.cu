@@ -1,8 +1,6 @@
 // Transports behind sp::Link (csrc/host/transport.hpp): NCCL for one process
 // per GPU, and the single-GPU loopback that runs every rank as a host thread
 // of one process (tests and single-GPU boxes).
-#include <cuda.h>
-
 #include <algorithm>
 #include <atomic>
 #include <memory>
@@ -60,30 +58,6 @@ class NcclLink final : public Link {
 };
 
 // ------------------------------------------------------------------ loopback
-using WaitFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
-using WriteFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
-
-struct MemOps {
-  WaitFn wait = nullptr;
-  WriteFn write = nullptr;
-};
-
-const MemOps& memops() {
-  static MemOps m;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      m.wait = reinterpret_cast<WaitFn>(p);
-    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      m.write = reinterpret_cast<WriteFn>(p);
-  });
-  return m;
-}
-
 constexpr int kSlots = 4096;  // messages in flight per (communicator, sender, receiver)
 constexpr int kComms = 8;
 
@@ -105,6 +79,18 @@ __device__ __forceinline__ void spin_until(const uint32_t* flag, uint32_t value)
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
     if (int32_t(v - value) >= 0) break;
     __nanosleep(256);
+  }
+}
+
+// Raise a flag from the stream (everything before it on the stream is
+// complete when this kernel runs): a kernel, not a stream memory operation —
+// a memop that must wait for the stream's previous kernel holds the whole
+// hardware channel, and a channel shared with a peer's spinning wait closes
+// a cycle.
+__global__ void loop_signal_kernel(uint32_t* flag, uint32_t value) {
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(value) : "memory");
   }
 }
 
@@ -159,8 +145,7 @@ struct LoopWorld {
 };
 
 LoopWorld* loop_world_create(int ranks) {
-  const MemOps& m = memops();
-  if (!m.wait || !m.write || ranks < 1) return nullptr;
+  if (ranks < 1) return nullptr;
   auto w = std::make_unique<LoopWorld>();
   w->n = ranks;
   const size_t nch = size_t(kComms) * ranks * ranks;
@@ -271,10 +256,6 @@ class LoopLink final : public Link {
   }
   Channel& chan(int src_local, int dst_local) { return w_->at(id_, mem_[size_t(src_local)], mem_[size_t(dst_local)]); }
 
-  static int mem_rc(CUresult r, const char* what) {
-    return r == CUDA_SUCCESS ? SP_OK : set_error(SP_ERR_CUDA, "loopback %s failed (CUresult %d)", what, int(r));
-  }
-
   int post(void* buf, int64_t bytes, int peer, cudaStream_t st, uint64_t* seq_out) {
     Channel& c = chan(peer, me_);
     const uint64_t seq = c.rseq++;
@@ -282,9 +263,9 @@ class LoopLink final : public Link {
     c.mail[slot].dst = buf;
     c.mail[slot].bytes = bytes;
     *seq_out = seq;
-    return mem_rc(memops().write(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(c.ready + slot),
-                                 cuuint32_t(seq + 1), CU_STREAM_WRITE_VALUE_DEFAULT),
-                  "write(ready)");
+    loop_signal_kernel<<<1, 32, 0, st>>>(c.ready + slot, uint32_t(seq + 1));
+    count_launch();
+    return cuda_status(cudaGetLastError(), "loopback post");
   }
   int wait_done(int peer, uint64_t seq, cudaStream_t st) {
     Channel& c = chan(peer, me_);
@@ -301,9 +282,9 @@ class LoopLink final : public Link {
     loop_copy_kernel<<<blocks, 256, 0, st>>>(c.mail + slot, static_cast<const uint8_t*>(buf), bytes, w_->err);
     count_launch(2);
     if (int rc = cuda_status(cudaGetLastError(), "loopback copy")) return rc;
-    return mem_rc(memops().write(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(c.done + slot),
-                                 cuuint32_t(seq + 1), CU_STREAM_WRITE_VALUE_DEFAULT),
-                  "write(done)");
+    loop_signal_kernel<<<1, 32, 0, st>>>(c.done + slot, uint32_t(seq + 1));
+    count_launch();
+    return cuda_status(cudaGetLastError(), "loopback done");
   }
 
   LoopWorld* w_;
@@ -403,6 +384,33 @@ int sp_loopback_destroy(void* world) {
 }
 
 int sp_loopback_errors(void* world) { return sp::loop_world_errors(static_cast<sp::LoopWorld*>(world)); }
+
+// Both ranks of the self-test enqueued from ONE host thread (rank 0's
+// operations, then rank 1's — enqueue never blocks), then both streams
+// synchronised: isolates the device protocol from host threading.
+int sp_loopback_pingpong_1thread(void* world, void* buf0, void* buf1, void* rbuf0, void* rbuf1, int64_t bytes,
+                                 int iters) {
+  auto* w = static_cast<sp::LoopWorld*>(world);
+  auto l0 = sp::make_loop_link(w, 6, {0, 1}, 0), l1 = sp::make_loop_link(w, 6, {0, 1}, 1);
+  if (!l0 || !l1) return sp::set_error(SP_ERR_INVALID, "pingpong: bad world");
+  cudaStream_t s0, s1;
+  cudaStreamCreateWithFlags(&s0, cudaStreamNonBlocking);
+  cudaStreamCreateWithFlags(&s1, cudaStreamNonBlocking);
+  int rc = SP_OK;
+  for (int i = 0; i < iters && rc == SP_OK; ++i) {
+    rc = l0->send(buf0, bytes, ncclUint8, 1, s0);
+    if (!rc) rc = l0->recv(rbuf0, bytes, ncclUint8, 1, s0);
+  }
+  for (int i = 0; i < iters && rc == SP_OK; ++i) {
+    rc = l1->recv(rbuf1, bytes, ncclUint8, 0, s1);
+    if (!rc) rc = l1->send(buf1, bytes, ncclUint8, 0, s1);
+  }
+  if (!rc) rc = sp::cuda_status(cudaStreamSynchronize(s0), "pingpong sync 0");
+  if (!rc) rc = sp::cuda_status(cudaStreamSynchronize(s1), "pingpong sync 1");
+  cudaStreamDestroy(s0);
+  cudaStreamDestroy(s1);
+  return rc;
+}
 
 // Transport self-test (tests/test_loopback_gpu.py): rank `rank` of a 2-rank
 // world exchanges `iters` messages of `bytes` with rank 1-rank on its own

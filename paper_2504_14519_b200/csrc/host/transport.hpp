@@ -11,12 +11,14 @@
 // Two implementations:
 //   * NCCL (one process per GPU, NVLink/NVSwitch) — the production path;
 //   * loopback (every rank a host thread of ONE process on ONE GPU): a
-//     receive publishes its destination and raises a device flag (stream
-//     memory write); the matching send's copy kernel waits for that flag,
-//     copies straight into the destination, and a "done" flag is raised that
-//     a one-CTA wait kernel on the receive's stream spins on (kernels, like
-//     NCCL's, not front-end stream waits: those would block every stream
-//     sharing the hardware channel).  No host-side rendezvous, so the host enqueue
+//     receive publishes its destination and raises a device flag; the
+//     matching send waits for that flag, copies straight into the
+//     destination and raises a "done" flag that the receive's stream waits
+//     on.  Waits and signals are all small kernels (a spinning one-CTA wait,
+//     a one-thread release store), like NCCL's, never stream memory
+//     operations: a front-end wait or a write that must wait for its
+//     stream's previous kernel holds the whole hardware channel, and a
+//     channel shared with a peer's stream closes a cycle.  No host-side rendezvous, so the host enqueue
 //     never blocks on a peer — the same progress semantics as NCCL.  It lets
 //     a single-GPU box run (and test) the multi-stage protocol bit for bit.
 #pragma once

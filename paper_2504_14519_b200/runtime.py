@@ -138,6 +138,7 @@ def _lib():
     lib.sp_loopback_destroy.argtypes = [C.c_void_p]
     lib.sp_loopback_errors.argtypes = [C.c_void_p]
     lib.sp_loopback_pingpong.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_int]
+    lib.sp_loopback_pingpong_1thread.argtypes = [C.c_void_p] + [C.c_void_p] * 4 + [C.c_int64, C.c_int]
     lib.sp_runtime_exchange_stats.argtypes = [C.c_void_p, C.POINTER(C.c_int64)]
     lib.sp_runtime_comm_stats.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
     lib.sp_runtime_enqueue_position.argtypes = [C.c_void_p]

@@ -1,5 +1,12 @@
+import os
 import sys
 from pathlib import Path
+
+# One hardware work queue per CUDA stream (the default 8 makes streams share
+# queues, and a waiting stream then stalls unrelated ones; the loopback
+# transport runs a dozen streams per rank in one process).  Must be set before
+# the CUDA context exists.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 import pytest
 

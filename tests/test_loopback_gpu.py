@@ -18,6 +18,30 @@ from test_attn_gpu import _need_gpu
 pytestmark = pytest.mark.gpu
 
 
+def test_loopback_transport_pingpong_one_thread():
+    """Both ranks' operations enqueued by one host thread: the device-side
+    protocol alone."""
+    _need_gpu()
+    from paper_2504_14519_b200.runtime import LoopbackWorld, _lib
+    world = LoopbackWorld(2)
+    nbytes = 1 << 20
+    b = [torch.full((nbytes,), v, dtype=torch.uint8, device="cuda") for v in (1, 2, 0, 0)]
+    torch.cuda.synchronize()
+    import threading
+    rc = [None]
+    t = threading.Thread(target=lambda: rc.__setitem__(0, _lib().sp_loopback_pingpong_1thread(
+        world.handle, b[0].data_ptr(), b[1].data_ptr(), b[2].data_ptr(), b[3].data_ptr(), nbytes, 4)), daemon=True)
+    t.start()
+    t.join(60)
+    if t.is_alive():
+        import os
+        import sys
+        print("one-thread loopback ping-pong did not finish in 60 s", file=sys.stderr, flush=True)
+        os._exit(3)
+    assert rc[0] == 0
+    assert int(b[2].min()) == 2 and int(b[3].max()) == 1
+
+
 def test_loopback_transport_pingpong():
     """The transport alone: two threads exchange messages (plain and grouped)
     through device flags and copy kernels; payloads arrive intact."""
