@@ -29,6 +29,11 @@ import argparse
 import ctypes as C
 import json
 import os
+
+# one hardware work queue per CUDA stream (the executor runs up to ten per
+# rank; shared queues let a waiting stream stall unrelated ones) — before the
+# CUDA context exists
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 import subprocess
 import sys
 import threading

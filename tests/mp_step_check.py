@@ -8,6 +8,11 @@ float64 oracle on the same bf16 weights and compares (same tolerances as
 tests/test_step_gpu.py).  Exit code 0 = parity holds.
 """
 import os
+
+# one hardware work queue per CUDA stream (the executor runs up to ten per
+# rank; shared queues let a waiting stream stall unrelated ones) — before the
+# CUDA context exists
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 import sys
 from pathlib import Path
 
