@@ -396,6 +396,17 @@ int bwd_check(int64_t q_rows, int n_chunks, int chunk_len, int heads, int kv_hea
 }  // namespace
 }  // namespace sp
 
+namespace sp {
+// Force-load this file's kernels (cudaFuncGetAttributes) — see preload_kernels
+int preload_attn_bwd() {
+  cudaFuncAttributes a;
+  if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(sp::attn_bwd_kernel<64>))) return cuda_status(e, "preload sp::attn_bwd_kernel<64>");
+  if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(sp::attn_bwd_prep<64>))) return cuda_status(e, "preload sp::attn_bwd_prep<64>");
+  if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(sp::attn_bwd_prep<128>))) return cuda_status(e, "preload sp::attn_bwd_prep<128>");
+  return SP_OK;
+}
+}  // namespace sp
+
 extern "C" int sp_attn_bwd_prep(const void* o, int64_t o_stride, const void* dout, int64_t do_stride, const float* lse,
                                 int64_t q_rows, int heads, int head_dim, float* stats, sp_stream_t stream) {
   using namespace sp;

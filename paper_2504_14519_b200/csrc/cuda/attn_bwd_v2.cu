@@ -387,4 +387,11 @@ int attn_bwd_d128(const void* q, int64_t q_rows, int64_t q_stride, const void* k
   return cuda_status(cudaGetLastError(), "attn_bwd_d128 launch");
 }
 
+
+// Force-load this file's kernels (cudaFuncGetAttributes) — see preload_kernels
+int preload_attn_bwd_v2() {
+  cudaFuncAttributes a;
+  if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(attn_bwd_d128_kernel<3, 1>))) return cuda_status(e, "preload attn_bwd_d128_kernel<3, 1>");
+  return SP_OK;
+}
 }  // namespace sp

@@ -345,6 +345,15 @@ int attn_fwd_dispatch(const void* q, int64_t q_rows, int64_t q_stride, const voi
 }  // namespace
 }  // namespace sp
 
+namespace sp {
+// Force-load this file's kernels (cudaFuncGetAttributes) — see preload_kernels
+int preload_attn_fwd() {
+  cudaFuncAttributes a;
+  if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(sp::attn_fwd_kernel<64, 3>))) return cuda_status(e, "preload sp::attn_fwd_kernel<64, 3>");
+  return SP_OK;
+}
+}  // namespace sp
+
 extern "C" int sp_attn_fwd(const void* q, int64_t q_rows, int64_t q_stride, const void* k_pool, const void* v_pool,
                            int64_t pool_rows, int64_t kv_stride, const int32_t* chunk_row, int n_chunks,
                            int chunk_len, int heads, int kv_heads, int head_dim, int causal, void* o,

@@ -367,4 +367,11 @@ int attn_fwd_d128_ps(const void* q, int64_t q_rows, int64_t q_stride, const void
   return cuda_status(cudaGetLastError(), "attn_fwd_d128_ps launch");
 }
 
+
+// Force-load this file's kernels (cudaFuncGetAttributes) — see preload_kernels
+int preload_attn_fwd_v4() {
+  cudaFuncAttributes a;
+  if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(attn_fwd_ps_kernel))) return cuda_status(e, "preload attn_fwd_ps_kernel");
+  return SP_OK;
+}
 }  // namespace sp

@@ -49,6 +49,16 @@ __global__ void __launch_bounds__(256) attn_merge_kernel(const __nv_bfloat16* oa
 }  // namespace
 }  // namespace sp
 
+namespace sp {
+// Force-load this file's kernels (cudaFuncGetAttributes) — see preload_kernels
+int preload_attn_merge() {
+  cudaFuncAttributes a;
+  if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(sp::attn_merge_kernel<64>))) return cuda_status(e, "preload sp::attn_merge_kernel<64>");
+  if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(sp::attn_merge_kernel<128>))) return cuda_status(e, "preload sp::attn_merge_kernel<128>");
+  return SP_OK;
+}
+}  // namespace sp
+
 extern "C" int sp_attn_merge(const void* o_a, const float* lse_a, const void* o_b, const float* lse_b, int64_t rows,
                              int heads, int head_dim, int64_t o_stride, void* o_out, float* lse_out,
                              sp_stream_t stream) {

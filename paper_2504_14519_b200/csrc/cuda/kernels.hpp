@@ -62,6 +62,16 @@ int attn_fwd_d128_ps(const void* q, int64_t q_rows, int64_t q_stride, const void
                      int heads, int kv_heads, const FwdMask& mk, void* o, int64_t o_stride, float* lse,
                      cudaStream_t st);
 
+// load every kernel of the library on the current device now (not lazily at
+// first launch, which can deadlock against a spinning receive; transport.cu)
+int preload_kernels();
+int preload_layers();
+int preload_attn_fwd();
+int preload_attn_fwd_v4();
+int preload_attn_bwd();
+int preload_attn_bwd_v2();
+int preload_attn_merge();
+
 // cudaFuncAttributeMaxDynamicSharedMemorySize once per (kernel, device)
 int set_smem_once(const void* fn, size_t smem, const char* what);
 

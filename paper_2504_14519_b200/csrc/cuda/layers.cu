@@ -660,4 +660,28 @@ int f32_to_bf16(const float* a, void* b, int64_t n, cudaStream_t st) {
   return cuda_status(cudaGetLastError(), "f32_to_bf16");
 }
 
+
+// Force-load this file's kernels (cudaFuncGetAttributes) — see preload_kernels
+int preload_layers() {
+  cudaFuncAttributes a;
+  if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(embed_fwd_k))) return cuda_status(e, "preload embed_fwd_k");
+  if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(embed_bwd_k))) return cuda_status(e, "preload embed_bwd_k");
+  if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(rmsnorm_fwd_k<4>))) return cuda_status(e, "preload rmsnorm_fwd_k<4>");
+  if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(rmsnorm_bwd_k<4>))) return cuda_status(e, "preload rmsnorm_bwd_k<4>");
+  if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(rmsnorm_dw_sum_k))) return cuda_status(e, "preload rmsnorm_dw_sum_k");
+  if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(rope_table_k))) return cuda_status(e, "preload rope_table_k");
+  if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(rope_qkv_fwd_k))) return cuda_status(e, "preload rope_qkv_fwd_k");
+  if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(rope_qkv_bwd_k))) return cuda_status(e, "preload rope_qkv_bwd_k");
+  if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(swiglu_fwd_k))) return cuda_status(e, "preload swiglu_fwd_k");
+  if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(swiglu_bwd_k))) return cuda_status(e, "preload swiglu_bwd_k");
+  if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(xent_k))) return cuda_status(e, "preload xent_k");
+  if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(xent_shard_stats_k))) return cuda_status(e, "preload xent_shard_stats_k");
+  if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(xent_shard_rescale_k))) return cuda_status(e, "preload xent_shard_rescale_k");
+  if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(xent_shard_grad_k))) return cuda_status(e, "preload xent_shard_grad_k");
+  if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(adamw_k))) return cuda_status(e, "preload adamw_k");
+  if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(init_normal_k))) return cuda_status(e, "preload init_normal_k");
+  if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(f32_to_bf16_k))) return cuda_status(e, "preload f32_to_bf16_k");
+  if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(add_f32_k))) return cuda_status(e, "preload add_f32_k");
+  return SP_OK;
+}
 }  // namespace sp

@@ -5,6 +5,7 @@
 #include <atomic>
 #include <memory>
 #include <mutex>
+#include <set>
 #include <vector>
 
 #include "kernels.hpp"
@@ -145,7 +146,7 @@ struct LoopWorld {
 };
 
 LoopWorld* loop_world_create(int ranks) {
-  if (ranks < 1) return nullptr;
+  if (ranks < 1 || preload_kernels() != SP_OK) return nullptr;
   auto w = std::make_unique<LoopWorld>();
   w->n = ranks;
   const size_t nch = size_t(kComms) * ranks * ranks;
@@ -364,6 +365,37 @@ std::unique_ptr<Link> make_loop_link(LoopWorld* w, int comm_id, std::vector<int>
   for (int m : members)
     if (m < 0 || m >= w->n) return nullptr;
   return std::make_unique<LoopLink>(w, comm_id, std::move(members), me);
+}
+
+// Force-load this file's kernels (cudaFuncGetAttributes) — see preload_kernels
+int preload_transport() {
+  cudaFuncAttributes a;
+  for (const void* k : {reinterpret_cast<const void*>(loop_signal_kernel), reinterpret_cast<const void*>(loop_wait_kernel),
+                        reinterpret_cast<const void*>(loop_copy_kernel), reinterpret_cast<const void*>(loop_combine_kernel)})
+    if (cudaError_t e = cudaFuncGetAttributes(&a, k)) return cuda_status(e, "preload transport");
+  return SP_OK;
+}
+
+// CUDA lazy loading (the default) loads a kernel at its first launch, and a
+// load may wait for the context to go idle.  A spinning receive (an NCCL
+// kernel, or a loopback wait) is then a deadlock: it waits for a peer whose
+// next kernel cannot load until the spinner ends.  The round-1 vocab-parallel
+// and interleaved stalls had exactly this shape (the host blocked inside step
+// enqueue at the first launch of a kernel type while a receive was posted).
+// Every kernel of the library is therefore loaded up front, before any
+// communication; library GEMMs are warmed by the runtime (warm_gemms).
+int preload_kernels() {
+  static std::mutex mu;
+  static std::set<int> done;
+  int dev = 0;
+  if (cudaError_t e = cudaGetDevice(&dev)) return cuda_status(e, "preload");
+  std::lock_guard<std::mutex> g(mu);
+  if (done.count(dev)) return SP_OK;
+  for (int (*f)() : {preload_layers, preload_attn_fwd, preload_attn_fwd_v4, preload_attn_bwd, preload_attn_bwd_v2,
+                     preload_attn_merge, preload_transport})
+    if (int rc = f()) return rc;
+  done.insert(dev);
+  return SP_OK;
 }
 
 }  // namespace sp

@@ -352,6 +352,7 @@ class Runtime {
     }
 
     SP_CUDA(cudaGetDevice(&device));  // host-side validation above runs without a GPU
+    SP_TRY(preload_kernels());        // before any communication (transport.cu)
     SP_CUDA(cudaStreamCreateWithFlags(&comp, cudaStreamNonBlocking));
     for (cudaStream_t* st : {&s_act_in, &s_act_out, &s_grad_in, &s_grad_out})
       SP_CUDA(cudaStreamCreateWithFlags(st, cudaStreamNonBlocking));
@@ -387,7 +388,42 @@ class Runtime {
     SP_TRY(alloc_exchange());
     SP_TRY(alloc_arena());
     SP_TRY(init_weights(c.seed));
+    SP_TRY(warm_gemms());
     SP_CUDA(cudaStreamSynchronize(comp));
+    return SP_OK;
+  }
+
+  // Run every library GEMM of the step once (same shapes, transposes, output
+  // types and beta, on the workspaces) before any communication, so cuBLASLt
+  // has chosen and LOADED each kernel: a lazily loaded kernel launched while
+  // a receive spins can deadlock (preload_kernels, transport.cu).  The
+  // gradient buffers the weight-gradient GEMMs touched are zeroed again.
+  int warm_gemms() {
+    LayerWs& x = ws[0];
+    const LayerParams& P = lp[0];
+    SP_TRY(gemm(false, true, Ls, qkv_w, h, x.xn, h, W(P.wqkv), h, qkv, qkv_w, false, 1.f, 0.f, comp));
+    SP_TRY(gemm(false, true, Ls, h, qd, x.o, qd, W(P.wo), qd, x.x_mid, h, false, 1.f, 1.f, comp, x.x_in));
+    SP_TRY(gemm(false, true, Ls, 2 * H, h, x.xn2, h, W(P.wgu), h, x.gu, 2 * H, false, 1.f, 0.f, comp));
+    SP_TRY(gemm(false, true, Ls, h, H, x.act, H, W(P.wd), H, x_final, h, false, 1.f, 1.f, comp, x.x_mid));
+    SP_TRY(gemm(false, false, Ls, H, h, tmp_h, h, W(P.wd), H, tmp_H, H, false, 1.f, 0.f, comp));
+    SP_TRY(gemm(true, false, h, H, Ls, tmp_h, h, x.act, H, G(P.wd), H, true, 1.f, 1.f, comp));
+    SP_TRY(gemm(false, false, Ls, h, 2 * H, tmp_2H, 2 * H, W(P.wgu), h, tmp_h, h, false, 1.f, 0.f, comp));
+    SP_TRY(gemm(true, false, 2 * H, h, Ls, tmp_2H, 2 * H, x.xn2, h, G(P.wgu), h, true, 1.f, 1.f, comp));
+    SP_TRY(gemm(false, false, Ls, qd, h, x_final, h, W(P.wo), qd, tmp_h, qd, false, 1.f, 0.f, comp));
+    SP_TRY(gemm(true, false, h, qd, Ls, x_final, h, x.o, qd, G(P.wo), qd, true, 1.f, 1.f, comp));
+    SP_TRY(gemm(false, false, Ls, h, qkv_w, dqkv, qkv_w, W(P.wqkv), h, tmp_h, h, false, 1.f, 0.f, comp));
+    SP_TRY(gemm(true, false, qkv_w, h, Ls, dqkv, qkv_w, x.xn, h, G(P.wqkv), h, true, 1.f, 1.f, comp));
+    if (vp) {
+      SP_TRY(gemm(false, true, Ls, Vs, h, vslots[0].xf, h, W(head), h, vlogits, Vs, true, 1.f, 0.f, comp));
+      SP_TRY(gemm(false, false, Ls, h, Vs, vdlog, Vs, W(head), h, vdxf, h, true, 1.f, 0.f, comp));
+      SP_TRY(gemm(true, false, Vs, h, Ls, vdlog, Vs, vslots[0].xf, h, G(head), h, true, 1.f, 1.f, comp));
+    } else if (last_dev) {
+      const int64_t V = cfg.vocab;
+      SP_TRY(gemm(false, true, Ls, V, h, xf, h, W(head), h, logits, V, true, 1.f, 0.f, comp));
+      SP_TRY(gemm(false, false, Ls, h, V, dlogits, V, W(head), h, tmp_h, h, false, 1.f, 0.f, comp));
+      SP_TRY(gemm(true, false, V, h, Ls, dlogits, V, xf, h, G(head), h, true, 1.f, 1.f, comp));
+    }
+    SP_CUDA(cudaMemsetAsync(grad, 0, n_params * 4, comp));
     return SP_OK;
   }
 
