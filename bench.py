@@ -202,8 +202,64 @@ def cpu_baseline(cfg, seconds: float):
               f"(Ls={ls} causal over {nch} chunks, d={d}) = {heads * flops_head / 1e9:.1f} GFLOP in {t:.1f} s "
               f"({rate / 1e9:.2f} GFLOP/s on {threads} threads), extrapolated to the step's "
               f"{cfg.model_flops_per_step() / 1e15:.1f} PFLOP of model FLOPs")
-    return {"value": tok_s, "unit": "tokens/s", "cores": threads, "kind": kind, "sample": sample,
-            "gflops": rate / 1e9, "seconds": t}
+    out = {"value": tok_s, "unit": "tokens/s", "cores": threads, "kind": kind, "sample": sample,
+           "gflops": rate / 1e9, "seconds": t}
+    try:
+        out["details"] = cpu_details(cfg, threads, lib if kind == "reference" else None)
+    except Exception as e:  # the headline baseline stands without the details
+        out["details"] = {"error": str(e)}
+    return out
+
+
+def cpu_details(cfg, threads, ref_lib):
+    """SURVEY §8(d)'s CPU-side numbers beside the headline sample: the
+    reference's host planning of this step in ms (single thread), warm
+    best-of-5 chunk_attention GFLOP/s at Ls 256/512/1024 (prefix <= 4 Ls,
+    one head per thread), and the c1 tiny training step on the fp64 CPU
+    oracle (tokens/s)."""
+    d = {}
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracle_lib as O
+    if ref_lib is not None:
+        p = 8  # planned as the PP=8 configuration of this workload (BASELINE configs[1])
+        t0 = time.perf_counter()
+        O.ref_text("ref_schedule_json", 6, p, cfg.interleave, cfg.microbatches, cfg.slices)
+        t1 = time.perf_counter()
+        O.ref_text("ref_exchange_json", p, cfg.interleave, cfg.microbatches, cfg.slices, 2, 1.0)
+        t2 = time.perf_counter()
+        O.ref_text("ref_simulate_json", p, cfg.interleave, cfg.microbatches, cfg.slices, 0,
+                   (C.c_double * 4)(1.0, 1e-3, 2.0, 1.0), (C.c_double * 2)(0.0, 0.0), cfg.seq_len, None)
+        t3 = time.perf_counter()
+        d["planning_ms"] = {"config": f"p={p} v={cfg.interleave} m={cfg.microbatches} n={cfg.slices}",
+                            "gen_slimpipe + schedule_to_json": (t1 - t0) * 1e3,
+                            "apply_exchange (early)": (t2 - t1) * 1e3, "simulate": (t3 - t2) * 1e3}
+        att = {}
+        for ls in (256, 512, 1024):
+            best = None
+            for _ in range(5):
+                sec = ref_lib.ref_time_chunk_attention(threads, ls, 4, 128, threads, 20240817)
+                best = sec if best is None else min(best, sec)
+            fl = threads * 4.0 * 128 * ls * (3 * ls + (ls + 1) / 2.0)
+            att[str(ls)] = fl / best / 1e9
+        d["chunk_attention_gflops_best_of_5"] = att
+    import numpy as np
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import model_oracle as MO
+    from paper_2504_14519_b200.runtime import StepConfig
+    c1 = StepConfig.c1(microbatches=1, seq_len=1024, slices=4)
+    rng = np.random.default_rng(0)
+    W = {n: [rng.normal(0, 0.02, s) for _ in range(c1.layers)] for n, s in (
+        ("attn_norm", (c1.hidden,)), ("wqkv", (3 * c1.hidden, c1.hidden)), ("wo", (c1.hidden, c1.hidden)),
+        ("mlp_norm", (c1.hidden,)), ("wgu", (2 * c1.ffn_hidden, c1.hidden)), ("wd", (c1.hidden, c1.ffn_hidden)))}
+    W["embedding"] = rng.normal(0, 0.02, (c1.vocab, c1.hidden))
+    W["final_norm"] = np.ones(c1.hidden)
+    W["head"] = rng.normal(0, 0.02, (c1.vocab, c1.hidden))
+    tok = rng.integers(0, c1.vocab, (1, c1.seq_len))
+    t0 = time.perf_counter()
+    MO.Model(W, c1.heads, c1.kv_heads, c1.rope_theta, c1.norm_eps).step(tok, np.roll(tok, -1, axis=1), c1.slices)
+    d["c1_oracle_step"] = {"tokens_per_s": c1.seq_len / (time.perf_counter() - t0),
+                           "shape": "c1 layers (4 x h256, 4 heads), 1 microbatch of 1K tokens in 4 slices, fp64 numpy"}
+    return d
 
 
 def run_reference(args):
@@ -400,7 +456,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             cb = cpu_baseline(cfg, args.cpu_seconds)
-            cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "details")}
         except Exception as e:  # never fail the bench line on the baseline leg
             cpu = {"value": None, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"failed: {e}"}
