@@ -23,6 +23,8 @@
 #include "kernels.hpp"
 #include "sm100.cuh"
 
+#include <cstdlib>
+
 
 namespace sp {
 namespace {
@@ -47,18 +49,20 @@ struct Params {
 
 // NS: Q/dO ring depth; NDS: dS^T tiles (2 = element math of pair j never
 // waits for the dQ MMA of pair j-1 to finish reading the previous tile)
-template <int NS, int NDS>
+// STQ: query rows of the dQ staging tile (64 = one TMA reduce per pair, 32 =
+// two, in half the shared memory)
+template <int NS, int NDS, int STQ>
 struct alignas(1024) Smem {
   __nv_bfloat16 k[BK * D];
   __nv_bfloat16 v[BK * D];
   __nv_bfloat16 q[NS][BQ * D];
   __nv_bfloat16 dout[NS][BQ * D];
   __nv_bfloat16 ds[NDS][BK * BQ];
-  float stage[1][BQ * D];  // dQ tile [q][d] on their way to the TMA reduce
+  float stage[STQ * D];  // dQ rows [q][d] on their way to the TMA reduce
 };
 
 template <int NS>
-struct Ctl {  // static shared memory: statistics and barriers
+struct Ctl {  // statistics and barriers (after the operand tiles)
   float lse2[NS][BQ];
   float delta[NS][BQ];
   uint64_t kv_full, q_full[NS], q_empty[NS], sdp_full[2], pds_ready, pds_free, dq_full[2], dq_free[2], acc_free[2],
@@ -73,15 +77,22 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
                : "memory");
 }
 
-template <int NS, int NDS>
+template <int NS, int NDS, int STQ, bool kPad>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_bwd_d128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
                          const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                          const __grid_constant__ CUtensorMap tm_dq, const __grid_constant__ Params prm) {
   extern __shared__ uint8_t smem_raw[];
-  static_assert(sizeof(Smem<NS, NDS>) % 1024 == 0, "operand tiles stay 1024-aligned");
-  auto& sm = *reinterpret_cast<Smem<NS, NDS>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ __align__(16) Ctl<NS> ctl;
+  using SmemT = Smem<NS, NDS, STQ>;
+  static_assert(sizeof(SmemT) % 1024 == 0, "operand tiles stay 1024-aligned");
+  // kPad: the launch added 1 KB to align the operand tiles; without it the
+  // dynamic window must start 1 KB-aligned (it does when the kernel has no
+  // static shared memory) — checked, never assumed
+  uint8_t* base = kPad ? reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023))
+                       : smem_raw;
+  if (!kPad && (smem_u32(smem_raw) & 1023u)) __trap();
+  auto& sm = *reinterpret_cast<SmemT*>(base);
+  auto& ctl = *reinterpret_cast<Ctl<NS>*>(base + sizeof(SmemT));
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int kt = blockIdx.x, kvh = blockIdx.y;
   const int key0 = kt * BK;
@@ -318,19 +329,29 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(&ctl.dq_free[bb]);
-      if (dtid == 0) bulk_wait_read<0>();  // the previous reduce has read the stage
-      named_bar_sync(1, kDrain);
-      const uint32_t st = smem_u32(sm.stage[0]) + uint32_t(d) * 4u;
+      // [q][d] rows of the stage, STQ queries per TMA reduce (a0: queries
+      // 0..31, a1: 32..63 of the pair)
+      auto stage_rows = [&](const float(&lo)[32], const float(&hi)[32], int q0) {
+        if (dtid == 0) bulk_wait_read<0>();  // the previous reduce has read the stage
+        named_bar_sync(1, kDrain);
+        const uint32_t st = smem_u32(sm.stage) + uint32_t(d) * 4u;
 #pragma unroll
-      for (int x = 0; x < 32; ++x) {
-        asm volatile("st.shared.f32 [%0], %1;" ::"r"(st + x * D * 4), "f"(a0[x]) : "memory");
-        asm volatile("st.shared.f32 [%0], %1;" ::"r"(st + (32 + x) * D * 4), "f"(a1[x]) : "memory");
-      }
-      fence_async_smem();
-      named_bar_sync(2, kDrain);
-      if (dtid == 0) {
-        tma_reduce_add_2d(&tm_dq, sm.stage[0], pair_head(jj) * D, pair_row(jj));
-        bulk_commit();
+        for (int x = 0; x < 32; ++x) {
+          asm volatile("st.shared.f32 [%0], %1;" ::"r"(st + x * D * 4), "f"(lo[x]) : "memory");
+          if (STQ == 64) asm volatile("st.shared.f32 [%0], %1;" ::"r"(st + (32 + x) * D * 4), "f"(hi[x]) : "memory");
+        }
+        fence_async_smem();
+        named_bar_sync(2, kDrain);
+        if (dtid == 0) {
+          tma_reduce_add_2d(&tm_dq, sm.stage, pair_head(jj) * D, pair_row(jj) + q0);
+          bulk_commit();
+        }
+      };
+      if (STQ == 64) {
+        stage_rows(a0, a1, 0);
+      } else {
+        stage_rows(a0, a0, 0);
+        stage_rows(a1, a1, 32);
       }
     }
     if (dtid == 0) bulk_wait<0>();
@@ -369,21 +390,35 @@ int attn_bwd_d128(const void* q, int64_t q_rows, int64_t q_stride, const void* k
     prm.chunk_row[c] = chunk_row[c];
     prm.acc_row[c] = acc_row[c];
   }
+  // SP_BWD_VARIANT (A/B measurements, read once): 0 = NS 3, one dS tile,
+  // 64-row dQ stage; 1 = NS 4 with a 32-row stage (fits only without the
+  // alignment pad); 2 = NS 3, two dS tiles, 32-row stage
+  static const int variant = [] {
+    const char* e = std::getenv("SP_BWD_VARIANT");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int stq = variant == 0 ? BQ : 32;
   CUtensorMap tq, tdo, tk, tv, tdq;
   if (!make_tmap_bf16(&tq, q, uint64_t(q_stride), uint64_t(q_rows), uint64_t(q_stride), BQ) ||
       !make_tmap_bf16(&tdo, dout, uint64_t(do_stride), uint64_t(q_rows), uint64_t(do_stride), BQ) ||
       !make_tmap_bf16(&tk, k_pool, uint64_t(kv_stride), uint64_t(pool_rows), uint64_t(kv_stride), BK) ||
       !make_tmap_bf16(&tv, v_pool, uint64_t(kv_stride), uint64_t(pool_rows), uint64_t(kv_stride), BK) ||
-      !make_tmap_f32(&tdq, dq_acc, uint64_t(heads) * D, uint64_t(q_rows), uint64_t(heads) * D, D, BQ))
+      !make_tmap_f32(&tdq, dq_acc, uint64_t(heads) * D, uint64_t(q_rows), uint64_t(heads) * D, D, uint32_t(stq)))
     return set_error(SP_ERR_CUDA, "attn_bwd_d128: cuTensorMapEncodeTiled failed (alignment?)");
-  // NS = 3 Q/dO stages and one dS tile: measured best (scripts/k2_ab.py,
-  // profiles/r02_k2_ab.json: NS = 2 with one or two dS tiles is 11-12 %
-  // slower; NS = 3 with two dS tiles exceeds the 227 KB per-CTA shared memory)
-  auto kern = attn_bwd_d128_kernel<3, 1>;
-  const size_t smem = sizeof(Smem<3, 1>) + 1024;
-  if (int rc = set_smem_once(reinterpret_cast<const void*>(kern), smem, "attn_bwd_d128: set smem")) return rc;
-  kern<<<dim3(prm.total_kv / BK, kv_heads), kThreads, smem, st>>>(tq, tdo, tk, tv, tdq, prm);
-  count_launch(1);
+  auto launch = [&](auto kern, size_t smem) -> int {
+    if (int rc = set_smem_once(reinterpret_cast<const void*>(kern), smem, "attn_bwd_d128: set smem")) return rc;
+    kern<<<dim3(prm.total_kv / BK, kv_heads), kThreads, smem, st>>>(tq, tdo, tk, tv, tdq, prm);
+    count_launch(1);
+    return SP_OK;
+  };
+  int rc = SP_OK;
+  if (variant == 1)
+    rc = launch(attn_bwd_d128_kernel<4, 1, 32, false>, sizeof(Smem<4, 1, 32>) + sizeof(Ctl<4>));
+  else if (variant == 2)
+    rc = launch(attn_bwd_d128_kernel<3, 2, 32, true>, sizeof(Smem<3, 2, 32>) + sizeof(Ctl<3>) + 1024);
+  else
+    rc = launch(attn_bwd_d128_kernel<3, 1, 64, true>, sizeof(Smem<3, 1, 64>) + sizeof(Ctl<3>) + 1024);
+  if (rc) return rc;
   return cuda_status(cudaGetLastError(), "attn_bwd_d128 launch");
 }
 
@@ -391,7 +426,10 @@ int attn_bwd_d128(const void* q, int64_t q_rows, int64_t q_stride, const void* k
 // Force-load this file's kernels (cudaFuncGetAttributes) — see preload_kernels
 int preload_attn_bwd_v2() {
   cudaFuncAttributes a;
-  if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(attn_bwd_d128_kernel<3, 1>))) return cuda_status(e, "preload attn_bwd_d128_kernel<3, 1>");
+  for (const void* k : {reinterpret_cast<const void*>(attn_bwd_d128_kernel<3, 1, 64, true>),
+                        reinterpret_cast<const void*>(attn_bwd_d128_kernel<4, 1, 32, false>),
+                        reinterpret_cast<const void*>(attn_bwd_d128_kernel<3, 2, 32, true>)})
+    if (cudaError_t e = cudaFuncGetAttributes(&a, k)) return cuda_status(e, "preload attn_bwd_d128_kernel");
   return SP_OK;
 }
 }  // namespace sp
