@@ -318,6 +318,17 @@ class LoopLink final : public Link {
   int reduce(float* buf, int64_t count, int root, cudaStream_t st) override {
     return gather_combine(buf, count, 0, root, st, false);
   }
+  int reserve(int64_t count) override {
+    const int64_t need = int64_t(mem_.size() - 1) * count;
+    if (need <= scratch_n_) return SP_OK;
+    if (scratch_) cudaFree(scratch_);
+    scratch_ = nullptr;
+    scratch_n_ = 0;
+    if (cudaError_t e = cudaMalloc(&scratch_, size_t(std::max<int64_t>(need, 1)) * 4))
+      return cuda_status(e, "loopback collective scratch");
+    scratch_n_ = need;
+    return SP_OK;
+  }
   int all_reduce(float* buf, int64_t count, ncclRedOp_t op, cudaStream_t st) override {
     if (op != ncclSum && op != ncclMax) return set_error(SP_ERR_UNSUPPORTED, "loopback all_reduce: sum or max only");
     return gather_combine(buf, count, op == ncclMax ? 1 : 0, 0, st, true);
@@ -330,14 +341,8 @@ class LoopLink final : public Link {
       SP_LOOP_TRY(send(buf, count, ncclFloat32, root, st));
       return back ? recv(buf, count, ncclFloat32, root, st) : SP_OK;
     }
-    const int64_t need = int64_t(n - 1) * count;
-    if (need > scratch_n_) {
-      if (scratch_) cudaFree(scratch_);
-      scratch_ = nullptr;
-      if (cudaError_t e = cudaMalloc(&scratch_, size_t(std::max<int64_t>(need, 1)) * 4))
-        return cuda_status(e, "loopback collective scratch");
-      scratch_n_ = need;
-    }
+    if (int64_t(n - 1) * count > scratch_n_)
+      return set_error(SP_ERR_RUNTIME, "loopback collective: scratch not reserved for %lld floats", (long long)count);
     SP_LOOP_TRY(group_start());
     for (int q = 0, x = 0; q < n; ++q)
       if (q != root) SP_LOOP_TRY(recv(scratch_ + int64_t(x++) * count, count, ncclFloat32, q, st));

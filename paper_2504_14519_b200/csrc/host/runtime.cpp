@@ -151,6 +151,9 @@ class Runtime {
   bf16raw* gout_buf[2] = {nullptr, nullptr}; // gradients sent to s-1 (dx)
   float *rope_cos = nullptr, *rope_sin = nullptr;  // [seq_len][d/2]
   float* norm_ws = nullptr;  // per-block RMSNorm dW partials (deterministic weight gradient)
+  int32_t *h_tok = nullptr, *h_tgt = nullptr;  // pinned staging of host inputs
+  float* h_loss = nullptr;
+  cudaEvent_t ev_staged = nullptr;
   float *dq_acc = nullptr, *delta_ws = nullptr, *logits = nullptr, *rstd_f = nullptr, *loss_dev = nullptr;
   int32_t *tokens = nullptr, *targets = nullptr;
 
@@ -228,6 +231,9 @@ class Runtime {
     if (nc_fwd) ncclCommDestroy(nc_fwd);
     for (cudaEvent_t e : tpool) cudaEventDestroy(e);
     if (xev) cudaEventDestroy(xev);
+    if (ev_staged) cudaEventDestroy(ev_staged);
+    for (void* hp : {static_cast<void*>(h_tok), static_cast<void*>(h_tgt), static_cast<void*>(h_loss)})
+      if (hp) cudaFreeHost(hp);
   }
 
   int timing_event(cudaEvent_t* e) {
@@ -507,7 +513,10 @@ class Runtime {
     for (int r = 0; r < p; ++r) all[size_t(r)] = r;
     if (!xplan.empty() || cfg.exchange_mode != 0)
       for (int k = 0; k < 2; ++k) lx[k] = make_loop_link(loop, 2 + k, all, rank);
-    if (vp) vlink = make_loop_link(loop, 4, all, rank);  // collectives over p2p (transport.cu)
+    if (vp) {  // collectives over p2p (transport.cu); scratch sized now, not inside a step
+      vlink = make_loop_link(loop, 4, all, rank);
+      SP_TRY(vlink->reserve(Ls * h));
+    }
     return SP_OK;
   }
 
@@ -956,6 +965,12 @@ class Runtime {
     SP_TRY(alloc(&loss_dev, 1));
     SP_TRY(alloc(&tokens, int64_t(cfg.microbatches) * cfg.seq_len));
     SP_TRY(alloc(&targets, int64_t(cfg.microbatches) * cfg.seq_len));
+    const size_t tok_bytes = size_t(cfg.microbatches) * size_t(cfg.seq_len) * 4;
+    SP_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h_tok), tok_bytes, cudaHostAllocDefault));
+    SP_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h_tgt), tok_bytes, cudaHostAllocDefault));
+    SP_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h_loss), 4, cudaHostAllocDefault));
+    SP_CUDA(cudaEventCreateWithFlags(&ev_staged, cudaEventDisableTiming));
+    SP_CUDA(cudaEventRecord(ev_staged, comp));
     if (last_dev) {
       SP_TRY(alloc(&xf, Ls * h));
       SP_TRY(alloc(&rstd_f, Ls));
@@ -1337,9 +1352,25 @@ class Runtime {
     x_bytes_sent = 0;
     const int64_t ntok = int64_t(cfg.microbatches) * cfg.seq_len;
     SP_CUDA(cudaEventRecord(step_start, comp));
-    const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-    if (first_dev && tok) SP_CUDA(cudaMemcpyAsync(tokens, tok, ntok * 4, kind, comp));
-    if ((last_dev || vp) && tgt) SP_CUDA(cudaMemcpyAsync(targets, tgt, ntok * 4, kind, comp));
+    // Host inputs go through pinned staging buffers: a pageable copy would
+    // block this thread inside the CUDA driver until the stream drained (and,
+    // with loopback ranks sharing one context, stall the other ranks' enqueue).
+    const bool need_tok = first_dev && tok, need_tgt = (last_dev || vp) && tgt;
+    if (on_device) {
+      if (need_tok) SP_CUDA(cudaMemcpyAsync(tokens, tok, ntok * 4, cudaMemcpyDeviceToDevice, comp));
+      if (need_tgt) SP_CUDA(cudaMemcpyAsync(targets, tgt, ntok * 4, cudaMemcpyDeviceToDevice, comp));
+    } else if (need_tok || need_tgt) {
+      SP_CUDA(cudaEventSynchronize(ev_staged));  // the previous step's copies have left the staging buffers
+      if (need_tok) {
+        std::memcpy(h_tok, tok, size_t(ntok) * 4);
+        SP_CUDA(cudaMemcpyAsync(tokens, h_tok, ntok * 4, cudaMemcpyHostToDevice, comp));
+      }
+      if (need_tgt) {
+        std::memcpy(h_tgt, tgt, size_t(ntok) * 4);
+        SP_CUDA(cudaMemcpyAsync(targets, h_tgt, ntok * 4, cudaMemcpyHostToDevice, comp));
+      }
+      SP_CUDA(cudaEventRecord(ev_staged, comp));
+    }
     SP_CUDA(cudaMemsetAsync(loss_dev, 0, 4, comp));
     for (pipelab::PassId id : order) {
       const pipelab::Pass& ps = sched.passes[id];
@@ -1375,10 +1406,9 @@ class Runtime {
     if (s_vocab) SP_TRY(link(s_vocab, comp));
     SP_CUDA(cudaEventRecord(step_end, comp));
     if (loss_out) {
-      float l = 0.f;
-      SP_CUDA(cudaMemcpyAsync(&l, loss_dev, 4, cudaMemcpyDeviceToHost, comp));
+      SP_CUDA(cudaMemcpyAsync(h_loss, loss_dev, 4, cudaMemcpyDeviceToHost, comp));
       SP_CUDA(cudaStreamSynchronize(comp));
-      *loss_out = last_dev ? l / float(ntok) : 0.f;
+      *loss_out = last_dev ? *h_loss / float(ntok) : 0.f;
     }
     return SP_OK;
   }

@@ -43,6 +43,9 @@ class Link {
   virtual int broadcast(void* buf, int64_t count, ncclDataType_t dt, int root, cudaStream_t st);
   virtual int all_reduce(float* buf, int64_t count, ncclRedOp_t op, cudaStream_t st);
   virtual int reduce(float* buf, int64_t count, int root, cudaStream_t st);
+  // pre-size any scratch the collectives need for `count` floats (allocation
+  // must not happen inside an enqueued step)
+  virtual int reserve(int64_t count) { return 0; }
 };
 
 // Takes ownership of `comm` (destroyed with the link).

@@ -44,7 +44,20 @@ def main():
                         interleave=int(os.environ.get("SP_V", 1)))
     step = SlimPipeStep(cfg, rank, world)
     tok, tgt = SP.inputs(cfg)
-    loss = step.step(tok, tgt, optimizer=False)
+    # the step on a watched thread: a stall reports where this rank stands
+    import threading
+    import time
+    from paper_2504_14519_b200.runtime import _lib
+    box = {}
+    th = threading.Thread(target=lambda: box.setdefault("loss", step.step(tok, tgt, optimizer=False)), daemon=True)
+    th.start()
+    th.join(float(os.environ.get("SP_STEP_TIMEOUT", 240)))
+    if th.is_alive():
+        print(f"rank {rank}: step stalled; host enqueuing pass #{_lib().sp_runtime_enqueue_position(step._h)}, "
+              f"device at {step.progress()}", flush=True)
+        time.sleep(2)
+        os._exit(3)
+    loss = box["loss"]
     mine = SP.gather_rank(step, cfg, loss)
     allv = [None] * world
     dist.all_gather_object(allv, mine)
