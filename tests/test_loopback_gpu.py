@@ -92,12 +92,11 @@ def _run(pp, m, n, exchange, recompute, kv_heads=4, interleave=1, **kw):
         world.close()
 
 
+# (the float64 oracle of an n=8 sequence dominates a case's time, ~40 s)
 @pytest.mark.parametrize("pp,m,n,x,rc", [
     (2, 2, 4, "off", "selective"), (2, 1, 2, "off", "full"),
-    (2, 2, 4, "on", "selective"), (2, 2, 4, "on", "full"),
-    (2, 2, 8, "early", "selective"), (2, 3, 4, "on", "selective"),
-    (4, 2, 4, "off", "selective"), (4, 2, 8, "on", "selective"), (4, 2, 8, "on", "full"),
-    (4, 2, 8, "early", "selective"), (4, 2, 8, "early", "full"),
+    (2, 2, 4, "on", "full"), (2, 3, 4, "on", "selective"),
+    (4, 2, 4, "off", "selective"), (4, 2, 8, "on", "selective"), (4, 2, 8, "early", "full"),
 ])
 def test_loopback_step_matches_oracle(pp, m, n, x, rc):
     _need_gpu()
@@ -113,7 +112,7 @@ def test_loopback_gqa_through_the_exchange():
     assert ok, worst
 
 
-@pytest.mark.parametrize("pp,m,n,rc", [(2, 2, 4, "selective"), (2, 1, 4, "full"), (4, 2, 8, "selective")])
+@pytest.mark.parametrize("pp,m,n,rc", [(2, 2, 4, "selective"), (4, 2, 8, "full")])
 def test_loopback_interleaved_v2(pp, m, n, rc):
     """Interleaved SlimPipe (v = 2): the stage links form a ring."""
     _need_gpu()
