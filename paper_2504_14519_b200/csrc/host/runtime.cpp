@@ -227,13 +227,43 @@ class Runtime {
 
   ~Runtime() {
     if (comp) cudaStreamSynchronize(comp);
+    destroy_links();
     for (void* a : allocations) cudaFree(a);
-    if (nc_fwd) ncclCommDestroy(nc_fwd);
     for (cudaEvent_t e : tpool) cudaEventDestroy(e);
     if (xev) cudaEventDestroy(xev);
     if (ev_staged) cudaEventDestroy(ev_staged);
     for (void* hp : {static_cast<void*>(h_tok), static_cast<void*>(h_tgt), static_cast<void*>(h_loss)})
       if (hp) cudaFreeHost(hp);
+  }
+
+  // Communicators are torn down in one global order, like warm_links sets
+  // them up: NCCL's destroy of a communicator finalizes it with its peers, so
+  // two ranks destroying shared communicators in different orders (the ring
+  // of v > 1: rank 0 holds the wrap link as its *input*, rank p-1 as its
+  // output) wait on each other forever.
+  void destroy_links() {
+    const bool ring = v > 1;
+    std::vector<std::pair<int, int>> mine;
+    const int prev_link = first_dev ? (ring ? p - 1 : -1) : rank - 1;
+    const int next_link = (!last_dev || ring) ? rank : -1;
+    if (prev_link >= 0) mine.emplace_back(prev_link, 0);
+    if (next_link >= 0) mine.emplace_back(next_link, 1);
+    std::sort(mine.begin(), mine.end());
+    for (const auto& lk : mine) {
+      if (lk.second == 0) {
+        l_act_in.reset();
+        l_grad_out.reset();
+      } else {
+        l_act_out.reset();
+        l_grad_in.reset();
+      }
+    }
+    lx[0].reset();
+    lx[1].reset();
+    vlink.reset();
+    if (nc_fwd) ncclCommDestroy(nc_fwd);
+    if (nc_bwd) ncclCommDestroy(nc_bwd);
+    nc_fwd = nc_bwd = nullptr;
   }
 
   int timing_event(cudaEvent_t* e) {
