@@ -5,7 +5,7 @@ per GPU) and tests/test_loopback_gpu.py (every rank a thread on one GPU).
 
 Tolerances: loss rel 1e-2; every parameter gradient max|g - ref| <=
 GRAD_TOL * max|ref| per tensor (bf16 activations through the whole stack;
-the measured worst case is printed).
+the measured worst case, 0.7-1.15 %, is printed).
 """
 from __future__ import annotations
 
@@ -18,7 +18,7 @@ ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT / "oracle"))
 
 NAMES = ["attn_norm", "wqkv", "wo", "mlp_norm", "wgu", "wd"]
-GRAD_TOL = 5e-2
+GRAD_TOL = 2.5e-2
 LOSS_TOL = 1e-2
 
 
