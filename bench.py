@@ -400,6 +400,12 @@ def main():
     mem = step.memory()
     at_tot = {k: sum_over_ranks(float(v)) for k, v in at.items()}
     launches_all = int(sum_over_ranks(float(launches)))
+    # cuBLASLt candidates timed at create (runtime warm-up): shapes where a
+    # non-default algorithm won, and the per-call time saved
+    plans = json.loads(native._json_call("sp_gemm_plans_json"))
+    won = [q for q in plans if q["chosen"] != 0]
+    gemm_tune = {"shapes": len(plans), "non_default": len(won),
+                 "ms_saved_per_call": sum(q["ms_first"] - q["ms_chosen"] for q in won)}
     # stage P2P over NVLink: fastest message of any rank (link rate once the
     # receive is posted) and the mean over all stage sends of the last step
     link = None
@@ -487,6 +493,7 @@ def main():
                          "attn_bwd_tflops": (at_tot["bwd_flops"] / max(1e-9, at_tot["bwd_ms"] / 1e3)) / 1e12,
                          "attn_share_of_step": (at_tot["fwd_ms"] + at_tot["bwd_ms"]) / world / step_ms},
             "stage_p2p": link,
+            "gemm_autotune": gemm_tune,
             "gpu_launches": launches_all,
             "clocks": clk,
             "e2e": e2e,

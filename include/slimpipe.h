@@ -51,6 +51,10 @@ void sp_free(char* p);
 int sp_version(void);
 long long sp_launch_count(void);         /* kernels launched by this library so far */
 long long sp_library_launch_count(void); /* cuBLASLt GEMM calls so far */
+/* GEMM plans so far (JSON list: shape, cuBLASLt candidates, the one kept,
+ * its time and the heuristic's first choice's; the runtime times candidates
+ * during its create-time warm-up).  Free with sp_free. */
+int sp_gemm_plans_json(char** out);
 
 /* ---------------------------------------------------------------- planning
  * scheme: 0 gpipe 1 terapipe 2 1f1b 3 interleaved_1f1b 4 zbv 5 vhalf 6 slimpipe

@@ -5,7 +5,11 @@
 // path, are the hand-written tcgen05 kernels in attn_fwd.cu / attn_bwd.cu.)
 #include <cublasLt.h>
 
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
 #include <map>
+#include <string>
 #include <mutex>
 #include <tuple>
 
@@ -18,6 +22,8 @@ struct Plan {
   cublasLtMatmulDesc_t op = nullptr;
   cublasLtMatrixLayout_t a = nullptr, b = nullptr, c = nullptr;
   cublasLtMatmulAlgo_t algo{};
+  int chosen = 0, candidates = 1;      // index among the heuristic's candidates
+  float ms_chosen = 0.f, ms_first = 0.f;  // timed when autotuned (ms per call)
 };
 
 using Key = std::tuple<int, bool, bool, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, bool>;
@@ -30,6 +36,7 @@ struct State {
   size_t ws_bytes = 64ull << 20;
   std::map<Key, Plan> plans;
   std::mutex mu;
+  bool tune = false;  // new plans time the heuristic's top candidates and keep the fastest
 };
 
 State& state() {
@@ -73,14 +80,49 @@ int gemm(bool trans_a, bool trans_b, int64_t M, int64_t N, int64_t K, const void
     cublasLtMatmulPreferenceCreate(&pref);
     cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &S.ws_bytes,
                                          sizeof S.ws_bytes);
-    cublasLtMatmulHeuristicResult_t res{};
+    constexpr int kCand = 6;
+    cublasLtMatmulHeuristicResult_t res[kCand]{};
     int found = 0;
-    cublasStatus_t hs = cublasLtMatmulAlgoGetHeuristic(S.lt, p.op, p.a, p.b, p.c, p.c, pref, 1, &res, &found);
+    cublasStatus_t hs =
+        cublasLtMatmulAlgoGetHeuristic(S.lt, p.op, p.a, p.b, p.c, p.c, pref, S.tune ? kCand : 1, res, &found);
     cublasLtMatmulPreferenceDestroy(pref);
     if (hs != CUBLAS_STATUS_SUCCESS || found == 0)
       return set_error(SP_ERR_CUDA, "cuBLASLt: no algorithm for %lldx%lldx%lld", (long long)M, (long long)N,
                        (long long)K);
-    p.algo = res.algo;
+    p.algo = res[0].algo;
+    p.candidates = found;
+    if (S.tune && found > 1) {
+      // autotune (runtime warm-up, before any communication): time every
+      // candidate on the call's own operands and keep the fastest
+      cudaEvent_t e0, e1;
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      float best = 0.f;
+      for (int x = 0; x < found; ++x) {
+        auto run = [&]() {
+          return cublasLtMatmul(S.lt, p.op, &alpha, B, p.a, A, p.b, &beta, c_in ? c_in : C, p.c, C, p.c, &res[x].algo,
+                                ws, S.ws_bytes, st);
+        };
+        if (run() != CUBLAS_STATUS_SUCCESS) continue;
+        cudaEventRecord(e0, st);
+        for (int r = 0; r < 3; ++r) run();
+        cudaEventRecord(e1, st);
+        cudaEventSynchronize(e1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        ms /= 3.f;
+        if (x == 0) p.ms_first = ms;
+        if (x == 0 || ms < best) {
+          best = ms;
+          p.algo = res[x].algo;
+          p.chosen = x;
+        }
+      }
+      p.ms_chosen = best;
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+      if (int rc = cuda_status(cudaGetLastError(), "gemm autotune")) return rc;
+    }
     it = S.plans.emplace(key, p).first;
   }
   const Plan& p = it->second;
@@ -92,4 +134,34 @@ int gemm(bool trans_a, bool trans_b, int64_t M, int64_t N, int64_t K, const void
                    "matmul");
 }
 
+void gemm_autotune(bool on) {
+  std::lock_guard<std::mutex> g(state().mu);
+  state().tune = on;
+}
+
+std::string gemm_plans_json() {
+  State& S = state();
+  std::lock_guard<std::mutex> g(S.mu);
+  std::string out = "[";
+  for (const auto& [k, p] : S.plans) {
+    char buf[256];
+    std::snprintf(buf, sizeof buf,
+                  "%s{\"M\": %lld, \"N\": %lld, \"K\": %lld, \"trans_a\": %d, \"trans_b\": %d, \"c_f32\": %d, "
+                  "\"candidates\": %d, \"chosen\": %d, \"ms_first\": %.4f, \"ms_chosen\": %.4f}",
+                  out.size() > 1 ? ", " : "", (long long)std::get<3>(k), (long long)std::get<4>(k),
+                  (long long)std::get<5>(k), int(std::get<1>(k)), int(std::get<2>(k)), int(std::get<9>(k)),
+                  p.candidates, p.chosen, p.ms_first, p.ms_chosen);
+    out += buf;
+  }
+  return out + "]";
+}
+
 }  // namespace sp
+
+extern "C" int sp_gemm_plans_json(char** out) {
+  const std::string s = sp::gemm_plans_json();
+  *out = static_cast<char*>(std::malloc(s.size() + 1));
+  if (!*out) return SP_ERR_RUNTIME;
+  std::memcpy(*out, s.c_str(), s.size() + 1);
+  return SP_OK;
+}

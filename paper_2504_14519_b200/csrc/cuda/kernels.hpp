@@ -90,5 +90,8 @@ int attn_bwd_d128(const void* q, int64_t q_rows, int64_t q_stride, const void* k
 int gemm(bool trans_a, bool trans_b, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, const void* B,
          int64_t ldb, void* C, int64_t ldc, bool c_f32, float alpha, float beta, cudaStream_t st,
          const void* c_in = nullptr);
+// while on, a GEMM shape seen for the first time times cuBLASLt's top
+// candidates on its own operands and keeps the fastest (runtime warm-up only)
+void gemm_autotune(bool on);
 
 }  // namespace sp

@@ -435,6 +435,12 @@ class Runtime {
   // a receive spins can deadlock (preload_kernels, transport.cu).  The
   // gradient buffers the weight-gradient GEMMs touched are zeroed again.
   int warm_gemms() {
+    gemm_autotune(true);
+    const int rc = warm_gemms_body();
+    gemm_autotune(false);
+    return rc;
+  }
+  int warm_gemms_body() {
     LayerWs& x = ws[0];
     const LayerParams& P = lp[0];
     SP_TRY(gemm(false, true, Ls, qkv_w, h, x.xn, h, W(P.wqkv), h, qkv, qkv_w, false, 1.f, 0.f, comp));

@@ -35,6 +35,7 @@ _SIGS = {
     "sp_version": (C.c_int, []),
     "sp_launch_count": (C.c_longlong, []),
     "sp_library_launch_count": (C.c_longlong, []),
+    "sp_gemm_plans_json": (C.c_int, [_charpp]),
     "sp_plan_schedule_json": (C.c_int, [C.c_int] * 5 + [_charpp]),
     "sp_plan_validate_json": (C.c_int, [C.c_int] * 5 + [_charpp]),
     "sp_plan_balance_json": (C.c_int, [_i64p, _i32p, C.c_int, C.c_int, _charpp]),
