@@ -486,6 +486,11 @@ def main():
                                             if calib else None),
             "peak_act_gb_per_gpu": arena_gb, "dkv_accum_gb_per_gpu": dkv_gb, "ledger_pred_gb_per_gpu": ledger_gb,
             "arena_slots": mem["slots"], "arena_high_water": mem["slots_high_water"],
+            # logits workspace of the stage(s) holding the LM head: [Ls, V] fp32 logits + dlogits
+            # (last stage), or the [Ls, V/p] shard (fp32 logits + bf16 dlogits) on every stage
+            # under vocabulary parallelism (reference logits_bytes, workload.cpp:154-160)
+            "logits_gb_per_gpu": (cfg.slice_len * (cfg.vocab // world) * 6 if cfg.vocab_parallel
+                                  else cfg.slice_len * cfg.vocab * 8) / 1e9,
             "roofline": {"kernel": f"sp_attn_{kind} (sm_100a tcgen05)", "bound": "tensor", "achieved": achieved,
                          "peak": peak_tf, "unit": "TFLOP/s", "frac": achieved / peak_tf, "traffic": traffic,
                          "peak_source": f"{peak_src} bf16 sustained",
