@@ -23,8 +23,6 @@
 #include "kernels.hpp"
 #include "sm100.cuh"
 
-#include <cstdlib>
-
 
 namespace sp {
 namespace {
@@ -390,14 +388,12 @@ int attn_bwd_d128(const void* q, int64_t q_rows, int64_t q_stride, const void* k
     prm.chunk_row[c] = chunk_row[c];
     prm.acc_row[c] = acc_row[c];
   }
-  // SP_BWD_VARIANT (A/B measurements, read once): 0 = NS 3, one dS tile,
-  // 64-row dQ stage; 1 = NS 4 with a 32-row stage (fits only without the
-  // alignment pad); 2 = NS 3, two dS tiles, 32-row stage
-  static const int variant = [] {
-    const char* e = std::getenv("SP_BWD_VARIANT");
-    return e ? std::atoi(e) : 0;
-  }();
-  const int stq = variant == 0 ? BQ : 32;
+  // NS = 3 Q/dO stages, one dS tile, 64-row dQ stage: measured best
+  // (scripts/k2_ab.py, profiles/r02_k2_ab.json): NS = 2 costs 11-12 %, a 32-row
+  // dQ stage (two reduces per pair, what NS = 4 needs to fit 227 KB) 10-13 %,
+  // a second dS tile +1 % at most
+  constexpr int kNS = 3, kNDS = 1, kSTQ = 64;
+  const int stq = kSTQ;
   CUtensorMap tq, tdo, tk, tv, tdq;
   if (!make_tmap_bf16(&tq, q, uint64_t(q_stride), uint64_t(q_rows), uint64_t(q_stride), BQ) ||
       !make_tmap_bf16(&tdo, dout, uint64_t(do_stride), uint64_t(q_rows), uint64_t(do_stride), BQ) ||
@@ -405,20 +401,11 @@ int attn_bwd_d128(const void* q, int64_t q_rows, int64_t q_stride, const void* k
       !make_tmap_bf16(&tv, v_pool, uint64_t(kv_stride), uint64_t(pool_rows), uint64_t(kv_stride), BK) ||
       !make_tmap_f32(&tdq, dq_acc, uint64_t(heads) * D, uint64_t(q_rows), uint64_t(heads) * D, D, uint32_t(stq)))
     return set_error(SP_ERR_CUDA, "attn_bwd_d128: cuTensorMapEncodeTiled failed (alignment?)");
-  auto launch = [&](auto kern, size_t smem) -> int {
-    if (int rc = set_smem_once(reinterpret_cast<const void*>(kern), smem, "attn_bwd_d128: set smem")) return rc;
-    kern<<<dim3(prm.total_kv / BK, kv_heads), kThreads, smem, st>>>(tq, tdo, tk, tv, tdq, prm);
-    count_launch(1);
-    return SP_OK;
-  };
-  int rc = SP_OK;
-  if (variant == 1)
-    rc = launch(attn_bwd_d128_kernel<4, 1, 32, false>, sizeof(Smem<4, 1, 32>) + sizeof(Ctl<4>));
-  else if (variant == 2)
-    rc = launch(attn_bwd_d128_kernel<3, 2, 32, true>, sizeof(Smem<3, 2, 32>) + sizeof(Ctl<3>) + 1024);
-  else
-    rc = launch(attn_bwd_d128_kernel<3, 1, 64, true>, sizeof(Smem<3, 1, 64>) + sizeof(Ctl<3>) + 1024);
-  if (rc) return rc;
+  auto kern = attn_bwd_d128_kernel<kNS, kNDS, kSTQ, true>;
+  const size_t smem = sizeof(Smem<kNS, kNDS, kSTQ>) + sizeof(Ctl<kNS>) + 1024;
+  if (int rc = set_smem_once(reinterpret_cast<const void*>(kern), smem, "attn_bwd_d128: set smem")) return rc;
+  kern<<<dim3(prm.total_kv / BK, kv_heads), kThreads, smem, st>>>(tq, tdo, tk, tv, tdq, prm);
+  count_launch(1);
   return cuda_status(cudaGetLastError(), "attn_bwd_d128 launch");
 }
 
@@ -426,10 +413,8 @@ int attn_bwd_d128(const void* q, int64_t q_rows, int64_t q_stride, const void* k
 // Force-load this file's kernels (cudaFuncGetAttributes) — see preload_kernels
 int preload_attn_bwd_v2() {
   cudaFuncAttributes a;
-  for (const void* k : {reinterpret_cast<const void*>(attn_bwd_d128_kernel<3, 1, 64, true>),
-                        reinterpret_cast<const void*>(attn_bwd_d128_kernel<4, 1, 32, false>),
-                        reinterpret_cast<const void*>(attn_bwd_d128_kernel<3, 2, 32, true>)})
-    if (cudaError_t e = cudaFuncGetAttributes(&a, k)) return cuda_status(e, "preload attn_bwd_d128_kernel");
+  if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(attn_bwd_d128_kernel<3, 1, 64, true>)))
+    return cuda_status(e, "preload attn_bwd_d128_kernel");
   return SP_OK;
 }
 }  // namespace sp

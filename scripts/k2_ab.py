@@ -1,5 +1,7 @@
-"""K2 A/B: time the backward kernel variants (SP_BWD_VARIANT, one process
-each) on the c2 representative slices and check they agree with variant 0.
+"""K2 A/B: time backward kernel variants on the c2 representative slices,
+one process per variant (the library read SP_BWD_VARIANT once while the
+variants were compiled in; the winner is now the only build — see
+profiles/r02_k2_ab.json for the measured variants), and check they agree.
 Writes gpurun_out/k2_ab.json."""
 import json
 import os

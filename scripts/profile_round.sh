@@ -24,10 +24,4 @@ echo "attn full rc=$?"
 # K2 variants (SP_BWD_VARIANT 0/1/2, scripts/k2_ab.py)
 timeout 600 python scripts/k2_ab.py > gpurun_out/r02_k2ab2.log 2>&1
 echo "k2 a/b rc=$?"
-# compute-sanitizer on K1 / K2 / K3 at c1-size shapes
-timeout 900 compute-sanitizer --tool memcheck --leak-check full python -m pytest tests/test_attn_gpu.py \
-  tests/test_attn_bwd_gpu.py -q -x -k "multihead or merge or sliced" > gpurun_out/r02_memcheck.log 2>&1
-echo "memcheck rc=$?"
-timeout 900 compute-sanitizer --tool racecheck python -m pytest tests/test_attn_gpu.py tests/test_attn_bwd_gpu.py \
-  -q -x -k "128-4-4-1-128-True or 64-4-4-4-256-True or 128-2-2-1-128" > gpurun_out/r02_racecheck.log 2>&1
-echo "racecheck rc=$?"
+# (compute-sanitizer is closed on this GPU pool: runs under it left GPUs needing a reset)
