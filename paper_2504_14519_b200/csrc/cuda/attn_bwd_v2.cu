@@ -23,13 +23,22 @@
 #include "kernels.hpp"
 #include "sm100.cuh"
 
+#include <cstdlib>
+
 
 namespace sp {
 namespace {
 
 constexpr int D = 128, BQ = 64, BK = 128;
-constexpr int kThreads = 480;
-constexpr int kCompute = 256;
+// NWG element-math warpgroups (2: 32 query columns per thread, 4: 16); warps:
+// 0 TMA producer, 1 TMEM owner + S/dP issuer, 2 .. 2+4*NWG-1 element math,
+// then the 4 dQ drain warps and the dQ/dV/dK issuer
+template <int NWG>
+struct Roles {
+  static constexpr int kEm0 = 2, kDrain0 = 2 + 4 * NWG, kIssueB = kDrain0 + 4;
+  static constexpr int kThreads = 32 * (kIssueB + 1);
+  static constexpr int kCompute = 128 * NWG;
+};
 constexpr int kDrain = 128;
 constexpr int kSlabQ = BQ * 64, kSlabK = BK * 64;  // elements per slab
 
@@ -75,8 +84,8 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
                : "memory");
 }
 
-template <int NS, int NDS, int STQ, bool kPad>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int NS, int NDS, int STQ, bool kPad, int NWG>
+__global__ void __launch_bounds__(Roles<NWG>::kThreads, 1)
     attn_bwd_d128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
                          const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                          const __grid_constant__ CUtensorMap tm_dq, const __grid_constant__ Params prm) {
@@ -122,7 +131,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&ctl.dq_free[b], kDrain);
       mbar_init(&ctl.acc_free[b], 1);
     }
-    mbar_init(&ctl.pds_ready, kCompute);
+    mbar_init(&ctl.pds_ready, Roles<NWG>::kCompute);
     mbar_init(&ctl.pds_free, 1);
     mbar_init(&ctl.acc_done, 1);
     fence_barrier_init();
@@ -156,7 +165,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         bulk_load(ctl.delta[s], prm.delta + int64_t(h) * prm.q_rows + qrow, BQ * 4, &ctl.q_full[s]);
       }
     }
-  } else if (warp == 1 || warp == 14) {
+  } else if (warp == 1 || warp == Roles<NWG>::kIssueB) {
     // Two issuing warps, each a whole warp with one elected lane per UMMA
     // (sm100.cuh *_w / umma_commit_warp): warp 1 issues S^T/dP^T, warp 14
     // dQ^T, dV, dK.  tcgen05 issue blocks for about the duration of the group
@@ -223,16 +232,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         umma_commit_warp(&ctl.acc_done);
       }
     }
-  } else if (warp < 10) {
-    // ------------------------------------------------ element math (2 WGs)
-    const int cw = warp - 2;         // 0..7
-    const int wg = cw >> 2;          // column half of every pair
+  } else if (warp < Roles<NWG>::kDrain0) {
+    // --------------------------------------------- element math (NWG WGs)
+    constexpr int CW = BQ / NWG;     // query columns of every pair per thread
+    const int cw = warp - 2;
+    const int wg = cw >> 2;          // column group of every pair
     const int quarter = warp & 3;    // TMEM lane quarter
     const int r = quarter * 32 + lane;
-    const int ctid = cw * 32 + lane;  // 0..255
     const uint32_t lane_off = uint32_t(quarter * 32) << 16;
     const int key_rel = key0 - off + r;
-    const int c0 = wg * 32;
+    const int c0 = wg * CW;
+    // P^T of queries [16kk, +16) sits at column (kk/2)*32 + (kk%2)*8 of the
+    // buffer, dS^T 16 columns further (the dV / dK TS-UMMA A layout)
+    const uint32_t pcol = NWG == 2 ? uint32_t(wg * 32) : uint32_t((wg >> 1) * 32 + (wg & 1) * 8);
 
     for (int j = 0; j < n_pairs; ++j) {
       const int s = j % NS, b = j & 1;
@@ -242,23 +254,28 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&ctl.q_full[s], (j / NS) & 1);
       mbar_wait(&ctl.sdp_full[b], (j >> 1) & 1);
       tc_fence_after();
-      float sv[32], dp[32];
-      tmem_ld32(tmem + lane_off + b * 128 + c0, sv);
-      tmem_ld32(tmem + lane_off + b * 128 + 64 + c0, dp);
+      float sv[CW], dp[CW];
+      if constexpr (CW == 32) {
+        tmem_ld32(tmem + lane_off + b * 128 + c0, sv);
+        tmem_ld32(tmem + lane_off + b * 128 + 64 + c0, dp);
+      } else {
+        tmem_ld16(tmem + lane_off + b * 128 + c0, sv);
+        tmem_ld16(tmem + lane_off + b * 128 + 64 + c0, dp);
+      }
       tmem_wait_ld();
       // P = exp2(S*scale*log2e - lse2), dS = P * (dP - delta) * scale on
       // packed fp32x2 (FFMA2/FMUL2); statistics come from smem 8 columns at a
       // time with 128-bit loads (they are uniform across the warp)
-      uint32_t pk[16], dk[16];
+      uint32_t pk[CW / 2], dk[CW / 2];
       // per-query statistics: one coalesced load per warp (lane i holds column
       // c0+i), then warp shuffles -- a broadcast LDS.128 per 4 columns cost 4
       // shared-memory wavefronts and was ~20 % of this kernel's smem traffic
-      const float my_nl = -ctl.lse2[s][c0 + lane];
-      const float my_nd = -ctl.delta[s][c0 + lane] * prm.scale;
+      const float my_nl = -ctl.lse2[s][c0 + (lane % CW)];
+      const float my_nd = -ctl.delta[s][c0 + (lane % CW)] * prm.scale;
       const float2 sl2x2 = make_float2(prm.scale_log2, prm.scale_log2);
       const float2 scx2 = make_float2(prm.scale, prm.scale);
 #pragma unroll
-      for (int x = 0; x < 32; x += 2) {
+      for (int x = 0; x < CW; x += 2) {
         const float2 nl = make_float2(__shfl_sync(0xffffffffu, my_nl, x), __shfl_sync(0xffffffffu, my_nl, x + 1));
         const float2 nd = make_float2(__shfl_sync(0xffffffffu, my_nd, x), __shfl_sync(0xffffffffu, my_nd, x + 1));
         const float2 t = ffma2(make_float2(sv[x], sv[x + 1]), sl2x2, nl);
@@ -276,10 +293,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t ds_a = smem_u32(sm.ds[NDS == 1 ? 0 : b]);
       // P^T / dS^T (packed bf16) over this WG's own S^T columns: A operands of
       // the dV / dK TS-UMMAs; dS^T also to smem: B operand of dQ^T = K^T dS^T.
-      tmem_st16(tmem + lane_off + b * 128 + wg * 32, pk);
-      tmem_st16(tmem + lane_off + b * 128 + wg * 32 + 16, dk);
+      if constexpr (CW == 32) {
+        tmem_st16(tmem + lane_off + b * 128 + pcol, pk);
+        tmem_st16(tmem + lane_off + b * 128 + pcol + 16, dk);
+      } else {
+        tmem_st8(tmem + lane_off + b * 128 + pcol, pk);
+        tmem_st8(tmem + lane_off + b * 128 + pcol + 16, dk);
+      }
 #pragma unroll
-      for (int g = 0; g < 4; ++g)
+      for (int g = 0; g < CW / 8; ++g)
         st_shared_v4(ds_a + sw128_offset(r, c0 + g * 8), dk[4 * g], dk[4 * g + 1], dk[4 * g + 2], dk[4 * g + 3]);
       tmem_wait_st();
       fence_async_smem();
@@ -292,10 +314,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&ctl.acc_done, 0);
       tc_fence_after();
       const int64_t arow = prm.acc_row[chunk] + key0 % prm.chunk_len + r;
-      float* dst = (wg == 0 ? prm.dk : prm.dv) + arow * prm.acc_stride + kvh * D;
-      const uint32_t col = wg == 0 ? kDK : kDV;
+      // WG halves: dK then dV; with 4 WGs each takes 64 of the 128 columns
+      const bool is_k = wg < NWG / 2;
+      const int c_base = NWG == 2 ? 0 : (wg % 2) * 64;
+      float* dst = (is_k ? prm.dk : prm.dv) + arow * prm.acc_stride + kvh * D + c_base;
+      const uint32_t col = (is_k ? kDK : kDV) + c_base;
 #pragma unroll
-      for (int ch = 0; ch < D / 32; ++ch) {
+      for (int ch = 0; ch < D / 32 / (NWG / 2); ++ch) {
         float a[32];
         tmem_ld32(tmem + lane_off + col + ch * 32, a);
         tmem_wait_ld();
@@ -308,14 +333,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     tc_fence_before();
-  } else if (warp < 14) {
+  } else if (warp < Roles<NWG>::kIssueB) {
     // --------------------------------------------- dQ drain (one warpgroup)
     // dQ^T of pair jj sits in its consumed dP^T columns (lane = head dim d,
     // columns = the pair's 64 queries): TMEM -> registers (frees the columns
     // for the S/dP of pair jj+2) -> smem stage [q][d] -> TMA reduce-add.
     const int quarter = warp & 3;
     const int d = quarter * 32 + lane;
-    const int dtid = (warp - 10) * 32 + lane;
+    const int dtid = (warp - Roles<NWG>::kDrain0) * 32 + lane;
     const uint32_t lane_off = uint32_t(quarter * 32) << 16;
     for (int jj = 0; jj < n_pairs; ++jj) {
       const int bb = jj & 1;
@@ -401,11 +426,21 @@ int attn_bwd_d128(const void* q, int64_t q_rows, int64_t q_stride, const void* k
       !make_tmap_bf16(&tv, v_pool, uint64_t(kv_stride), uint64_t(pool_rows), uint64_t(kv_stride), BK) ||
       !make_tmap_f32(&tdq, dq_acc, uint64_t(heads) * D, uint64_t(q_rows), uint64_t(heads) * D, D, uint32_t(stq)))
     return set_error(SP_ERR_CUDA, "attn_bwd_d128: cuTensorMapEncodeTiled failed (alignment?)");
-  auto kern = attn_bwd_d128_kernel<kNS, kNDS, kSTQ, true>;
+  // SP_BWD_NWG (A/B, read once): element-math warpgroups, 2 (default) or 4
+  static const int nwg = [] {
+    const char* e = std::getenv("SP_BWD_NWG");
+    return e && std::atoi(e) == 4 ? 4 : 2;
+  }();
   const size_t smem = sizeof(Smem<kNS, kNDS, kSTQ>) + sizeof(Ctl<kNS>) + 1024;
-  if (int rc = set_smem_once(reinterpret_cast<const void*>(kern), smem, "attn_bwd_d128: set smem")) return rc;
-  kern<<<dim3(prm.total_kv / BK, kv_heads), kThreads, smem, st>>>(tq, tdo, tk, tv, tdq, prm);
-  count_launch(1);
+  auto launch = [&](auto kern, int threads) -> int {
+    if (int rc = set_smem_once(reinterpret_cast<const void*>(kern), smem, "attn_bwd_d128: set smem")) return rc;
+    kern<<<dim3(prm.total_kv / BK, kv_heads), threads, smem, st>>>(tq, tdo, tk, tv, tdq, prm);
+    count_launch(1);
+    return SP_OK;
+  };
+  const int rc = nwg == 4 ? launch(attn_bwd_d128_kernel<kNS, kNDS, kSTQ, true, 4>, Roles<4>::kThreads)
+                          : launch(attn_bwd_d128_kernel<kNS, kNDS, kSTQ, true, 2>, Roles<2>::kThreads);
+  if (rc) return rc;
   return cuda_status(cudaGetLastError(), "attn_bwd_d128 launch");
 }
 
@@ -413,8 +448,9 @@ int attn_bwd_d128(const void* q, int64_t q_rows, int64_t q_stride, const void* k
 // Force-load this file's kernels (cudaFuncGetAttributes) — see preload_kernels
 int preload_attn_bwd_v2() {
   cudaFuncAttributes a;
-  if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(attn_bwd_d128_kernel<3, 1, 64, true>)))
-    return cuda_status(e, "preload attn_bwd_d128_kernel");
+  for (const void* k : {reinterpret_cast<const void*>(attn_bwd_d128_kernel<3, 1, 64, true, 2>),
+                        reinterpret_cast<const void*>(attn_bwd_d128_kernel<3, 1, 64, true, 4>)})
+    if (cudaError_t e = cudaFuncGetAttributes(&a, k)) return cuda_status(e, "preload attn_bwd_d128_kernel");
   return SP_OK;
 }
 }  // namespace sp

@@ -54,7 +54,8 @@ if __name__ == "__main__":
         sys.exit(0)
     res = {}
     for v in os.environ.get("VARIANTS", "0 1 2").split():
-        r = subprocess.run([sys.executable, __file__, "child"], env=dict(os.environ, SP_BWD_VARIANT=v),
+        var = os.environ.get("VARIANT_VAR", "SP_BWD_VARIANT")
+        r = subprocess.run([sys.executable, __file__, "child"], env=dict(os.environ, **{var: v}),
                            capture_output=True, text=True, timeout=600)
         line = [x for x in r.stdout.splitlines() if x.startswith("{")]
         res[v] = json.loads(line[-1]) if line else {"error": r.stderr[-2000:]}
