@@ -70,6 +70,10 @@ def lib() -> C.CDLL:
         if not LIB_PATH.exists():
             raise RuntimeError(f"{LIB_PATH} is not built; run `python -m paper_2504_14519_b200.build` "
                                "(there is no fallback implementation)")
+        # torch first: the library links NCCL by soname, and the process must
+        # hold torch's (newer) libnccl.so.2 — loaded after an older system copy,
+        # libtorch_cuda fails on symbols the older one lacks
+        import torch  # noqa: F401
         handle = C.CDLL(str(LIB_PATH), mode=os.RTLD_NOW | os.RTLD_LOCAL)
         for name, (res, args) in _SIGS.items():
             fn = getattr(handle, name, None)

@@ -8,11 +8,9 @@ exactly as under NCCL, and the assembled model is compared with the float64
 oracle (tests/step_parity.py tolerances)."""
 from __future__ import annotations
 
-import numpy as np
 import pytest
 import torch
 
-import step_parity as SP
 from test_attn_gpu import _need_gpu
 
 pytestmark = pytest.mark.gpu
@@ -72,43 +70,43 @@ def test_loopback_transport_pingpong():
     assert int(bufs[0][1].min()) == 2 and int(bufs[1][1].max()) == 1
 
 
-def _run(pp, m, n, exchange, recompute, kv_heads=4, interleave=1, **kw):
-    from paper_2504_14519_b200.runtime import LoopbackWorld, SlimPipeStep, StepConfig
-    cfg = StepConfig.c1(pp=pp, microbatches=m, slices=n, layers=2 * pp * interleave, exchange=exchange,
-                        seq_len=1024 * n, recompute=recompute, kv_heads=kv_heads, interleave=interleave, **kw)
-    world = LoopbackWorld(pp)
-    steps = [SlimPipeStep(cfg, r, pp, loopback=world) for r in range(pp)]
+def _run(pp, m, n, exchange, recompute, kv_heads=4, interleave=1, vocab_parallel=False):
+    """One case in its own process (tests/loopback_step_check.py): a stall
+    ends that process and its GPU context, not the session."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    args = [sys.executable, str(root / "tests" / "loopback_step_check.py"), str(pp), str(m), str(n), exchange,
+            recompute, str(kv_heads), str(interleave), "1" if vocab_parallel else "0"]
     try:
-        tok, tgt = SP.inputs(cfg)
-        torch.cuda.synchronize()
-        losses = world.run(lambda r: steps[r].step(tok, tgt, optimizer=False), timeout=120, steps=steps)
-        assert world.errors() == 0, "loopback transport saw mismatched message sizes"
-        allv = [SP.gather_rank(steps[r], cfg, losses[r]) for r in range(pp)]
-        ok, worst, _ = SP.compare(cfg, allv, tok, tgt)
-        return ok, worst, [s.exchange_stats() for s in steps]
-    finally:
-        for s in steps:
-            s.close()
-        world.close()
+        r = subprocess.run(args, capture_output=True, text=True, timeout=300,
+                           env=dict(os.environ, PYTHONUNBUFFERED="1"))
+    except subprocess.TimeoutExpired as e:
+        print(e.stdout or "", e.stderr or "")
+        return False, "timeout"
+    print(r.stdout[-4000:], r.stderr[-3000:])
+    worst = [ln for ln in r.stdout.splitlines() if ln.startswith("worst grad err")]
+    return r.returncode == 0, worst[-1] if worst else r.returncode
 
 
 # (the float64 oracle of an n=8 sequence dominates a case's time, ~40 s)
 @pytest.mark.parametrize("pp,m,n,x,rc", [
     (2, 2, 4, "off", "selective"), (2, 1, 2, "off", "full"),
-    (2, 2, 4, "on", "full"), (2, 3, 4, "on", "selective"),
+    (2, 2, 4, "on", "full"), (2, 2, 8, "early", "selective"),
     (4, 2, 4, "off", "selective"), (4, 2, 8, "on", "selective"), (4, 2, 8, "early", "full"),
 ])
 def test_loopback_step_matches_oracle(pp, m, n, x, rc):
+    """(the child also checks that exchange on / early really moved work)"""
     _need_gpu()
-    ok, worst, xs = _run(pp, m, n, x, rc)
+    ok, worst = _run(pp, m, n, x, rc)
     assert ok, worst
-    if x != "off":  # the tick plans really moved attention work
-        assert sum(s["passes_out"] for s in xs) > 0 and sum(s["bytes_sent"] for s in xs) > 0
 
 
 def test_loopback_gqa_through_the_exchange():
     _need_gpu()
-    ok, worst, _ = _run(2, 2, 4, "on", "selective", kv_heads=2)
+    ok, worst = _run(2, 2, 4, "on", "selective", kv_heads=2)
     assert ok, worst
 
 
@@ -116,7 +114,7 @@ def test_loopback_gqa_through_the_exchange():
 def test_loopback_interleaved_v2(pp, m, n, rc):
     """Interleaved SlimPipe (v = 2): the stage links form a ring."""
     _need_gpu()
-    ok, worst, _ = _run(pp, m, n, "off", rc, interleave=2)
+    ok, worst = _run(pp, m, n, "off", rc, interleave=2)
     assert ok, worst
 
 
@@ -126,5 +124,5 @@ def test_loopback_vocab_parallel(pp, m, n, rc):
     simulator.cpp:414-522): LM head and cross entropy split over all stages;
     the collectives run as gathers/broadcasts over the loopback links."""
     _need_gpu()
-    ok, worst, _ = _run(pp, m, n, "off", rc, vocab=1024, vocab_parallel=True)
+    ok, worst = _run(pp, m, n, "off", rc, vocab_parallel=True)
     assert ok, worst
