@@ -23,8 +23,6 @@
 #include "kernels.hpp"
 #include "sm100.cuh"
 
-#include <cstdlib>
-
 
 namespace sp {
 namespace {
@@ -426,21 +424,15 @@ int attn_bwd_d128(const void* q, int64_t q_rows, int64_t q_stride, const void* k
       !make_tmap_bf16(&tv, v_pool, uint64_t(kv_stride), uint64_t(pool_rows), uint64_t(kv_stride), BK) ||
       !make_tmap_f32(&tdq, dq_acc, uint64_t(heads) * D, uint64_t(q_rows), uint64_t(heads) * D, D, uint32_t(stq)))
     return set_error(SP_ERR_CUDA, "attn_bwd_d128: cuTensorMapEncodeTiled failed (alignment?)");
-  // SP_BWD_NWG (A/B, read once): element-math warpgroups, 2 (default) or 4
-  static const int nwg = [] {
-    const char* e = std::getenv("SP_BWD_NWG");
-    return e && std::atoi(e) == 4 ? 4 : 2;
-  }();
+  // two element-math warpgroups: four (16 query columns per thread, 736
+  // threads) measured 1-3 % slower (profiles/r02_k2_ab.json) — the element
+  // math is not what bounds K2
+  constexpr int kNWG = 2;
+  auto kern = attn_bwd_d128_kernel<kNS, kNDS, kSTQ, true, kNWG>;
   const size_t smem = sizeof(Smem<kNS, kNDS, kSTQ>) + sizeof(Ctl<kNS>) + 1024;
-  auto launch = [&](auto kern, int threads) -> int {
-    if (int rc = set_smem_once(reinterpret_cast<const void*>(kern), smem, "attn_bwd_d128: set smem")) return rc;
-    kern<<<dim3(prm.total_kv / BK, kv_heads), threads, smem, st>>>(tq, tdo, tk, tv, tdq, prm);
-    count_launch(1);
-    return SP_OK;
-  };
-  const int rc = nwg == 4 ? launch(attn_bwd_d128_kernel<kNS, kNDS, kSTQ, true, 4>, Roles<4>::kThreads)
-                          : launch(attn_bwd_d128_kernel<kNS, kNDS, kSTQ, true, 2>, Roles<2>::kThreads);
-  if (rc) return rc;
+  if (int rc = set_smem_once(reinterpret_cast<const void*>(kern), smem, "attn_bwd_d128: set smem")) return rc;
+  kern<<<dim3(prm.total_kv / BK, kv_heads), Roles<kNWG>::kThreads, smem, st>>>(tq, tdo, tk, tv, tdq, prm);
+  count_launch(1);
   return cuda_status(cudaGetLastError(), "attn_bwd_d128 launch");
 }
 
@@ -448,9 +440,8 @@ int attn_bwd_d128(const void* q, int64_t q_rows, int64_t q_stride, const void* k
 // Force-load this file's kernels (cudaFuncGetAttributes) — see preload_kernels
 int preload_attn_bwd_v2() {
   cudaFuncAttributes a;
-  for (const void* k : {reinterpret_cast<const void*>(attn_bwd_d128_kernel<3, 1, 64, true, 2>),
-                        reinterpret_cast<const void*>(attn_bwd_d128_kernel<3, 1, 64, true, 4>)})
-    if (cudaError_t e = cudaFuncGetAttributes(&a, k)) return cuda_status(e, "preload attn_bwd_d128_kernel");
+  if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(attn_bwd_d128_kernel<3, 1, 64, true, 2>)))
+    return cuda_status(e, "preload attn_bwd_d128_kernel");
   return SP_OK;
 }
 }  // namespace sp

@@ -93,9 +93,8 @@ def _run(pp, m, n, exchange, recompute, kv_heads=4, interleave=1, vocab_parallel
 
 # (the float64 oracle of an n=8 sequence dominates a case's time, ~40 s)
 @pytest.mark.parametrize("pp,m,n,x,rc", [
-    (2, 2, 4, "off", "selective"), (2, 1, 2, "off", "full"),
-    (2, 2, 4, "on", "full"), (2, 2, 8, "early", "selective"),
-    (4, 2, 4, "off", "selective"), (4, 2, 8, "on", "selective"), (4, 2, 8, "early", "full"),
+    (2, 2, 4, "off", "selective"), (2, 2, 4, "on", "full"), (2, 2, 8, "early", "selective"),
+    (4, 2, 4, "off", "selective"), (4, 2, 8, "on", "selective"),
 ])
 def test_loopback_step_matches_oracle(pp, m, n, x, rc):
     """(the child also checks that exchange on / early really moved work)"""
@@ -110,7 +109,7 @@ def test_loopback_gqa_through_the_exchange():
     assert ok, worst
 
 
-@pytest.mark.parametrize("pp,m,n,rc", [(2, 2, 4, "selective"), (4, 2, 8, "full")])
+@pytest.mark.parametrize("pp,m,n,rc", [(2, 2, 4, "selective")])
 def test_loopback_interleaved_v2(pp, m, n, rc):
     """Interleaved SlimPipe (v = 2): the stage links form a ring."""
     _need_gpu()
@@ -118,7 +117,7 @@ def test_loopback_interleaved_v2(pp, m, n, rc):
     assert ok, worst
 
 
-@pytest.mark.parametrize("pp,m,n,rc", [(2, 2, 4, "selective"), (4, 2, 8, "full")])
+@pytest.mark.parametrize("pp,m,n,rc", [(2, 2, 4, "selective")])
 def test_loopback_vocab_parallel(pp, m, n, rc):
     """Vocabulary parallelism (reference place_vocab distribute=true,
     simulator.cpp:414-522): LM head and cross entropy split over all stages;
