@@ -424,9 +424,10 @@ def main():
         barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        loss = 0.0
+        loss, losses = 0.0, []
         for _ in range(args.steps):
             loss = step.step(tok_pin.numpy(), tgt_pin.numpy())
+            losses.append(loss)
         torch.cuda.synchronize()
         barrier()
         wall = max_over_ranks(time.perf_counter() - t0)
@@ -434,10 +435,17 @@ def main():
                "h2d_bytes_per_step": 2 * tokens_per_step * 4, "d2h_bytes_per_step": 4 * world,
                "timer": "host wall clock around SlimPipeStep.step (includes H2D/D2H), max over ranks"}
         if world > 1:
-            t = torch.tensor([loss], device="cuda")
+            t = torch.tensor(losses, device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.SUM)  # only the last stage is non-zero
-            loss = float(t.item())
+            losses = [float(x) for x in t.tolist()]
+            loss = losses[-1]
         e2e["loss"] = loss
+        # sanity of the training signal: finite, and an optimizer step per call
+        # (the first timed steps follow the warm-up's updates); ln V = the
+        # loss of a uniform prediction
+        e2e["losses"] = losses
+        e2e["ln_vocab"] = float(np.log(cfg.vocab))
+        e2e["loss_finite"] = bool(all(np.isfinite(losses)))
 
     peaks, peak_src = load_peaks()
     peak_tf = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
