@@ -73,6 +73,8 @@ def parse():
                     help="attention workload redistribution (reference ExchangeMode); no effect at PP=1")
     ap.add_argument("--vocab-parallel", action="store_true",
                     help="shard the LM head and cross entropy over all stages (PP>1; SURVEY §8f rank 1)")
+    ap.add_argument("--offload", action="store_true",
+                    help="activation offload: stage inputs + attention O/LSE in pinned host memory between F and BW")
     ap.add_argument("--interleave", type=int, default=1,
                     help="v stages per GPU (interleaved SlimPipe, even PP; SURVEY §8f rank 2)")
     ap.add_argument("--scenario", default=None,
@@ -105,13 +107,14 @@ def make_cfg(args, world):
                             ("slices", args.slices), ("microbatches", args.microbatches)) if v is not None}
     return base.__class__(**{**base.__dict__, **kw, "pp": world, "exchange": args.exchange,
                              "recompute": args.recompute, "vocab_parallel": bool(args.vocab_parallel and world > 1),
-                             "interleave": args.interleave if world > 1 else 1})
+                             "interleave": args.interleave if world > 1 else 1, "offload": bool(args.offload)})
 
 
 def workload_name(cfg, model="c2"):
     return (f"{MODEL_NAMES[model][0]} layer shapes x{cfg.layers} layers, {cfg.seq_len // 1024}K ctx, n={cfg.slices} slices, "
             f"m={cfg.microbatches}, PP={cfg.pp}, exchange={cfg.exchange}, recompute={cfg.recompute}"
-            + (", vocab-parallel" if cfg.vocab_parallel else "") + (f", v={cfg.interleave}" if cfg.interleave > 1 else ""))
+            + (", vocab-parallel" if cfg.vocab_parallel else "") + (f", v={cfg.interleave}" if cfg.interleave > 1 else "")
+            + (", activation offload" if cfg.offload else ""))
 
 
 # ----------------------------------------------------------------- clocks
@@ -494,6 +497,7 @@ def main():
                                             if calib else None),
             "peak_act_gb_per_gpu": arena_gb, "dkv_accum_gb_per_gpu": dkv_gb, "ledger_pred_gb_per_gpu": ledger_gb,
             "arena_slots": mem["slots"], "arena_high_water": mem["slots_high_water"],
+            "offload_host_gb_per_gpu": max_over_ranks(mem["offload_host_bytes"] / 1e9),
             # logits workspace of the stage(s) holding the LM head: [Ls, V] fp32 logits + dlogits
             # (last stage), or the [Ls, V/p] shard (fp32 logits + bf16 dlogits) on every stage
             # under vocabulary parallelism (reference logits_bytes, workload.cpp:154-160)

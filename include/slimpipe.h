@@ -211,6 +211,12 @@ typedef struct {
    * 0 or 1 = one stage per device.  v > 1 needs an even pp >= 2, exchange
    * off and vocab_parallel 0. */
   int32_t interleave;
+  /* 1: activation offload (reference offload_ratio, workload.cpp:130-132, at
+   * ratio "everything but K/V"): each slot's stage input and — selective
+   * recompute — per-layer attention O/LSE go to pinned host memory after the
+   * forward pass and come back at its backward; the device arena keeps only
+   * the K/V chunks later slices attend to.  0: everything stays in HBM. */
+  int32_t offload;
 } sp_model_config;
 
 #define SP_STEP_NO_OPTIMIZER 1
@@ -252,6 +258,8 @@ int sp_runtime_timeline(void* handle, double* out, int cap);
 int sp_runtime_attn_stats(void* handle, double* out6);
 int sp_runtime_memory(void* handle, int64_t* out7);
 int sp_runtime_recompute(void* handle);
+/* pinned host bytes holding offloaded activations (0 without offload) */
+long long sp_runtime_offload_bytes(void* handle);
 /* Diagnostics: position in this rank's pass order of the first pass not yet
  * finished on the compute stream (-1: all done); out4 = kind, microbatch,
  * slice, stage of that pass.  Non-blocking. */

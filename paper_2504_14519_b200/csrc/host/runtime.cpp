@@ -138,6 +138,18 @@ class Runtime {
   std::vector<float*> lse_pool;     // [slots][heads][Ls] per layer
   std::vector<int> free_slots;
   std::map<std::pair<int, int>, int> slot_of;
+  // activation offload (cfg.offload): a slot's stage input and per-layer O/LSE
+  // live in pinned host memory between its F and BW; one device staging set
+  // (x_stage, o_stage/l_stage per layer) serves the pass that runs
+  bool offload = false;
+  bf16raw *hx = nullptr, *ho = nullptr, *x_stage = nullptr;
+  float* hl = nullptr;
+  std::vector<bf16raw*> o_stage;
+  std::vector<float*> l_stage;
+  cudaStream_t s_off = nullptr;
+  cudaEvent_t ev_x_off = nullptr, ev_x_in = nullptr;
+  std::vector<cudaEvent_t> ev_o_off, ev_o_in;
+  size_t offload_bytes = 0;
   int slots_in_use = 0, slots_high_water = 0;
   // fp32 dK/dV chunk accumulators (one microbatch, indexed by slice)
   std::vector<float*> dk_acc, dv_acc;
@@ -232,8 +244,13 @@ class Runtime {
     for (cudaEvent_t e : tpool) cudaEventDestroy(e);
     if (xev) cudaEventDestroy(xev);
     if (ev_staged) cudaEventDestroy(ev_staged);
-    for (void* hp : {static_cast<void*>(h_tok), static_cast<void*>(h_tgt), static_cast<void*>(h_loss)})
+    for (void* hp : {static_cast<void*>(h_tok), static_cast<void*>(h_tgt), static_cast<void*>(h_loss),
+                     static_cast<void*>(hx), static_cast<void*>(ho), static_cast<void*>(hl)})
       if (hp) cudaFreeHost(hp);
+    for (cudaEvent_t e : {ev_x_off, ev_x_in})
+      if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : ev_o_off) cudaEventDestroy(e);
+    for (cudaEvent_t e : ev_o_in) cudaEventDestroy(e);
   }
 
   // Communicators are torn down in one global order, like warm_links sets
@@ -319,6 +336,8 @@ class Runtime {
     Ls = c.seq_len / c.slices;
     if (c.recompute < 0 || c.recompute > 2) return set_error(SP_ERR_INVALID, "recompute must be 0, 1 or 2");
     stash = c.recompute != 1;  // 2 (auto) is settled in alloc_arena once the parameters are resident
+    if (c.offload < 0 || c.offload > 1) return set_error(SP_ERR_INVALID, "offload must be 0 or 1");
+    offload = c.offload == 1;
     h = c.hidden;
     H = c.ffn_hidden;
     qd = int64_t(c.heads) * c.head_dim;
@@ -912,7 +931,8 @@ class Runtime {
 
   int alloc_arena() {
     const int64_t rows = int64_t(slots) * Ls;
-    SP_TRY(alloc(&x_pool, rows * h));
+    if (offload) SP_TRY(alloc(&x_stage, Ls * h));
+    else SP_TRY(alloc(&x_pool, rows * h));
     k_pool.assign(Lps, nullptr);
     v_pool.assign(Lps, nullptr);
     dk_acc.assign(size_t(v) * Lps, nullptr);  // per local chunk and layer
@@ -931,11 +951,19 @@ class Runtime {
     if (cfg.recompute == 2) {  // auto: stash O/LSE only if it fits beside everything allocated so far
       size_t free_b = 0, total_b = 0;
       SP_CUDA(cudaMemGetInfo(&free_b, &total_b));
-      const double stash_b = double(Lps) * rows * (qd * 2 + double(cfg.heads) * 4);
+      // (offloaded: the device keeps one pass's staging, the slots live on the host)
+      const double stash_b = double(Lps) * (offload ? Ls : rows) * (qd * 2 + double(cfg.heads) * 4);
       const double margin = 2.0 * double(1 << 30);  // cuBLASLt workspaces, NCCL buffers, allocator slack
       stash = stash_b + margin < double(free_b);
     }
-    if (stash) {
+    if (stash && offload) {
+      o_stage.assign(Lps, nullptr);
+      l_stage.assign(Lps, nullptr);
+      for (int l = 0; l < Lps; ++l) {
+        SP_TRY(alloc(&o_stage[l], Ls * qd));
+        SP_TRY(alloc(&l_stage[l], int64_t(cfg.heads) * Ls));
+      }
+    } else if (stash) {
       o_pool.assign(Lps, nullptr);
       lse_pool.assign(Lps, nullptr);
       const size_t n_before = allocations.size();
@@ -957,10 +985,39 @@ class Runtime {
         stash = false;
       }
     }
+    if (offload) {  // the host side of the slots, and the copy stream / events
+      auto host = [&](void** p, size_t bytes) -> int {
+        SP_CUDA(cudaHostAlloc(p, std::max<size_t>(bytes, 16), cudaHostAllocDefault));
+        offload_bytes += bytes;
+        return SP_OK;
+      };
+      SP_TRY(host(reinterpret_cast<void**>(&hx), size_t(rows) * size_t(h) * 2));
+      if (stash) {
+        SP_TRY(host(reinterpret_cast<void**>(&ho), size_t(slots) * Lps * size_t(Ls) * size_t(qd) * 2));
+        SP_TRY(host(reinterpret_cast<void**>(&hl), size_t(slots) * Lps * size_t(cfg.heads) * size_t(Ls) * 4));
+      }
+      SP_CUDA(cudaStreamCreateWithFlags(&s_off, cudaStreamNonBlocking));
+      for (cudaEvent_t* e : {&ev_x_off, &ev_x_in}) {
+        SP_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+        SP_CUDA(cudaEventRecord(*e, s_off));
+      }
+      ev_o_off.assign(Lps, nullptr);
+      ev_o_in.assign(Lps, nullptr);
+      for (int l = 0; l < Lps; ++l)
+        for (cudaEvent_t* e : {&ev_o_off[l], &ev_o_in[l]}) {
+          SP_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+          SP_CUDA(cudaEventRecord(*e, s_off));
+        }
+    }
     free_slots.clear();
     for (int s = slots - 1; s >= 0; --s) free_slots.push_back(s);  // pop_back -> lowest first
     return SP_OK;
   }
+
+  // offload helpers: a slot's host copies
+  bf16raw* host_x(int slot) { return hx + int64_t(slot) * Ls * h; }
+  bf16raw* host_o(int slot, int l) { return ho + (int64_t(slot) * Lps + l) * Ls * qd; }
+  float* host_l(int slot, int l) { return hl + (int64_t(slot) * Lps + l) * cfg.heads * Ls; }
 
   int alloc_workspace() {
     ws.resize(Lps);
@@ -1096,6 +1153,11 @@ class Runtime {
   // attention output of layer l for slice (k, i): the slot's stash or the workspace
   void bind_attn_out(int l, int slot) {
     LayerWs& x = ws[l];
+    if (stash && offload) {
+      x.o = o_stage[l];
+      x.lse = l_stage[l];
+      return;
+    }
     x.o = stash ? o_pool[l] + int64_t(slot) * Ls * qd : x.o_ws;
     x.lse = stash ? lse_pool[l] + int64_t(slot) * cfg.heads * Ls : x.lse_ws;
   }
@@ -1110,7 +1172,19 @@ class Runtime {
     SP_TRY(gemm(false, true, Ls, qkv_w, h, x.xn, h, W(P.wqkv), h, qkv, qkv_w, false, 1.f, 0.f, comp));
     SP_TRY(rope_qkv_fwd(qkv, Ls, cfg.heads, cfg.kv_heads, cfg.head_dim, pos0, rope_cos, rope_sin, x.q, qd,
                         k_pool[l] + int64_t(slot) * Ls * kvd, v_pool[l] + int64_t(slot) * Ls * kvd, kvd, comp));
-    if (!(recompute && stash)) SP_TRY(attention_forward(l, k, i, x, px));
+    const bool staged = stash && offload;
+    if (!(recompute && stash)) {
+      if (staged) SP_CUDA(cudaStreamWaitEvent(comp, ev_o_off[l], 0));  // last pass's copy-out of o_stage[l]
+      SP_TRY(attention_forward(l, k, i, x, px));
+      if (staged) {  // O/LSE of this slot-layer to the host, overlapping the rest of the pass
+        SP_TRY(hand_off(comp, s_off));
+        SP_CUDA(cudaMemcpyAsync(host_o(slot, l), x.o, Ls * qd * 2, cudaMemcpyDeviceToHost, s_off));
+        SP_CUDA(cudaMemcpyAsync(host_l(slot, l), x.lse, int64_t(cfg.heads) * Ls * 4, cudaMemcpyDeviceToHost, s_off));
+        SP_CUDA(cudaEventRecord(ev_o_off[l], s_off));
+      }
+    } else if (staged) {
+      SP_CUDA(cudaStreamWaitEvent(comp, ev_o_in[l], 0));  // the backward's copy-in of this layer's stash
+    }
     SP_TRY(gemm(false, true, Ls, h, qd, x.o, qd, W(P.wo), qd, x.x_mid, h, false, 1.f, 1.f, comp, x.x_in));
     SP_TRY(rmsnorm_fwd(x.x_mid, W(P.mlp_norm), x.xn2, x.rstd2, Ls, int(h), cfg.norm_eps, comp));
     SP_TRY(gemm(false, true, Ls, 2 * H, h, x.xn2, h, W(P.wgu), h, x.gu, 2 * H, false, 1.f, 0.f, comp));
@@ -1133,8 +1207,9 @@ class Runtime {
     free_slots.pop_back();
     slot_of[sk(k, i)] = slot;
     slots_high_water = std::max(slots_high_water, ++slots_in_use);
-    bf16raw* xs = x_pool + int64_t(slot) * Ls * h;
+    bf16raw* xs = offload ? x_stage : x_pool + int64_t(slot) * Ls * h;
     const int64_t tok0 = int64_t(k - 1) * cfg.seq_len + int64_t(i - 1) * Ls;
+    if (offload) SP_CUDA(cudaStreamWaitEvent(comp, ev_x_off, 0));  // the last copy-out of x_stage is done
     if (stage == 1) {
       SP_CUDA(cudaEventRecord(t0, comp));
       SP_TRY(embed_fwd(tokens + tok0, W(emb), xs, Ls, int(h), comp));
@@ -1152,6 +1227,11 @@ class Runtime {
       SP_CUDA(cudaEventRecord(ev_ain_free[b], comp));
     }
     SP_CUDA(cudaMemcpyAsync(ws[0].x_in, xs, Ls * h * 2, cudaMemcpyDeviceToDevice, comp));
+    if (offload) {  // the stage input to the slot's host copy
+      SP_TRY(hand_off(comp, s_off));
+      SP_CUDA(cudaMemcpyAsync(host_x(slot), xs, Ls * h * 2, cudaMemcpyDeviceToHost, s_off));
+      SP_CUDA(cudaEventRecord(ev_x_off, s_off));
+    }
     if (stage < nst) {
       const int b = out_idx;
       out_idx ^= 1;
@@ -1315,8 +1395,20 @@ class Runtime {
     const PassX* px = pass_x(pid);
     if (px && !px->in.empty()) SP_TRY(post_remote(*px));
     const int slot = slot_of.at(sk(k, i));
-    bf16raw* xs = x_pool + int64_t(slot) * Ls * h;
+    bf16raw* xs = offload ? x_stage : x_pool + int64_t(slot) * Ls * h;
     const int64_t tok0 = int64_t(k - 1) * cfg.seq_len + int64_t(i - 1) * Ls;
+    if (offload) {  // bring the slot's stash back (after every earlier use of the staging)
+      SP_TRY(hand_off(comp, s_off));
+      SP_CUDA(cudaMemcpyAsync(x_stage, host_x(slot), Ls * h * 2, cudaMemcpyHostToDevice, s_off));
+      SP_CUDA(cudaEventRecord(ev_x_in, s_off));
+      if (stash)
+        for (int l = 0; l < Lps; ++l) {
+          SP_CUDA(cudaMemcpyAsync(o_stage[l], host_o(slot, l), Ls * qd * 2, cudaMemcpyHostToDevice, s_off));
+          SP_CUDA(cudaMemcpyAsync(l_stage[l], host_l(slot, l), int64_t(cfg.heads) * Ls * 4, cudaMemcpyHostToDevice,
+                                  s_off));
+          SP_CUDA(cudaEventRecord(ev_o_in[l], s_off));
+        }
+    }
     // gradient input
     bf16raw* dx = nullptr;
     int gb = -1;
@@ -1334,6 +1426,7 @@ class Runtime {
       dx = gout_buf[gout_idx];  // last stage: dX is produced here, sent from here
     }
     // recompute (Full checkpointing)
+    if (offload) SP_CUDA(cudaStreamWaitEvent(comp, ev_x_in, 0));
     SP_CUDA(cudaMemcpyAsync(ws[0].x_in, xs, Ls * h * 2, cudaMemcpyDeviceToDevice, comp));
     bf16raw* top = stage < nst ? tmp_h : x_final;
     if (stage == nst) {
@@ -1434,6 +1527,7 @@ class Runtime {
     enq_pos = -1;
     // drain comm streams into the compute stream so step_end covers them
     for (cudaStream_t st : {s_act_in, s_act_out, s_grad_in, s_grad_out}) SP_TRY(hand_off(st, comp));
+    if (s_off) SP_TRY(hand_off(s_off, comp));
     for (int c = 0; c < 2; ++c)
       if (cx[c]) {
         SP_TRY(link(cx[c], comp));
@@ -1594,12 +1688,20 @@ int sp_runtime_exchange_stats(void* handle, int64_t* out3) {
 // {slots, slots_high_water, slot_bytes, ledger_peak_units, bytes_allocated, n_params, layers_per_stage}
 int sp_runtime_recompute(void* handle) { return static_cast<Runtime*>(handle)->stash ? 0 : 1; }
 
+long long sp_runtime_offload_bytes(void* handle) {
+  return static_cast<long long>(static_cast<Runtime*>(handle)->offload_bytes);
+}
+
 int sp_runtime_memory(void* handle, int64_t* out7) {
   Runtime* rt = static_cast<Runtime*>(handle);
   out7[0] = rt->slots;
   out7[1] = rt->slots_high_water;
-  out7[2] = rt->Ls * rt->h * 2 + int64_t(rt->Lps) * 2 * rt->Ls * rt->kvd * 2 +
-            (rt->stash ? int64_t(rt->Lps) * rt->Ls * (rt->qd * 2 + int64_t(rt->cfg.heads) * 4) : 0);
+  // device bytes per slot: K/V per layer, plus the stage input and O/LSE
+  // stash unless they are offloaded to the host
+  out7[2] = int64_t(rt->Lps) * 2 * rt->Ls * rt->kvd * 2 +
+            (rt->offload ? 0
+                         : rt->Ls * rt->h * 2 +
+                               (rt->stash ? int64_t(rt->Lps) * rt->Ls * (rt->qd * 2 + int64_t(rt->cfg.heads) * 4) : 0));
   out7[3] = rt->ledger.per_device[rt->rank].peak_activation_units;
   out7[4] = int64_t(rt->bytes_allocated);
   out7[5] = rt->n_params;

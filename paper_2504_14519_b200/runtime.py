@@ -25,7 +25,7 @@ class _Cfg(C.Structure):
                                          "microbatches", "slices", "pp", "rank", "exchange_mode")] + [
         ("seq_len", C.c_int64), ("rope_theta", C.c_float), ("norm_eps", C.c_float), ("lr", C.c_float),
         ("seed", C.c_uint64), ("recompute", C.c_int32), ("vocab_parallel", C.c_int32),
-        ("interleave", C.c_int32)]
+        ("interleave", C.c_int32), ("offload", C.c_int32)]
 
 
 RECOMPUTE = {"selective": 0, "full": 1, "auto": 2}
@@ -47,6 +47,7 @@ class StepConfig:
     recompute: str = "auto"  # "selective": stash attention O/LSE, "full": K1 again in the backward, "auto": selective if it fits
     vocab_parallel: bool = False  # LM head + cross entropy split by vocabulary across the pp stages
     interleave: int = 1  # v stages per device (interleaved SlimPipe; even pp, exchange off)
+    offload: bool = False  # stage inputs + attention O/LSE to pinned host memory between F and BW
     rope_theta: float = 10000.0
     norm_eps: float = 1e-5
     lr: float = 1e-4
@@ -86,7 +87,7 @@ class StepConfig:
         """A reference scenario file (scenario.cpp schema) as the executed step:
         the same file drives plan.simulate / plan.gantt_text and the GPU run.
         Only what the executor runs is accepted: scheme slimpipe, tp = cp = dp
-        = ep = 1, checkpointing selective or full, no offload."""
+        = ep = 1, checkpointing selective or full."""
         from . import plan as P
         sc = P.scenario(text)  # strict: unknown fields and bad values raise ValueError
         md, pa, rn = sc["model"], sc["parallelism"], sc["run"]
@@ -97,13 +98,14 @@ class StepConfig:
                 raise ValueError(f"scenario: {k} = {pa[k]} is not on the executed path (pipeline only)")
         if rn["checkpointing"] not in ("selective", "full"):
             raise ValueError(f"scenario: checkpointing {rn['checkpointing']} (the executor recomputes: selective|full)")
-        if rn["offload_ratio"] != 0:
-            raise ValueError("scenario: activation offload is not executed")
+        # offload_ratio > 0 runs the executor's activation offload, which moves
+        # every activation but the K/V chunks (stage inputs, attention O/LSE)
+        # to the host — the ratio itself is not tunable
         kw = dict(layers=md["layers"], hidden=md["hidden"], ffn_hidden=md["ffn"], heads=md["heads"],
                   kv_heads=md["query_groups"], vocab=md["vocab"], seq_len=rn["seq_len"], slices=rn["slices"],
                   microbatches=rn["microbatches"], pp=pa["pp"], interleave=pa["stages_per_device"],
                   exchange=sc["exchange"], recompute=rn["checkpointing"], vocab_parallel=bool(rn["vocab_parallel"]),
-                  seed=sc["seed"])
+                  offload=rn["offload_ratio"] > 0, seed=sc["seed"])
         kw.update(overrides)
         return StepConfig(**kw)
 
@@ -111,7 +113,7 @@ class StepConfig:
         return _Cfg(self.layers, self.hidden, self.ffn_hidden, self.heads, self.kv_heads, self.head_dim, self.vocab,
                     self.microbatches, self.slices, self.pp, rank, N.MODES[self.exchange], self.seq_len,
                     self.rope_theta, self.norm_eps, self.lr, self.seed, RECOMPUTE[self.recompute],
-                    int(self.vocab_parallel), int(self.interleave))
+                    int(self.vocab_parallel), int(self.interleave), int(self.offload))
 
     # ---- accounting ----
     def linear_params_per_layer(self) -> int:
@@ -151,6 +153,8 @@ def _lib():
     lib.sp_runtime_attn_stats.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
     lib.sp_runtime_memory.argtypes = [C.c_void_p, C.POINTER(C.c_int64)]
     lib.sp_runtime_recompute.argtypes = [C.c_void_p]
+    lib.sp_runtime_offload_bytes.argtypes = [C.c_void_p]
+    lib.sp_runtime_offload_bytes.restype = C.c_longlong
     lib.sp_runtime_progress.argtypes = [C.c_void_p, C.POINTER(C.c_int32)]
     lib.sp_runtime_param.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int64, C.c_int]
     return lib
@@ -347,6 +351,7 @@ class SlimPipeStep:
                 "layers_per_stage"]
         out = dict(zip(keys, list(b)))
         out["recompute"] = "full" if _lib().sp_runtime_recompute(self._h) else "selective"
+        out["offload_host_bytes"] = int(_lib().sp_runtime_offload_bytes(self._h))
         return out
 
     def exchange_stats(self) -> dict:

@@ -57,7 +57,10 @@ def _pull(step, cfg):
                                           # GQA 4:2 on the d=64 kernels, and d=128 (production K1/K2) with GQA
                                           (2, 4, "selective", {"kv_heads": 2}),
                                           (2, 4, "selective", {"hidden": 512, "kv_heads": 2, "ffn_hidden": 1024}),
-                                          (1, 4, "full", {"hidden": 512, "kv_heads": 4, "ffn_hidden": 1024})])
+                                          (1, 4, "full", {"hidden": 512, "kv_heads": 4, "ffn_hidden": 1024}),
+                                          # activation offload (stage input + O/LSE via pinned host memory)
+                                          (2, 4, "selective", {"offload": True}),
+                                          (2, 4, "full", {"offload": True, "hidden": 512, "ffn_hidden": 1024})])
 def test_c1_step_matches_oracle(m, n, rc, shape):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
