@@ -195,3 +195,12 @@ def test_one_scenario_file_drives_simulate_and_the_step():
     direct = P.simulate(cfg.pp, cfg.interleave, cfg.microbatches, cfg.slices, cfg.exchange, (1.0, 0.0, 2.0, 1.0),
                         (0.0, 0.0), cfg.seq_len)
     assert sim == direct and len(sim["busy"]) == cfg.pp
+
+
+def test_scenario_offload_ratio_runs_the_executor_offload():
+    """offload_ratio > 0 (reference workload.cpp:130-132) selects the
+    executor's activation offload (everything but K/V to the host)."""
+    text = SCENARIOS[1].replace('"checkpointing":"selective"}', '"checkpointing":"selective","offload_ratio":0.5}')
+    cfg = StepConfig.from_scenario(text)
+    assert cfg.offload and cfg.to_c(0).offload == 1
+    assert not StepConfig.from_scenario(SCENARIOS[1]).offload
