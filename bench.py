@@ -75,6 +75,7 @@ def parse():
                     help="shard the LM head and cross entropy over all stages (PP>1; SURVEY §8f rank 1)")
     ap.add_argument("--offload", action="store_true",
                     help="activation offload: stage inputs + attention O/LSE in pinned host memory between F and BW")
+    ap.add_argument("--dkv-bf16", action="store_true", help="dK/dV chunk accumulators stored in bf16 (half their HBM)")
     ap.add_argument("--interleave", type=int, default=1,
                     help="v stages per GPU (interleaved SlimPipe, even PP; SURVEY §8f rank 2)")
     ap.add_argument("--scenario", default=None,
@@ -107,14 +108,15 @@ def make_cfg(args, world):
                             ("slices", args.slices), ("microbatches", args.microbatches)) if v is not None}
     return base.__class__(**{**base.__dict__, **kw, "pp": world, "exchange": args.exchange,
                              "recompute": args.recompute, "vocab_parallel": bool(args.vocab_parallel and world > 1),
-                             "interleave": args.interleave if world > 1 else 1, "offload": bool(args.offload)})
+                             "interleave": args.interleave if world > 1 else 1, "offload": bool(args.offload),
+                             "dkv_bf16": bool(args.dkv_bf16)})
 
 
 def workload_name(cfg, model="c2"):
     return (f"{MODEL_NAMES[model][0]} layer shapes x{cfg.layers} layers, {cfg.seq_len // 1024}K ctx, n={cfg.slices} slices, "
             f"m={cfg.microbatches}, PP={cfg.pp}, exchange={cfg.exchange}, recompute={cfg.recompute}"
             + (", vocab-parallel" if cfg.vocab_parallel else "") + (f", v={cfg.interleave}" if cfg.interleave > 1 else "")
-            + (", activation offload" if cfg.offload else ""))
+            + (", activation offload" if cfg.offload else "") + (", bf16 dK/dV accumulators" if cfg.dkv_bf16 else ""))
 
 
 # ----------------------------------------------------------------- clocks
@@ -464,7 +466,7 @@ def main():
         traffic = json.loads(prof.read_text()).get(f"attn_{kind}", {}).get("dram_bytes_per_launch")
     # activation memory: arena slots x slot bytes (x stash + per-layer K/V), max over ranks
     arena_gb = max_over_ranks(mem["slots"] * mem["slot_bytes"] / 1e9)
-    dkv_gb = cfg.layers // world * cfg.seq_len * 2 * cfg.kv_heads * cfg.head_dim * 4 / 1e9
+    dkv_gb = cfg.layers // world * cfg.seq_len * 2 * cfg.kv_heads * cfg.head_dim * (2 if cfg.dkv_bf16 else 4) / 1e9
     mm = PL.activation_bytes(PL.ModelShape(cfg.layers, cfg.hidden, cfg.ffn_hidden, cfg.heads, cfg.kv_heads,
                                            cfg.vocab), 1, 1, world, 1, cfg.seq_len, cfg.microbatches, cfg.slices)
     ledger_gb = float(mm["slice_stage"]) * (cfg.slices + 2 * (world - 1)) / 1e9 if cfg.microbatches * cfg.slices >= \

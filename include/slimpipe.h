@@ -217,6 +217,10 @@ typedef struct {
    * forward pass and come back at its backward; the device arena keeps only
    * the K/V chunks later slices attend to.  0: everything stays in HBM. */
   int32_t offload;
+  /* 1: the fp32 dK/dV chunk accumulators are stored in bf16 (sums kept in
+   * fp32 inside each backward kernel, rounded once per slice contribution):
+   * half their HBM; 0: fp32 storage. */
+  int32_t dkv_bf16;
 } sp_model_config;
 
 #define SP_STEP_NO_OPTIMIZER 1

@@ -45,8 +45,8 @@ struct BwdParams {
   const float* delta;  // [heads][q_rows]
   float* dq;           // [q_rows][heads*D]
   int64_t dq_stride;
-  float* dk;           // [acc_rows][kv_heads*D]
-  float* dv;
+  void* dk;            // [acc_rows][kv_heads*D], fp32 or bf16 (AccT)
+  void* dv;
   int64_t acc_stride;
   int chunk_row[SP_MAX_CHUNKS];
   int acc_row[SP_MAX_CHUNKS];
@@ -94,7 +94,7 @@ __device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float 
                : "memory");
 }
 
-template <int D>
+template <int D, typename AccT>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
                     const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
@@ -309,22 +309,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&sm.acc_done, 0);
       tc_fence_after();
       const int64_t arow = prm.acc_row[chunk] + key0 % prm.chunk_len + r;
-      float* dkp = prm.dk + arow * prm.acc_stride + kvh * D;
-      float* dvp = prm.dv + arow * prm.acc_stride + kvh * D;
+      AccT* dkp = static_cast<AccT*>(prm.dk) + arow * prm.acc_stride + kvh * D;
+      AccT* dvp = static_cast<AccT*>(prm.dv) + arow * prm.acc_stride + kvh * D;
 #pragma unroll
       for (int ch = 0; ch < D / 32; ++ch) {
         float a[32], b[32];
         tmem_ld32(tmem + lane_off + Cfg::kDK + ch * 32, a);
         tmem_ld32(tmem + lane_off + Cfg::kDV + ch * 32, b);
         tmem_wait_ld();
-        float4* gk = reinterpret_cast<float4*>(dkp + ch * 32);
-        float4* gv = reinterpret_cast<float4*>(dvp + ch * 32);
-#pragma unroll
-        for (int x = 0; x < 8; ++x) {
-          float4 ok = gk[x], ov = gv[x];
-          gk[x] = make_float4(ok.x + a[4 * x], ok.y + a[4 * x + 1], ok.z + a[4 * x + 2], ok.w + a[4 * x + 3]);
-          gv[x] = make_float4(ov.x + b[4 * x], ov.y + b[4 * x + 1], ov.z + b[4 * x + 2], ov.w + b[4 * x + 3]);
-        }
+        acc_add32(dkp + ch * 32, a);
+        acc_add32(dvp + ch * 32, b);
       }
     }
     tc_fence_before();
@@ -362,10 +356,10 @@ __global__ void __launch_bounds__(256) attn_bwd_prep(const __nv_bfloat16* __rest
   }
 }
 
-template <int D>
+template <int D, typename AccT>
 int launch_bwd(const CUtensorMap& tq, const CUtensorMap& tdo, const CUtensorMap& tk, const CUtensorMap& tv,
                const BwdParams& prm, int k_tiles, int kv_heads, cudaStream_t st) {
-  auto kern = attn_bwd_kernel<D>;
+  auto kern = attn_bwd_kernel<D, AccT>;
   const size_t smem = sizeof(BwdSmem<D>) + 1024;
   if (int rc = set_smem_once(reinterpret_cast<const void*>(kern), smem, "attn_bwd: set smem")) return rc;
   kern<<<dim3(k_tiles, kv_heads), kThreads, smem, st>>>(tq, tdo, tk, tv, prm);
@@ -400,7 +394,8 @@ namespace sp {
 // Force-load this file's kernels (cudaFuncGetAttributes) — see preload_kernels
 int preload_attn_bwd() {
   cudaFuncAttributes a;
-  if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(sp::attn_bwd_kernel<64>))) return cuda_status(e, "preload sp::attn_bwd_kernel<64>");
+  if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(sp::attn_bwd_kernel<64, float>))) return cuda_status(e, "preload sp::attn_bwd_kernel<64>");
+  if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(sp::attn_bwd_kernel<64, __nv_bfloat16>))) return cuda_status(e, "preload sp::attn_bwd_kernel<64, bf16>");
   if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(sp::attn_bwd_prep<64>))) return cuda_status(e, "preload sp::attn_bwd_prep<64>");
   if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(sp::attn_bwd_prep<128>))) return cuda_status(e, "preload sp::attn_bwd_prep<128>");
   return SP_OK;
@@ -427,16 +422,18 @@ extern "C" int sp_attn_bwd_prep(const void* o, int64_t o_stride, const void* dou
   return cuda_status(cudaGetLastError(), "attn_bwd_prep launch");
 }
 
-extern "C" int sp_attn_bwd_core(const void* q, int64_t q_rows, int64_t q_stride, const void* k_pool,
-                                const void* v_pool, int64_t pool_rows, int64_t kv_stride, const int32_t* chunk_row,
-                                int n_chunks, int chunk_len, int heads, int kv_heads, int head_dim, int causal,
-                                const void* dout, int64_t do_stride, const float* stats, float* dq_acc, float* dk_acc,
-                                float* dv_acc, int64_t acc_rows, const int32_t* acc_row, sp_stream_t stream) {
-  using namespace sp;
+namespace sp {
+// sp_attn_bwd_core with the chunk accumulators' storage type chosen: fp32, or
+// bf16 (acc_bf16; the runtime's dkv_bf16 option)
+int attn_bwd_core(const void* q, int64_t q_rows, int64_t q_stride, const void* k_pool, const void* v_pool,
+                  int64_t pool_rows, int64_t kv_stride, const int32_t* chunk_row, int n_chunks, int chunk_len,
+                  int heads, int kv_heads, int head_dim, int causal, const void* dout, int64_t do_stride,
+                  const float* stats, float* dq_acc, void* dk_acc, void* dv_acc, int64_t acc_rows,
+                  const int32_t* acc_row, bool acc_bf16, cudaStream_t stream) {
   if (int rc = bwd_check(q_rows, n_chunks, chunk_len, heads, kv_heads, head_dim, causal, q_stride, kv_stride,
                          do_stride))
     return rc;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaStream_t st = stream;
   const float* lse2 = stats;
   const float* delta = stats + int64_t(heads) * q_rows;
   const int64_t total_kv = int64_t(n_chunks) * chunk_len;
@@ -447,7 +444,7 @@ extern "C" int sp_attn_bwd_core(const void* q, int64_t q_rows, int64_t q_stride,
   if (head_dim == 128)  // attn_bwd_v2.cu
     return attn_bwd_d128(q, q_rows, q_stride, k_pool, v_pool, pool_rows, kv_stride, chunk_row, n_chunks, chunk_len,
                          heads, kv_heads, causal, dout, do_stride, lse2, delta, dq_acc, dk_acc, dv_acc, acc_rows,
-                         acc_row, st);
+                         acc_row, acc_bf16, st);
   BwdParams prm{};
   prm.q_rows = int(q_rows);
   prm.total_kv = int(total_kv);
@@ -476,7 +473,19 @@ extern "C" int sp_attn_bwd_core(const void* q, int64_t q_rows, int64_t q_stride,
       !make_tmap_bf16(&tv, v_pool, uint64_t(kv_stride), uint64_t(pool_rows), uint64_t(kv_stride), 128))
     return set_error(SP_ERR_CUDA, "sp_attn_bwd: cuTensorMapEncodeTiled failed (alignment?)");
   const int k_tiles = int(total_kv / 128);
-  return launch_bwd<64>(tq, tdo, tk, tv, prm, k_tiles, kv_heads, st);
+  return acc_bf16 ? launch_bwd<64, __nv_bfloat16>(tq, tdo, tk, tv, prm, k_tiles, kv_heads, st)
+                  : launch_bwd<64, float>(tq, tdo, tk, tv, prm, k_tiles, kv_heads, st);
+}
+}  // namespace sp
+
+extern "C" int sp_attn_bwd_core(const void* q, int64_t q_rows, int64_t q_stride, const void* k_pool,
+                                const void* v_pool, int64_t pool_rows, int64_t kv_stride, const int32_t* chunk_row,
+                                int n_chunks, int chunk_len, int heads, int kv_heads, int head_dim, int causal,
+                                const void* dout, int64_t do_stride, const float* stats, float* dq_acc, float* dk_acc,
+                                float* dv_acc, int64_t acc_rows, const int32_t* acc_row, sp_stream_t stream) {
+  return sp::attn_bwd_core(q, q_rows, q_stride, k_pool, v_pool, pool_rows, kv_stride, chunk_row, n_chunks, chunk_len,
+                           heads, kv_heads, head_dim, causal, dout, do_stride, stats, dq_acc, dk_acc, dv_acc, acc_rows,
+                           acc_row, false, static_cast<cudaStream_t>(stream));
 }
 
 extern "C" int sp_attn_bwd(const void* q, int64_t q_rows, int64_t q_stride, const void* k_pool, const void* v_pool,

@@ -45,8 +45,8 @@ struct Params {
   float scale, scale_log2;
   const float* lse2;
   const float* delta;
-  float* dk;
-  float* dv;
+  void* dk;  // chunk accumulators: fp32, or bf16 with AccT = __nv_bfloat16
+  void* dv;
   int64_t acc_stride;
   int chunk_row[SP_MAX_CHUNKS];
   int acc_row[SP_MAX_CHUNKS];
@@ -82,7 +82,7 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
                : "memory");
 }
 
-template <int NS, int NDS, int STQ, bool kPad, int NWG>
+template <int NS, int NDS, int STQ, bool kPad, int NWG, typename AccT>
 __global__ void __launch_bounds__(Roles<NWG>::kThreads, 1)
     attn_bwd_d128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
                          const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
@@ -315,19 +315,14 @@ __global__ void __launch_bounds__(Roles<NWG>::kThreads, 1)
       // WG halves: dK then dV; with 4 WGs each takes 64 of the 128 columns
       const bool is_k = wg < NWG / 2;
       const int c_base = NWG == 2 ? 0 : (wg % 2) * 64;
-      float* dst = (is_k ? prm.dk : prm.dv) + arow * prm.acc_stride + kvh * D + c_base;
+      AccT* dst = static_cast<AccT*>(is_k ? prm.dk : prm.dv) + arow * prm.acc_stride + kvh * D + c_base;
       const uint32_t col = (is_k ? kDK : kDV) + c_base;
 #pragma unroll
       for (int ch = 0; ch < D / 32 / (NWG / 2); ++ch) {
         float a[32];
         tmem_ld32(tmem + lane_off + col + ch * 32, a);
         tmem_wait_ld();
-        float4* g4 = reinterpret_cast<float4*>(dst + ch * 32);
-#pragma unroll
-        for (int x = 0; x < 8; ++x) {
-          const float4 o = g4[x];
-          g4[x] = make_float4(o.x + a[4 * x], o.y + a[4 * x + 1], o.z + a[4 * x + 2], o.w + a[4 * x + 3]);
-        }
+        acc_add32(dst + ch * 32, a);
       }
     }
     tc_fence_before();
@@ -391,8 +386,8 @@ __global__ void __launch_bounds__(Roles<NWG>::kThreads, 1)
 int attn_bwd_d128(const void* q, int64_t q_rows, int64_t q_stride, const void* k_pool, const void* v_pool,
                   int64_t pool_rows, int64_t kv_stride, const int32_t* chunk_row, int n_chunks, int chunk_len,
                   int heads, int kv_heads, int causal, const void* dout, int64_t do_stride, const float* lse2,
-                  const float* delta, float* dq_acc, float* dk_acc, float* dv_acc, int64_t acc_rows,
-                  const int32_t* acc_row, cudaStream_t st) {
+                  const float* delta, float* dq_acc, void* dk_acc, void* dv_acc, int64_t acc_rows,
+                  const int32_t* acc_row, bool acc_bf16, cudaStream_t st) {
   Params prm{};
   prm.q_rows = int(q_rows);
   prm.total_kv = n_chunks * chunk_len;
@@ -428,11 +423,16 @@ int attn_bwd_d128(const void* q, int64_t q_rows, int64_t q_stride, const void* k
   // threads) measured 1-3 % slower (profiles/r02_k2_ab.json) — the element
   // math is not what bounds K2
   constexpr int kNWG = 2;
-  auto kern = attn_bwd_d128_kernel<kNS, kNDS, kSTQ, true, kNWG>;
   const size_t smem = sizeof(Smem<kNS, kNDS, kSTQ>) + sizeof(Ctl<kNS>) + 1024;
-  if (int rc = set_smem_once(reinterpret_cast<const void*>(kern), smem, "attn_bwd_d128: set smem")) return rc;
-  kern<<<dim3(prm.total_kv / BK, kv_heads), Roles<kNWG>::kThreads, smem, st>>>(tq, tdo, tk, tv, tdq, prm);
-  count_launch(1);
+  auto launch = [&](auto kern) -> int {
+    if (int rc = set_smem_once(reinterpret_cast<const void*>(kern), smem, "attn_bwd_d128: set smem")) return rc;
+    kern<<<dim3(prm.total_kv / BK, kv_heads), Roles<kNWG>::kThreads, smem, st>>>(tq, tdo, tk, tv, tdq, prm);
+    count_launch(1);
+    return SP_OK;
+  };
+  const int rc = acc_bf16 ? launch(attn_bwd_d128_kernel<kNS, kNDS, kSTQ, true, kNWG, __nv_bfloat16>)
+                          : launch(attn_bwd_d128_kernel<kNS, kNDS, kSTQ, true, kNWG, float>);
+  if (rc) return rc;
   return cuda_status(cudaGetLastError(), "attn_bwd_d128 launch");
 }
 
@@ -440,8 +440,9 @@ int attn_bwd_d128(const void* q, int64_t q_rows, int64_t q_stride, const void* k
 // Force-load this file's kernels (cudaFuncGetAttributes) — see preload_kernels
 int preload_attn_bwd_v2() {
   cudaFuncAttributes a;
-  if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(attn_bwd_d128_kernel<3, 1, 64, true, 2>)))
-    return cuda_status(e, "preload attn_bwd_d128_kernel");
+  for (const void* k : {reinterpret_cast<const void*>(attn_bwd_d128_kernel<3, 1, 64, true, 2, float>),
+                        reinterpret_cast<const void*>(attn_bwd_d128_kernel<3, 1, 64, true, 2, __nv_bfloat16>)})
+    if (cudaError_t e = cudaFuncGetAttributes(&a, k)) return cuda_status(e, "preload attn_bwd_d128_kernel");
   return SP_OK;
 }
 }  // namespace sp

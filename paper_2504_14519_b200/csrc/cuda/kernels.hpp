@@ -27,8 +27,11 @@ int rope_table(float* cs, float* sn, int64_t positions, int d, double theta, cud
 int rope_qkv_fwd(const void* qkv, int64_t rows, int heads, int kv_heads, int d, int64_t pos0, const float* cs,
                  const float* sn, void* q_out, int64_t q_stride, void* k_out, void* v_out, int64_t kv_stride,
                  cudaStream_t st);
-int rope_qkv_bwd(const float* dq, float* dk, float* dv, int64_t kv_stride, int64_t rows, int heads, int kv_heads,
-                 int d, int64_t pos0, const float* cs, const float* sn, void* dqkv, int zero_kv, cudaStream_t st);
+// dk/dv: fp32, or bf16 when acc_bf16 (the dK/dV chunk accumulators' storage)
+int rope_qkv_bwd(const float* dq, void* dk, void* dv, int64_t kv_stride, int64_t rows, int heads, int kv_heads,
+                 int d, int64_t pos0, const float* cs, const float* sn, void* dqkv, int zero_kv, cudaStream_t st,
+                 bool acc_bf16 = false);
+int add_to_bf16(void* dst, const float* src, int64_t n, cudaStream_t st);  // bf16 dst += fp32 src
 int swiglu_fwd(const void* gu, void* act, int64_t rows, int H, cudaStream_t st);
 int swiglu_bwd(const void* dact, const void* gu, void* dgu, int64_t rows, int H, cudaStream_t st);
 int cross_entropy(const float* logits, const int32_t* tgt, int64_t rows, int V, float scale, void* dlogits,
@@ -79,8 +82,14 @@ int set_smem_once(const void* fn, size_t smem, const char* what);
 int attn_bwd_d128(const void* q, int64_t q_rows, int64_t q_stride, const void* k_pool, const void* v_pool,
                   int64_t pool_rows, int64_t kv_stride, const int32_t* chunk_row, int n_chunks, int chunk_len,
                   int heads, int kv_heads, int causal, const void* dout, int64_t do_stride, const float* lse2,
-                  const float* delta, float* dq_acc, float* dk_acc, float* dv_acc, int64_t acc_rows,
-                  const int32_t* acc_row, cudaStream_t st);
+                  const float* delta, float* dq_acc, void* dk_acc, void* dv_acc, int64_t acc_rows,
+                  const int32_t* acc_row, bool acc_bf16, cudaStream_t st);
+// sp_attn_bwd_core with fp32 (acc_bf16 = false) or bf16 dK/dV chunk accumulators
+int attn_bwd_core(const void* q, int64_t q_rows, int64_t q_stride, const void* k_pool, const void* v_pool,
+                  int64_t pool_rows, int64_t kv_stride, const int32_t* chunk_row, int n_chunks, int chunk_len,
+                  int heads, int kv_heads, int head_dim, int causal, const void* dout, int64_t do_stride,
+                  const float* stats, float* dq_acc, void* dk_acc, void* dv_acc, int64_t acc_rows,
+                  const int32_t* acc_row, bool acc_bf16, cudaStream_t stream);
 
 // gemm.cu — row-major GEMMs on cuBLASLt (bf16 inputs, fp32 accumulate).
 //   C[M,N] = alpha * op(A) op(B) + beta * C

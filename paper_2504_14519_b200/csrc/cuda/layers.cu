@@ -249,7 +249,20 @@ __global__ void rope_qkv_fwd_k(const bf16* __restrict__ qkv, int heads, int kv_h
 // from dq (q_rows x heads*d); dk/dv from the chunk accumulators (zeroed after
 // reading when `zero_kv`).  y1 = x1 c - x2 s, y2 = x2 c + x1 s  =>
 // dx1 = g1 c + g2 s, dx2 = g2 c - g1 s.
-__global__ void rope_qkv_bwd_k(const float* __restrict__ dq, float* dk, float* dv, int64_t kv_stride, int heads,
+// 4 consecutive accumulator values as floats (fp32 or bf16 storage), and
+// their reset
+__device__ __forceinline__ float4 ld_acc4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ float4 ld_acc4(const bf16* p) {
+  const uint2 u = *reinterpret_cast<const uint2*>(p);
+  const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+  const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+  return make_float4(a.x, a.y, b.x, b.y);
+}
+__device__ __forceinline__ void zero_acc4(float* p) { *reinterpret_cast<float4*>(p) = make_float4(0.f, 0.f, 0.f, 0.f); }
+__device__ __forceinline__ void zero_acc4(bf16* p) { *reinterpret_cast<uint2*>(p) = make_uint2(0u, 0u); }
+
+template <typename AccT>
+__global__ void rope_qkv_bwd_k(const float* __restrict__ dq, AccT* dk, AccT* dv, int64_t kv_stride, int heads,
                                int kv_heads, int d, int64_t pos0, const float* __restrict__ cs,
                                const float* __restrict__ sn, bf16* __restrict__ dqkv, int zero_kv) {
   const int64_t r = blockIdx.x;
@@ -257,15 +270,21 @@ __global__ void rope_qkv_bwd_k(const float* __restrict__ dq, float* dk, float* d
   bf16* dst = dqkv + r * int64_t(heads + 2 * kv_heads) * d;
   const float* c_row = cs + (pos0 + r) * half;
   const float* s_row = sn + (pos0 + r) * half;
-  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int idx = threadIdx.x; idx < (heads + kv_heads) * qpr; idx += blockDim.x) {
     const int h = idx / qpr, j = (idx % qpr) * 4;
-    float* g = h < heads ? const_cast<float*>(dq) + r * int64_t(heads) * d + h * d : dk + r * kv_stride + (h - heads) * d;
-    const float4 a = *reinterpret_cast<const float4*>(g + j);
-    const float4 b = *reinterpret_cast<const float4*>(g + j + half);
-    if (h >= heads && zero_kv) {
-      *reinterpret_cast<float4*>(g + j) = zero;
-      *reinterpret_cast<float4*>(g + j + half) = zero;
+    float4 a, b;
+    if (h < heads) {
+      const float* g = dq + r * int64_t(heads) * d + h * d;
+      a = ld_acc4(g + j);
+      b = ld_acc4(g + j + half);
+    } else {
+      AccT* g = dk + r * kv_stride + (h - heads) * d;
+      a = ld_acc4(g + j);
+      b = ld_acc4(g + j + half);
+      if (zero_kv) {
+        zero_acc4(g + j);
+        zero_acc4(g + j + half);
+      }
     }
     const float4 c = *reinterpret_cast<const float4*>(c_row + j);
     const float4 sv = *reinterpret_cast<const float4*>(s_row + j);
@@ -281,11 +300,21 @@ __global__ void rope_qkv_bwd_k(const float* __restrict__ dq, float* dk, float* d
     st4(dst + h * d + j + half, o2);
   }
   for (int idx = threadIdx.x; idx < kv_heads * d / 4; idx += blockDim.x) {
-    float4* p = reinterpret_cast<float4*>(dv + r * kv_stride) + idx;
-    const float4 v = *p;
+    AccT* p = dv + r * kv_stride + idx * 4;
+    const float4 v = ld_acc4(p);
     const float f[4] = {v.x, v.y, v.z, v.w};
     st4(dst + (heads + kv_heads) * d + idx * 4, f);
-    if (zero_kv) *p = zero;
+    if (zero_kv) zero_acc4(p);
+  }
+}
+
+// bf16 dst += fp32 src (the exchange's returned dK/dV partials into bf16 accumulators)
+__global__ void add_to_bf16_k(bf16* __restrict__ d, const float* __restrict__ s, int64_t n2) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n2; i += int64_t(gridDim.x) * blockDim.x) {
+    __nv_bfloat162* p = reinterpret_cast<__nv_bfloat162*>(d) + i;
+    const float2 a = __bfloat1622float2(*p);
+    const float2 b = reinterpret_cast<const float2*>(s)[i];
+    *p = __floats2bfloat162_rn(a.x + b.x, a.y + b.y);
   }
 }
 
@@ -582,12 +611,24 @@ int rope_qkv_fwd(const void* qkv, int64_t rows, int heads, int kv_heads, int d, 
   return cuda_status(cudaGetLastError(), "rope_qkv_fwd");
 }
 
-int rope_qkv_bwd(const float* dq, float* dk, float* dv, int64_t kv_stride, int64_t rows, int heads, int kv_heads,
-                 int d, int64_t pos0, const float* cs, const float* sn, void* dqkv, int zero_kv, cudaStream_t st) {
-  rope_qkv_bwd_k<<<unsigned(rows), 256, 0, st>>>(dq, dk, dv, kv_stride, heads, kv_heads, d, pos0, cs, sn, (bf16*)dqkv,
-                                                 zero_kv);
+int rope_qkv_bwd(const float* dq, void* dk, void* dv, int64_t kv_stride, int64_t rows, int heads, int kv_heads,
+                 int d, int64_t pos0, const float* cs, const float* sn, void* dqkv, int zero_kv, cudaStream_t st,
+                 bool acc_bf16) {
+  if (acc_bf16)
+    rope_qkv_bwd_k<<<unsigned(rows), 256, 0, st>>>(dq, static_cast<bf16*>(dk), static_cast<bf16*>(dv), kv_stride, heads,
+                                                   kv_heads, d, pos0, cs, sn, (bf16*)dqkv, zero_kv);
+  else
+    rope_qkv_bwd_k<<<unsigned(rows), 256, 0, st>>>(dq, static_cast<float*>(dk), static_cast<float*>(dv), kv_stride,
+                                                   heads, kv_heads, d, pos0, cs, sn, (bf16*)dqkv, zero_kv);
   count_launch();
   return cuda_status(cudaGetLastError(), "rope_qkv_bwd");
+}
+
+int add_to_bf16(void* dst, const float* src, int64_t n, cudaStream_t st) {
+  if (n % 2) return set_error(SP_ERR_UNSUPPORTED, "add_to_bf16: odd length");
+  add_to_bf16_k<<<grid_for(n / 2, 256), 256, 0, st>>>(static_cast<bf16*>(dst), src, n / 2);
+  count_launch();
+  return cuda_status(cudaGetLastError(), "add_to_bf16");
 }
 
 int swiglu_fwd(const void* gu, void* act, int64_t rows, int H, cudaStream_t st) {
@@ -671,7 +712,9 @@ int preload_layers() {
   if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(rmsnorm_dw_sum_k))) return cuda_status(e, "preload rmsnorm_dw_sum_k");
   if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(rope_table_k))) return cuda_status(e, "preload rope_table_k");
   if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(rope_qkv_fwd_k))) return cuda_status(e, "preload rope_qkv_fwd_k");
-  if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(rope_qkv_bwd_k))) return cuda_status(e, "preload rope_qkv_bwd_k");
+  if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(rope_qkv_bwd_k<float>))) return cuda_status(e, "preload rope_qkv_bwd_k");
+  if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(rope_qkv_bwd_k<bf16>))) return cuda_status(e, "preload rope_qkv_bwd_k<bf16>");
+  if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(add_to_bf16_k))) return cuda_status(e, "preload add_to_bf16_k");
   if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(swiglu_fwd_k))) return cuda_status(e, "preload swiglu_fwd_k");
   if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(swiglu_bwd_k))) return cuda_status(e, "preload swiglu_bwd_k");
   if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(xent_k))) return cuda_status(e, "preload xent_k");

@@ -340,6 +340,32 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// dst[0..32) += a for a dK/dV chunk accumulator row segment: fp32 storage, or
+// bf16 storage (the runtime's dkv_bf16 option: fp32 sums rounded to bf16
+// after every slice's contribution)
+__device__ __forceinline__ void acc_add32(float* dst, const float (&a)[32]) {
+  float4* g = reinterpret_cast<float4*>(dst);
+#pragma unroll
+  for (int x = 0; x < 8; ++x) {
+    const float4 o = g[x];
+    g[x] = make_float4(o.x + a[4 * x], o.y + a[4 * x + 1], o.z + a[4 * x + 2], o.w + a[4 * x + 3]);
+  }
+}
+__device__ __forceinline__ void acc_add32(__nv_bfloat16* dst, const float (&a)[32]) {
+  uint4* g = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+  for (int x = 0; x < 4; ++x) {
+    uint4 o = g[x];
+    uint32_t w[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]));
+      w[e] = pack_bf16(f.x + a[8 * x + 2 * e], f.y + a[8 * x + 2 * e + 1]);
+    }
+    g[x] = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }

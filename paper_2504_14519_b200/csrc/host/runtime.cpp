@@ -152,7 +152,10 @@ class Runtime {
   size_t offload_bytes = 0;
   int slots_in_use = 0, slots_high_water = 0;
   // fp32 dK/dV chunk accumulators (one microbatch, indexed by slice)
-  std::vector<float*> dk_acc, dv_acc;
+  std::vector<void*> dk_acc, dv_acc;  // fp32, or bf16 with cfg.dkv_bf16
+  bool dkv_bf16 = false;
+  int64_t acc_es = 4;  // accumulator element size
+  void* acc_at(void* base, int64_t elems) const { return static_cast<char*>(base) + elems * acc_es; }
 
   // workspaces
   std::vector<LayerWs> ws;
@@ -338,6 +341,9 @@ class Runtime {
     stash = c.recompute != 1;  // 2 (auto) is settled in alloc_arena once the parameters are resident
     if (c.offload < 0 || c.offload > 1) return set_error(SP_ERR_INVALID, "offload must be 0 or 1");
     offload = c.offload == 1;
+    if (c.dkv_bf16 < 0 || c.dkv_bf16 > 1) return set_error(SP_ERR_INVALID, "dkv_bf16 must be 0 or 1");
+    dkv_bf16 = c.dkv_bf16 == 1;
+    acc_es = dkv_bf16 ? 2 : 4;
     h = c.hidden;
     H = c.ffn_hidden;
     qd = int64_t(c.heads) * c.head_dim;
@@ -943,10 +949,11 @@ class Runtime {
       SP_TRY(alloc(&v_pool[l], rows * kvd));
     }
     for (int l = 0; l < v * Lps; ++l) {
-      SP_TRY(alloc(&dk_acc[l], acc_rows * kvd));
-      SP_TRY(alloc(&dv_acc[l], acc_rows * kvd));
-      SP_CUDA(cudaMemsetAsync(dk_acc[l], 0, acc_rows * kvd * 4, comp));
-      SP_CUDA(cudaMemsetAsync(dv_acc[l], 0, acc_rows * kvd * 4, comp));
+      // byte buffers of acc_es-sized elements
+      SP_TRY(alloc(reinterpret_cast<char**>(&dk_acc[l]), acc_rows * kvd * acc_es));
+      SP_TRY(alloc(reinterpret_cast<char**>(&dv_acc[l]), acc_rows * kvd * acc_es));
+      SP_CUDA(cudaMemsetAsync(dk_acc[l], 0, acc_rows * kvd * acc_es, comp));
+      SP_CUDA(cudaMemsetAsync(dv_acc[l], 0, acc_rows * kvd * acc_es, comp));
     }
     if (cfg.recompute == 2) {  // auto: stash O/LSE only if it fits beside everything allocated so far
       size_t free_b = 0, total_b = 0;
@@ -1308,9 +1315,10 @@ class Runtime {
     t.flops = 2.5 * attn_flops(int(rows.size()), causal);
     t.kind = 1;
     SP_CUDA(cudaEventRecord(t.a, comp));
-    SP_TRY(sp_attn_bwd_core(x.q, Ls, qd, k_pool[l], v_pool[l], int64_t(slots) * Ls, kvd, rows.data(), int(rows.size()),
-                            int(Ls), cfg.heads, cfg.kv_heads, cfg.head_dim, causal, tmp_h, qd, delta_ws, dq_acc,
-                            dk_acc[lbase + l], dv_acc[lbase + l], int64_t(cfg.slices) * Ls, acc_rows.data(), comp));
+    SP_TRY(attn_bwd_core(x.q, Ls, qd, k_pool[l], v_pool[l], int64_t(slots) * Ls, kvd, rows.data(), int(rows.size()),
+                         int(Ls), cfg.heads, cfg.kv_heads, cfg.head_dim, causal, tmp_h, qd, delta_ws, dq_acc,
+                         dk_acc[lbase + l], dv_acc[lbase + l], int64_t(cfg.slices) * Ls, acc_rows.data(), dkv_bf16,
+                         comp));
     SP_CUDA(cudaEventRecord(t.b, comp));
     attn_times.push_back(t);
     if (out) {
@@ -1330,14 +1338,20 @@ class Runtime {
         SP_TRY(add_f32(dq_acc, b.dq_rem + tt * Ls * qd, Ls * qd, comp));
         for (std::size_t x2 = 0; x2 < xo.chunks.size(); ++x2) {
           const int64_t dst = int64_t(xo.chunks[x2] - 1) * Ls * kvd, src = int64_t(xo.base + x2) * Ls * kvd;
-          SP_TRY(add_f32(dk_acc[lbase + l] + dst, b.dk_rem + src, Ls * kvd, comp));
-          SP_TRY(add_f32(dv_acc[lbase + l] + dst, b.dv_rem + src, Ls * kvd, comp));
+          if (dkv_bf16) {
+            SP_TRY(add_to_bf16(acc_at(dk_acc[lbase + l], dst), b.dk_rem + src, Ls * kvd, comp));
+            SP_TRY(add_to_bf16(acc_at(dv_acc[lbase + l], dst), b.dv_rem + src, Ls * kvd, comp));
+          } else {
+            SP_TRY(add_f32(static_cast<float*>(acc_at(dk_acc[lbase + l], dst)), b.dk_rem + src, Ls * kvd, comp));
+            SP_TRY(add_f32(static_cast<float*>(acc_at(dv_acc[lbase + l], dst)), b.dv_rem + src, Ls * kvd, comp));
+          }
         }
       }
     }
     // chunk i's dK/dV is complete: RoPE backward into d_qkv and reset the rows
-    SP_TRY(rope_qkv_bwd(dq_acc, dk_acc[lbase + l] + pos0 * kvd, dv_acc[lbase + l] + pos0 * kvd, kvd, Ls, cfg.heads, cfg.kv_heads,
-                        cfg.head_dim, pos0, rope_cos, rope_sin, dqkv, 1, comp));
+    SP_TRY(rope_qkv_bwd(dq_acc, acc_at(dk_acc[lbase + l], pos0 * kvd), acc_at(dv_acc[lbase + l], pos0 * kvd), kvd, Ls,
+                        cfg.heads, cfg.kv_heads,
+                        cfg.head_dim, pos0, rope_cos, rope_sin, dqkv, 1, comp, dkv_bf16));
     SP_TRY(gemm(false, false, Ls, h, qkv_w, dqkv, qkv_w, W(P.wqkv), h, tmp_h, h, false, 1.f, 0.f, comp));   // dxn
     SP_TRY(gemm(true, false, qkv_w, h, Ls, dqkv, qkv_w, x.xn, h, G(P.wqkv), h, true, 1.f, 1.f, comp));      // dWqkv
     SP_TRY(rmsnorm_bwd(tmp_h, x.x_in, W(P.attn_norm), x.rstd1, dx, dx, G(P.attn_norm), Ls, int(h), comp, norm_ws));

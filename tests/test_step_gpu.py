@@ -60,8 +60,13 @@ def _pull(step, cfg):
                                           (1, 4, "full", {"hidden": 512, "kv_heads": 4, "ffn_hidden": 1024}),
                                           # activation offload (stage input + O/LSE via pinned host memory)
                                           (2, 4, "selective", {"offload": True}),
-                                          (2, 4, "full", {"offload": True, "hidden": 512, "ffn_hidden": 1024})],
-                         ids=["base", "m1n2", "full", "gqa", "d128-gqa", "d128-full", "offload", "offload-d128-full"])
+                                          (2, 4, "full", {"offload": True, "hidden": 512, "ffn_hidden": 1024}),
+                                          # bf16 dK/dV accumulators (d=64 and d=128 kernels)
+                                          (2, 4, "selective", {"dkv_bf16": True}),
+                                          (2, 4, "selective", {"dkv_bf16": True, "hidden": 512, "kv_heads": 2,
+                                                               "ffn_hidden": 1024})],
+                         ids=["base", "m1n2", "full", "gqa", "d128-gqa", "d128-full", "offload", "offload-d128-full",
+                              "dkv-bf16", "dkv-bf16-d128-gqa"])
 def test_c1_step_matches_oracle(m, n, rc, shape):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
