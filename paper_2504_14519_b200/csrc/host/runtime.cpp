@@ -332,6 +332,12 @@ class Runtime {
       return set_error(SP_ERR_UNSUPPORTED, "interleave > 1 needs an even pp >= 2 (stage ring links)");
     if (v > 1 && (c.exchange_mode != 0 || c.vocab_parallel))
       return set_error(SP_ERR_UNSUPPORTED, "interleave > 1 runs with exchange off and vocab_parallel 0");
+    // the exchange serves peers on the same per-class stream as its own
+    // requests; with the vocabulary collectives holding every rank's compute
+    // stream at the same pass, a served partial can queue behind a request
+    // that waits on that pass (measured: PP=4 stall) — not combined
+    if (c.vocab_parallel && c.exchange_mode != 0 && c.pp > 1)
+      return set_error(SP_ERR_UNSUPPORTED, "vocab_parallel runs with exchange off");
     if (c.layers % nst) return set_error(SP_ERR_INVALID, "layers (%d) must divide by pp*v (%d)", c.layers, nst);
     if (c.seq_len % c.slices) return set_error(SP_ERR_INVALID, "run: seq_len must be divisible by slices");
     if (c.hidden != c.heads * c.head_dim) return set_error(SP_ERR_INVALID, "hidden != heads * head_dim");

@@ -64,6 +64,8 @@ def test_runtime_rejects_invalid_configs_before_touching_the_device(kw, msg):
     ({"pp": 2, "layers": 6, "interleave": 2}, "SP_ERR_INVALID", b"pp*v"),
     ({"pp": 2, "layers": 2, "vocab": 1002, "vocab_parallel": True}, "SP_ERR_INVALID", b"multiple of 4"),
     ({"slices": 512, "seq_len": 512 * 128}, "SP_ERR_UNSUPPORTED", b"SP_MAX_CHUNKS"),  # before any NCCL call
+    ({"pp": 2, "layers": 4, "vocab": 1024, "vocab_parallel": True, "exchange": "on"}, "SP_ERR_UNSUPPORTED",
+     b"exchange off"),
 ])
 def test_experimental_paths_reject_unsupported_configs_host_side(kw, code, msg):
     """Interleaving / vocabulary parallelism preconditions (runtime.cpp init),

@@ -19,7 +19,7 @@ ROOT = Path(__file__).resolve().parents[1]
                                          (4, 2, 8, "early", "full"),
                                          (2, 2, 4, "on", "selective-gqa"),  # GQA 4:2 through the exchange
                                          (2, 2, 4, "off", "selective-vp"),  # vocabulary parallelism (§8f)
-                                         (4, 2, 8, "off", "full-vp"), (4, 2, 8, "on", "selective-vp"),
+                                         (4, 2, 8, "off", "full-vp"),
                                          (2, 2, 4, "off", "selective-v2"),  # interleaved v=2 (§8f rank 2)
                                          (2, 1, 4, "off", "full-v2"), (4, 2, 8, "off", "selective-v2"),
                                          (2, 2, 4, "on", "selective-ol"),  # activation offload
