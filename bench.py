@@ -75,6 +75,10 @@ def parse():
                     help="shard the LM head and cross entropy over all stages (PP>1; SURVEY §8f rank 1)")
     ap.add_argument("--offload", action="store_true",
                     help="activation offload: stage inputs + attention O/LSE in pinned host memory between F and BW")
+    ap.add_argument("--exchange-min-chunks", type=int, default=0,
+                    help="exchange placement: drop plan transfers that move fewer KV chunks")
+    ap.add_argument("--exchange-skip-last", action="store_true",
+                    help="exchange placement: drop plan transfers into the last stage (it also runs the LM head)")
     ap.add_argument("--dkv-bf16", action="store_true", help="dK/dV chunk accumulators stored in bf16 (half their HBM)")
     ap.add_argument("--interleave", type=int, default=1,
                     help="v stages per GPU (interleaved SlimPipe, even PP; SURVEY §8f rank 2)")
@@ -109,14 +113,17 @@ def make_cfg(args, world):
     return base.__class__(**{**base.__dict__, **kw, "pp": world, "exchange": args.exchange,
                              "recompute": args.recompute, "vocab_parallel": bool(args.vocab_parallel and world > 1),
                              "interleave": args.interleave if world > 1 else 1, "offload": bool(args.offload),
-                             "dkv_bf16": bool(args.dkv_bf16)})
+                             "dkv_bf16": bool(args.dkv_bf16), "exchange_min_chunks": args.exchange_min_chunks,
+                             "exchange_skip_last": bool(args.exchange_skip_last)})
 
 
 def workload_name(cfg, model="c2"):
     return (f"{MODEL_NAMES[model][0]} layer shapes x{cfg.layers} layers, {cfg.seq_len // 1024}K ctx, n={cfg.slices} slices, "
             f"m={cfg.microbatches}, PP={cfg.pp}, exchange={cfg.exchange}, recompute={cfg.recompute}"
             + (", vocab-parallel" if cfg.vocab_parallel else "") + (f", v={cfg.interleave}" if cfg.interleave > 1 else "")
-            + (", activation offload" if cfg.offload else "") + (", bf16 dK/dV accumulators" if cfg.dkv_bf16 else ""))
+            + (", activation offload" if cfg.offload else "") + (", bf16 dK/dV accumulators" if cfg.dkv_bf16 else "")
+            + (f", exchange min {cfg.exchange_min_chunks} chunks" if cfg.exchange != "off" and cfg.exchange_min_chunks > 1 else "")
+            + (", no exchange into the last stage" if cfg.exchange != "off" and cfg.exchange_skip_last else ""))
 
 
 # ----------------------------------------------------------------- clocks
@@ -471,6 +478,9 @@ def main():
                                            cfg.vocab), 1, 1, world, 1, cfg.seq_len, cfg.microbatches, cfg.slices)
     ledger_gb = float(mm["slice_stage"]) * (cfg.slices + 2 * (world - 1)) / 1e9 if cfg.microbatches * cfg.slices >= \
         cfg.slices + 2 * (world - 1) else None
+    offload_gb = max_over_ranks(mem["offload_host_bytes"] / 1e9)  # collectives: every rank, before the rank-0 line
+    xst = step.exchange_stats() if cfg.exchange != "off" else None
+    x_out = sum_over_ranks(xst["passes_out"]) if xst else 0
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -499,7 +509,8 @@ def main():
                                             if calib else None),
             "peak_act_gb_per_gpu": arena_gb, "dkv_accum_gb_per_gpu": dkv_gb, "ledger_pred_gb_per_gpu": ledger_gb,
             "arena_slots": mem["slots"], "arena_high_water": mem["slots_high_water"],
-            "offload_host_gb_per_gpu": max_over_ranks(mem["offload_host_bytes"] / 1e9),
+            "offload_host_gb_per_gpu": offload_gb,
+            "exchange_passes_sending": int(x_out),  # passes (all ranks) that ship attention work under the placement
             # logits workspace of the stage(s) holding the LM head: [Ls, V] fp32 logits + dlogits
             # (last stage), or the [Ls, V/p] shard (fp32 logits + bf16 dlogits) on every stage
             # under vocabulary parallelism (reference logits_bytes, workload.cpp:154-160)

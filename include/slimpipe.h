@@ -221,6 +221,14 @@ typedef struct {
    * fp32 inside each backward kernel, rounded once per slice contribution):
    * half their HBM; 0: fp32 storage. */
   int32_t dkv_bf16;
+  /* exchange placement (exchange_mode != 0): the executor runs the reference
+   * plan's transfers (apply_exchange, simulator.cpp:56-108) except those that
+   * move fewer than exchange_min_chunks KV chunks (0 or 1 = keep all) and,
+   * with exchange_skip_last = 1, those whose receiver is the last stage —
+   * which also runs the LM head and the loss that the plan's attention-only
+   * tick loads do not count.  Every rank drops the same transfers. */
+  int32_t exchange_min_chunks;
+  int32_t exchange_skip_last;
 } sp_model_config;
 
 #define SP_STEP_NO_OPTIMIZER 1

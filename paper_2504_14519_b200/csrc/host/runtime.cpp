@@ -336,6 +336,8 @@ class Runtime {
     // requests; with the vocabulary collectives holding every rank's compute
     // stream at the same pass, a served partial can queue behind a request
     // that waits on that pass (measured: PP=4 stall) — not combined
+    if (c.exchange_min_chunks < 0 || c.exchange_skip_last < 0 || c.exchange_skip_last > 1)
+      return set_error(SP_ERR_INVALID, "exchange_min_chunks must be >= 0 and exchange_skip_last 0 or 1");
     if (c.vocab_parallel && c.exchange_mode != 0 && c.pp > 1)
       return set_error(SP_ERR_UNSUPPORTED, "vocab_parallel runs with exchange off");
     if (c.layers % nst) return set_error(SP_ERR_INVALID, "layers (%d) must divide by pp*v (%d)", c.layers, nst);
@@ -705,6 +707,9 @@ class Runtime {
       for (const pipelab::Transfer& tr : tp.plan.transfers) {
         const int sp = pass_of(tr.src), dp = pass_of(tr.dst);
         if (sp < 0 || dp < 0) continue;
+        // placement filter (slimpipe.h): identical on every rank
+        if (int(tr.kv_chunk_indices.size()) < cfg.exchange_min_chunks) continue;
+        if (cfg.exchange_skip_last && tr.dst == p) continue;
         std::vector<int> ch(tr.kv_chunk_indices.begin(), tr.kv_chunk_indices.end());
         if (tr.src == me) {
           PassX& px = xplan[sp];

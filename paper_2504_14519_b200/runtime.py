@@ -25,7 +25,8 @@ class _Cfg(C.Structure):
                                          "microbatches", "slices", "pp", "rank", "exchange_mode")] + [
         ("seq_len", C.c_int64), ("rope_theta", C.c_float), ("norm_eps", C.c_float), ("lr", C.c_float),
         ("seed", C.c_uint64), ("recompute", C.c_int32), ("vocab_parallel", C.c_int32),
-        ("interleave", C.c_int32), ("offload", C.c_int32), ("dkv_bf16", C.c_int32)]
+        ("interleave", C.c_int32), ("offload", C.c_int32), ("dkv_bf16", C.c_int32),
+        ("exchange_min_chunks", C.c_int32), ("exchange_skip_last", C.c_int32)]
 
 
 RECOMPUTE = {"selective": 0, "full": 1, "auto": 2}
@@ -49,6 +50,8 @@ class StepConfig:
     interleave: int = 1  # v stages per device (interleaved SlimPipe; even pp, exchange off)
     offload: bool = False  # stage inputs + attention O/LSE to pinned host memory between F and BW
     dkv_bf16: bool = False  # dK/dV chunk accumulators stored in bf16 (half their HBM)
+    exchange_min_chunks: int = 0  # exchange placement: drop plan transfers moving fewer KV chunks
+    exchange_skip_last: bool = False  # exchange placement: drop plan transfers into the last stage
     rope_theta: float = 10000.0
     norm_eps: float = 1e-5
     lr: float = 1e-4
@@ -114,7 +117,8 @@ class StepConfig:
         return _Cfg(self.layers, self.hidden, self.ffn_hidden, self.heads, self.kv_heads, self.head_dim, self.vocab,
                     self.microbatches, self.slices, self.pp, rank, N.MODES[self.exchange], self.seq_len,
                     self.rope_theta, self.norm_eps, self.lr, self.seed, RECOMPUTE[self.recompute],
-                    int(self.vocab_parallel), int(self.interleave), int(self.offload), int(self.dkv_bf16))
+                    int(self.vocab_parallel), int(self.interleave), int(self.offload), int(self.dkv_bf16),
+                    int(self.exchange_min_chunks), int(self.exchange_skip_last))
 
     # ---- accounting ----
     def linear_params_per_layer(self) -> int:

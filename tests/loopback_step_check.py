@@ -6,6 +6,7 @@ wedging the test session:
 
     python tests/loopback_step_check.py PP M N EXCHANGE RECOMPUTE [KV_HEADS INTERLEAVE VOCAB_PARALLEL]
 
+(env SP_XMIN / SP_XSKIP=1: the exchange placement filter, slimpipe.h)
 Exit code 0 = parity holds; 3 = the step did not finish in time."""
 import os
 
@@ -29,7 +30,9 @@ def main():
     v = int(sys.argv[7]) if len(sys.argv) > 7 else 1
     vp = len(sys.argv) > 8 and sys.argv[8] == "1"
     cfg = StepConfig.c1(pp=pp, microbatches=m, slices=n, layers=2 * pp * v, exchange=x, seq_len=1024 * n,
-                        recompute=rc, kv_heads=kv, interleave=v, vocab=1024 if vp else 1000, vocab_parallel=vp)
+                        recompute=rc, kv_heads=kv, interleave=v, vocab=1024 if vp else 1000, vocab_parallel=vp,
+                        exchange_min_chunks=int(os.environ.get("SP_XMIN", 0)),
+                        exchange_skip_last=os.environ.get("SP_XSKIP") == "1")
     world = LoopbackWorld(pp)
     steps = [SlimPipeStep(cfg, r, pp, loopback=world) for r in range(pp)]
     tok, tgt = SP.inputs(cfg)

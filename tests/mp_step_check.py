@@ -41,7 +41,9 @@ def main():
                         vocab=1024 if vp else 1000,  # vocab shards must be a multiple of 4 wide
                         seq_len=1024 * n, recompute=os.environ.get("SP_RC", "selective"),
                         kv_heads=int(os.environ.get("SP_KV", 4)), vocab_parallel=vp,
-                        interleave=int(os.environ.get("SP_V", 1)), offload=os.environ.get("SP_OFFLOAD") == "1")
+                        interleave=int(os.environ.get("SP_V", 1)), offload=os.environ.get("SP_OFFLOAD") == "1",
+                        exchange_min_chunks=int(os.environ.get("SP_XMIN", 0)),
+                        exchange_skip_last=os.environ.get("SP_XSKIP") == "1")
     step = SlimPipeStep(cfg, rank, world)
     tok, tgt = SP.inputs(cfg)
     # the step on a watched thread: a stall reports where this rank stands

@@ -66,6 +66,8 @@ def test_runtime_rejects_invalid_configs_before_touching_the_device(kw, msg):
     ({"slices": 512, "seq_len": 512 * 128}, "SP_ERR_UNSUPPORTED", b"SP_MAX_CHUNKS"),  # before any NCCL call
     ({"pp": 2, "layers": 4, "vocab": 1024, "vocab_parallel": True, "exchange": "on"}, "SP_ERR_UNSUPPORTED",
      b"exchange off"),
+    ({"pp": 2, "layers": 4, "exchange": "on", "exchange_min_chunks": -1}, "SP_ERR_INVALID", b"exchange_min_chunks"),
+    ({"pp": 2, "layers": 4, "exchange": "on", "exchange_skip_last": 2}, "SP_ERR_INVALID", b"exchange_skip_last"),
 ])
 def test_experimental_paths_reject_unsupported_configs_host_side(kw, code, msg):
     """Interleaving / vocabulary parallelism preconditions (runtime.cpp init),

@@ -70,7 +70,7 @@ def test_loopback_transport_pingpong():
     assert int(bufs[0][1].min()) == 2 and int(bufs[1][1].max()) == 1
 
 
-def _run(pp, m, n, exchange, recompute, kv_heads=4, interleave=1, vocab_parallel=False):
+def _run(pp, m, n, exchange, recompute, kv_heads=4, interleave=1, vocab_parallel=False, env=None):
     """One case in its own process (tests/loopback_step_check.py): a stall
     ends that process and its GPU context, not the session."""
     import os
@@ -82,7 +82,7 @@ def _run(pp, m, n, exchange, recompute, kv_heads=4, interleave=1, vocab_parallel
             recompute, str(kv_heads), str(interleave), "1" if vocab_parallel else "0"]
     try:
         r = subprocess.run(args, capture_output=True, text=True, timeout=300,
-                           env=dict(os.environ, PYTHONUNBUFFERED="1"))
+                           env=dict(os.environ, PYTHONUNBUFFERED="1", **(env or {})))
     except subprocess.TimeoutExpired as e:
         print(e.stdout or "", e.stderr or "")
         return False, "timeout"
@@ -100,6 +100,15 @@ def test_loopback_step_matches_oracle(pp, m, n, x, rc):
     """(the child also checks that exchange on / early really moved work)"""
     _need_gpu()
     ok, worst = _run(pp, m, n, x, rc)
+    assert ok, worst
+
+
+def test_loopback_exchange_placement_filter():
+    """The placement filter (slimpipe.h exchange_min_chunks / skip_last):
+    only the plan's multi-chunk transfers that avoid the last stage run —
+    still parity, still work moved."""
+    _need_gpu()
+    ok, worst = _run(4, 2, 8, "early", "selective", env={"SP_XMIN": "2", "SP_XSKIP": "1"})
     assert ok, worst
 
 
