@@ -384,9 +384,21 @@ def main():
     # last timed step: per-pass busy (bubble) and attention kernel timings
     step_ms, passes = step.timeline()
     per_dev = [passes]
+    clock_check = None
     if world > 1 and (args.gantt or args.calibrate):
-        per_dev = [None] * world
+        # each rank's spans are relative to its own step start; shift them onto
+        # rank 0's clock with the GPUs' global timers stamped at step start
+        per_dev, clocks = [None] * world, [None] * world
         dist.all_gather_object(per_dev, passes)
+        dist.all_gather_object(clocks, step.step_clock_ns())
+        per_dev = [[(i, s + (clocks[r] - clocks[0]) / 1e6, e + (clocks[r] - clocks[0]) / 1e6) for i, s, e in spans]
+                   for r, spans in enumerate(per_dev)]
+        # sanity of the common clock: a stage's first pass cannot start before
+        # the previous stage's first pass ended (its input)
+        firsts = [min(spans, key=lambda x: x[1]) for spans in per_dev]
+        clock_check = {"offsets_ms": [(c - clocks[0]) / 1e6 for c in clocks],
+                       "causality_violation_ms": max(0.0, max(firsts[r - 1][2] - firsts[r][1]
+                                                              for r in range(1, world)))}
     calib = None
     if args.calibrate and rank == 0 and not cfg.vocab_parallel:
         from paper_2504_14519_b200 import calibrate as CAL
@@ -505,6 +517,7 @@ def main():
                        "l2": "inputs larger than L2 (per-step working set tens of GB)"},
             "mfu": mfu, "mfu_nominal": mfu_nominal, "mfu_peak_tflops": peak_tf,
             "bubble_fraction": bubble,
+            "timeline_clock": clock_check,
             "bubble_simulated_calibrated": ({k: v["bubble"] for k, v in calib["simulated"].items()}
                                             if calib else None),
             "peak_act_gb_per_gpu": arena_gb, "dkv_accum_gb_per_gpu": dkv_gb, "ledger_pred_gb_per_gpu": ledger_gb,
