@@ -96,6 +96,15 @@ class Runtime {
   // compute stream to reach their pass instead of being posted as soon as a
   // ring buffer frees (fewer NCCL kernels spinning on the SMs at once)
   bool jit_recv = std::getenv("SP_JIT_RECV") != nullptr;
+  // exchange serves post their receives when the receiving pass starts on
+  // this rank's compute stream instead of as soon as the exchange stream
+  // reaches them: an NCCL receive kernel spins on its SMs until the sender's
+  // data arrives, and a serve queued from the host's run-ahead would spin
+  // for most of the step (SP_XSERVE_JIT=0 restores the early post)
+  bool xserve_jit = [] {
+    const char* e = std::getenv("SP_XSERVE_JIT");
+    return !(e && e[0] == '0');
+  }();
   int64_t Ls = 0, h = 0, H = 0, qd = 0, kvd = 0, qkv_w = 0;
   pipelab::Schedule sched;
   std::vector<pipelab::PassId> order;
@@ -510,7 +519,7 @@ class Runtime {
     ncclUniqueId id[SP_NCCL_IDS];
     std::memcpy(id, ids, sizeof id);
     // SP_NCCL_MAX_CTAS=N (diagnostics, default unset = NCCL's choice) caps
-    // the CTAs of every stage communicator's kernels
+    // the CTAs of every stage and exchange communicator's kernels
     ncclConfig_t ccfg = NCCL_CONFIG_INITIALIZER;
     ncclConfig_t* pcfg = nullptr;
     if (const char* mc = std::getenv("SP_NCCL_MAX_CTAS")) {
@@ -554,7 +563,8 @@ class Runtime {
     if (!xplan.empty() || cfg.exchange_mode != 0)
       for (int k = 0; k < 2; ++k) {
         ncclComm_t cm = nullptr;
-        SP_NCCL(ncclCommInitRank(&cm, p, id[2 + k], rank));
+        if (pcfg) SP_NCCL(ncclCommInitRankConfig(&cm, p, id[2 + k], rank, pcfg));
+        else SP_NCCL(ncclCommInitRank(&cm, p, id[2 + k], rank));
         lx[k] = make_nccl_link(cm);
       }
     if (vp) {  // the vocabulary collectives run on the world communicator nc_bwd
@@ -833,6 +843,7 @@ class Runtime {
     const int c = px.cls;
     XBuf& b = xb[c];
     const int64_t a = cfg.heads;
+    if (xserve_jit) SP_TRY(link(comp, cx[c]));
     auto fwd_layer = [&]() -> int {
       for (std::size_t t = 0; t < px.in.size(); ++t) {
         const XIn& xi = px.in[t];
