@@ -15,7 +15,7 @@ import stream_model as SM
 def test_enqueue_program_is_deadlock_free(p, v, m, n, vp):
     assert not SM.deadlocks(p, v, m, n, vp)
     assert not SM.deadlocks(p, v, m, n, vp, host_queue=8)
-    assert not SM.deadlocks(p, v, m, n, vp, jit_recv=True)  # SP_JIT_RECV=1
+    assert not SM.deadlocks(p, v, m, n, vp, jit_recv=True)  # the executor's default (SP_JIT_RECV=0: early posts)
 
 
 def test_model_detects_a_collective_order_fault():
