@@ -386,19 +386,19 @@ def main():
     per_dev = [passes]
     clock_check = None
     if world > 1 and (args.gantt or args.calibrate):
-        # each rank's spans are relative to its own step start; shift them onto
-        # rank 0's clock with the GPUs' global timers stamped at step start
-        per_dev, clocks = [None] * world, [None] * world
+        per_dev = [None] * world
         dist.all_gather_object(per_dev, passes)
-        dist.all_gather_object(clocks, step.step_clock_ns())
-        per_dev = [[(i, s + (clocks[r] - clocks[0]) / 1e6, e + (clocks[r] - clocks[0]) / 1e6) for i, s, e in spans]
-                   for r, spans in enumerate(per_dev)]
-        # sanity of the common clock: a stage's first pass cannot start before
-        # the previous stage's first pass ended (its input)
-        firsts = [min(spans, key=lambda x: x[1]) for spans in per_dev]
-        clock_check = {"offsets_ms": [(c - clocks[0]) / 1e6 for c in clocks],
-                       "causality_violation_ms": max(0.0, max(firsts[r - 1][2] - firsts[r][1]
-                                                              for r in range(1, world)))}
+        # each rank's spans are relative to its own step start (CUDA events are
+        # per device, and the GPUs' global timers measured hundreds of ms apart),
+        # so place rank r on rank 0's clock by its first dependency: its first
+        # pass starts when the previous stage's first pass has delivered its
+        # output (the rank was waiting for it; the 128 MB message is < 1 ms)
+        offsets = [0.0]
+        for r in range(1, world):
+            prev_end = min(per_dev[r - 1], key=lambda x: x[1])[2] + offsets[r - 1]
+            offsets.append(prev_end - min(per_dev[r], key=lambda x: x[1])[1])
+        per_dev = [[(i, s + offsets[r], e + offsets[r]) for i, s, e in spans] for r, spans in enumerate(per_dev)]
+        clock_check = {"method": "first-pass dependency", "offsets_ms": offsets}
     calib = None
     if args.calibrate and rank == 0 and not cfg.vocab_parallel:
         from paper_2504_14519_b200 import calibrate as CAL

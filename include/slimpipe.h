@@ -267,9 +267,6 @@ int sp_runtime_step(void* handle, const int32_t* tokens, const int32_t* targets,
 int sp_runtime_sync(void* handle);
 void* sp_runtime_stream(void* handle);
 int sp_runtime_timeline(void* handle, double* out, int cap);
-/* %globaltimer (ns) of the GPU when the last step started: places every
- * rank's device-relative timeline on one clock (shift by the difference). */
-int sp_runtime_step_clock(void* handle, long long* ns);
 int sp_runtime_attn_stats(void* handle, double* out6);
 int sp_runtime_memory(void* handle, int64_t* out7);
 int sp_runtime_recompute(void* handle);

@@ -67,8 +67,9 @@ def fit_costs(p: int, v: int, m: int, n: int, seq_len: int, per_device) -> dict:
 def measured_bubble(per_device) -> tuple[float, float]:
     """(makespan, bubble) with the reference definition (p * makespan - sum busy)
     / sum busy (simulator.cpp:381-382) on measured spans, all on one clock
-    whose zero is stage 1's step start (bench.py shifts each rank's spans by
-    the GPUs' global-timer difference), as simulate() starts at 0."""
+    whose zero is stage 1's step start (bench.py shifts each rank so that its
+    first pass starts where the previous stage's first pass ended), as
+    simulate() starts at 0."""
     busy = sum(e - s for spans in per_device for _, s, e in spans)
     mk = max(e for spans in per_device for _, _, e in spans)
     return mk, (len(per_device) * mk - busy) / busy if busy > 0 else 0.0

@@ -32,7 +32,6 @@ int rope_qkv_bwd(const float* dq, void* dk, void* dv, int64_t kv_stride, int64_t
                  int d, int64_t pos0, const float* cs, const float* sn, void* dqkv, int zero_kv, cudaStream_t st,
                  bool acc_bf16 = false);
 int add_to_bf16(void* dst, const float* src, int64_t n, cudaStream_t st);  // bf16 dst += fp32 src
-int stamp_globaltimer(unsigned long long* out, cudaStream_t st);          // *out = %globaltimer (ns)
 int swiglu_fwd(const void* gu, void* act, int64_t rows, int H, cudaStream_t st);
 int swiglu_bwd(const void* dact, const void* gu, void* dgu, int64_t rows, int H, cudaStream_t st);
 int cross_entropy(const float* logits, const int32_t* tgt, int64_t rows, int V, float scale, void* dlogits,

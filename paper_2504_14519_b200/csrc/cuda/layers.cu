@@ -701,21 +701,6 @@ int f32_to_bf16(const float* a, void* b, int64_t n, cudaStream_t st) {
   return cuda_status(cudaGetLastError(), "f32_to_bf16");
 }
 
-// The GPU's global nanosecond timer when the stream reaches this point: the
-// executor stamps each step's start with it so per-device timelines (CUDA
-// events, device-relative) can be placed on one clock across ranks.
-__global__ void globaltimer_k(unsigned long long* out) {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  *out = t;
-}
-
-int stamp_globaltimer(unsigned long long* out, cudaStream_t st) {
-  globaltimer_k<<<1, 1, 0, st>>>(out);
-  count_launch();
-  return cuda_status(cudaGetLastError(), "stamp_globaltimer");
-}
-
 // Force-load this file's kernels (cudaFuncGetAttributes) — see preload_kernels
 int preload_layers() {
   cudaFuncAttributes a;
@@ -729,7 +714,6 @@ int preload_layers() {
   if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(rope_qkv_bwd_k<float>))) return cuda_status(e, "preload rope_qkv_bwd_k");
   if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(rope_qkv_bwd_k<bf16>))) return cuda_status(e, "preload rope_qkv_bwd_k<bf16>");
   if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(add_to_bf16_k))) return cuda_status(e, "preload add_to_bf16_k");
-  if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(globaltimer_k))) return cuda_status(e, "preload globaltimer_k");
   if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(swiglu_fwd_k))) return cuda_status(e, "preload swiglu_fwd_k");
   if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(swiglu_bwd_k))) return cuda_status(e, "preload swiglu_bwd_k");
   if (cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(xent_k))) return cuda_status(e, "preload xent_k");

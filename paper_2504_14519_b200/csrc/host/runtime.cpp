@@ -250,7 +250,6 @@ class Runtime {
   } xb[2];
   int64_t x_bytes_sent = 0;
   cudaEvent_t step_start = nullptr, step_end = nullptr;
-  unsigned long long* d_clock = nullptr;  // %globaltimer at step_start (ns), one device word
   std::atomic<int> enq_pos{-1};  // diagnostics: pass (index in order) the host is enqueuing, -1 idle
   size_t bytes_allocated = 0;
   std::vector<void*> allocations;
@@ -259,7 +258,6 @@ class Runtime {
     if (comp) cudaStreamSynchronize(comp);
     destroy_links();
     for (void* a : allocations) cudaFree(a);
-    if (d_clock) cudaFree(d_clock);
     for (cudaEvent_t e : tpool) cudaEventDestroy(e);
     if (xev) cudaEventDestroy(xev);
     if (ev_staged) cudaEventDestroy(ev_staged);
@@ -452,7 +450,6 @@ class Runtime {
       SP_CUDA(cudaEventRecord(ev_ain_free[x], comp));
     }
     SP_CUDA(cudaEventCreate(&step_start));
-    SP_CUDA(cudaMalloc(&d_clock, sizeof *d_clock));
     SP_CUDA(cudaEventCreate(&step_end));
     SP_CUDA(cudaEventCreateWithFlags(&xev, cudaEventDisableTiming));
 
@@ -1525,7 +1522,6 @@ class Runtime {
     x_bytes_sent = 0;
     const int64_t ntok = int64_t(cfg.microbatches) * cfg.seq_len;
     SP_CUDA(cudaEventRecord(step_start, comp));
-    SP_TRY(stamp_globaltimer(d_clock, comp));
     // Host inputs go through pinned staging buffers: a pageable copy would
     // block this thread inside the CUDA driver until the stream drained (and,
     // with loopback ranks sharing one context, stall the other ranks' enqueue).
@@ -1678,16 +1674,6 @@ int sp_runtime_timeline(void* handle, double* out, int cap) {
     out[n++] = b;
   }
   return n;
-}
-
-// The GPU global timer (ns) when the last step's start event was reached:
-// rank r's timeline shifted by (clock_r - clock_0) / 1e6 ms is on rank 0's clock.
-int sp_runtime_step_clock(void* handle, long long* ns) {
-  if (handle) cudaSetDevice(static_cast<Runtime*>(handle)->device);
-  Runtime* rt = static_cast<Runtime*>(handle);
-  cudaError_t e = cudaEventSynchronize(rt->step_end);
-  if (e == cudaSuccess) e = cudaMemcpy(ns, rt->d_clock, sizeof *rt->d_clock, cudaMemcpyDeviceToHost);
-  return e == cudaSuccess ? SP_OK : sp::cuda_status(e, "step clock");
 }
 
 // Attention kernel timing of the last step: out = {fwd_ms, fwd_flops, fwd_launches,

@@ -147,7 +147,6 @@ def _lib():
     lib.sp_loopback_pingpong.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_int]
     lib.sp_loopback_pingpong_1thread.argtypes = [C.c_void_p] + [C.c_void_p] * 4 + [C.c_int64, C.c_int]
     lib.sp_runtime_exchange_stats.argtypes = [C.c_void_p, C.POINTER(C.c_int64)]
-    lib.sp_runtime_step_clock.argtypes = [C.c_void_p, C.POINTER(C.c_longlong)]
     lib.sp_runtime_comm_stats.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
     lib.sp_runtime_enqueue_position.argtypes = [C.c_void_p]
     lib.sp_runtime_destroy.argtypes = [C.c_void_p]
@@ -343,12 +342,6 @@ class SlimPipeStep:
             N.check(n, "sp_runtime_timeline")
         vals = list(buf[:n])
         return vals[0], [(int(vals[i]), vals[i + 1], vals[i + 2]) for i in range(1, n, 3)]
-
-    def step_clock_ns(self) -> int:
-        """GPU global timer (ns) at the last step's start (aligns ranks' timelines)."""
-        t = C.c_longlong()
-        N.check(_lib().sp_runtime_step_clock(self._h, C.byref(t)), "sp_runtime_step_clock")
-        return int(t.value)
 
     def attn_stats(self) -> dict:
         b = (C.c_double * 6)()
