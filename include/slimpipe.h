@@ -68,6 +68,12 @@ int sp_plan_validate_json(int p, int v, int m, int n, int mutation, char** out);
 int sp_plan_balance_json(const int64_t* loads, const int32_t* devices, int count, int early, char** out);
 /* reference simulator.cpp:56-108 */
 int sp_plan_exchange_json(int p, int v, int m, int n, int mode, double beta_attn, char** out);
+/* The executor's per-pass exchange wiring for one rank (0-based): the plan of
+ * sp_plan_exchange_json (v = 1) after the placement filter of sp_model_config
+ * (exchange_min_chunks, exchange_skip_last) — JSON list of {pass, kind,
+ * microbatch, slice, cls, out: [{peer, base, chunks}], in: [{peer, i_src,
+ * base, chunks}]}, exactly what sp_runtime_create builds. */
+int sp_exchange_passes_json(int p, int m, int n, int mode, int rank, int min_chunks, int skip_last, char** out);
 /* reference workload.cpp:87-141; model={L,h,H,a,g,V,bytes,loss_bytes},
  * par={t,c,p,v}, run={S,m,n,ckpt(0 none,1 selective,2 full)} */
 int sp_plan_activation_json(const int64_t* model, const int64_t* par, const int64_t* run, double offload,

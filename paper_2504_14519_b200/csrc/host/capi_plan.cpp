@@ -19,6 +19,7 @@
 #include "pipelab/workload.hpp"
 #include "errors.hpp"
 #include "slimpipe.h"
+#include "xplan.hpp"
 
 using namespace pipelab;
 
@@ -181,6 +182,48 @@ int sp_plan_exchange_json(int p, int v, int m, int n, int mode, double beta, cha
     CostModel cm = c.cost;
     cm.beta_attn = beta;
     return annotation_json(apply_exchange(gen_slimpipe(c), cm, ExchangeMode(mode)));
+  });
+}
+
+int sp_exchange_passes_json(int p, int m, int n, int mode, int rank, int min_chunks, int skip_last, char** out) {
+  return guarded(out, [&] {
+    if (rank < 0 || rank >= p) throw std::invalid_argument("rank out of range");
+    GenConfig c = gen_cfg(p, 1, m, n);
+    const Schedule s = gen_slimpipe(c);
+    CostModel cm = c.cost;
+    cm.beta_attn = 1.0;  // as the runtime: the plan depends on slice indices only
+    const auto xp = sp::exchange_passes(s, apply_exchange(s, cm, ExchangeMode(mode)), rank, p, min_chunks,
+                                        skip_last != 0);
+    std::ostringstream o;
+    auto ints = [&](const std::vector<int>& v) {
+      o << '[';
+      for (std::size_t i = 0; i < v.size(); ++i) o << (i ? "," : "") << v[i];
+      o << ']';
+    };
+    o << '[';
+    bool first = true;
+    for (const auto& [pid, px] : xp) {
+      const Pass& ps = s.passes[pid];
+      o << (first ? "" : ",") << "{\"pass\":" << pid << ",\"kind\":\"" << (ps.kind == PassKind::Forward ? "F" : "BW")
+        << "\",\"microbatch\":" << ps.microbatch << ",\"slice\":" << ps.slice << ",\"cls\":" << px.cls
+        << ",\"out\":[";
+      for (std::size_t i = 0; i < px.out.size(); ++i) {
+        o << (i ? "," : "") << "{\"peer\":" << px.out[i].peer << ",\"base\":" << px.out[i].base << ",\"chunks\":";
+        ints(px.out[i].chunks);
+        o << '}';
+      }
+      o << "],\"in\":[";
+      for (std::size_t i = 0; i < px.in.size(); ++i) {
+        o << (i ? "," : "") << "{\"peer\":" << px.in[i].peer << ",\"i_src\":" << px.in[i].i_src
+          << ",\"base\":" << px.in[i].base << ",\"chunks\":";
+        ints(px.in[i].chunks);
+        o << '}';
+      }
+      o << "]}";
+      first = false;
+    }
+    o << ']';
+    return o.str();
   });
 }
 

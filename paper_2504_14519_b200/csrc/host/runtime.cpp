@@ -44,6 +44,7 @@
 #include "pipelab/simulator.hpp"
 #include "slimpipe.h"
 #include "transport.hpp"
+#include "xplan.hpp"
 
 namespace sp {
 namespace {
@@ -222,22 +223,6 @@ class Runtime {
   // simulator.cpp:56-108): per-pass transfer lists of this rank, two classes
   // (0: forward ticks, 1: backward ticks) each with its own NCCL
   // communicator, copy stream and high-priority remote-compute stream.
-  struct XOut {  // this rank ships Q (+ KV chunks) of its pass to `peer`
-    int peer;
-    std::vector<int> chunks;  // sender-microbatch chunk ids, 1-based, ascending
-    int base;                 // chunk offset in this rank's partial-receive pool
-  };
-  struct XIn {  // this rank computes a partial for `peer`'s pass
-    int peer, i_src;
-    std::vector<int> chunks;
-    int base;  // chunk offset in the receive pool
-  };
-  struct PassX {
-    int cls = 0;
-    std::vector<XOut> out;
-    std::vector<XIn> in;
-    int in_chunks = 0, out_chunks = 0;
-  };
   std::map<int, PassX> xplan;
   pipelab::ExchangeAnnotation ann;
   std::unique_ptr<Link> lx[2];
@@ -708,38 +693,9 @@ class Runtime {
     return SP_OK;
   }
 
-  // Per-pass transfer lists of this rank from the tick plans (transfers are
-  // sorted by (src, dst) in every plan, so both ends post their NCCL calls
-  // in the same order).
+  // Per-pass transfer lists of this rank from the tick plans (xplan.hpp).
   void build_xplan() {
-    const int me = rank + 1;
-    for (const pipelab::TickPlan& tp : ann.ticks) {
-      auto pass_of = [&](int dev) -> int {
-        for (std::size_t x = 0; x < tp.loads.size(); ++x)
-          if (tp.loads[x].device == dev) return tp.passes[x];
-        return -1;
-      };
-      for (const pipelab::Transfer& tr : tp.plan.transfers) {
-        const int sp = pass_of(tr.src), dp = pass_of(tr.dst);
-        if (sp < 0 || dp < 0) continue;
-        // placement filter (slimpipe.h): identical on every rank
-        if (int(tr.kv_chunk_indices.size()) < cfg.exchange_min_chunks) continue;
-        if (cfg.exchange_skip_last && tr.dst == p) continue;
-        std::vector<int> ch(tr.kv_chunk_indices.begin(), tr.kv_chunk_indices.end());
-        if (tr.src == me) {
-          PassX& px = xplan[sp];
-          px.cls = tp.forward ? 0 : 1;
-          px.out.push_back({tr.dst - 1, ch, px.out_chunks});
-          px.out_chunks += int(ch.size());
-        }
-        if (tr.dst == me) {
-          PassX& px = xplan[dp];
-          px.cls = tp.forward ? 0 : 1;
-          px.in.push_back({tr.src - 1, sched.passes[sp].slice, ch, px.in_chunks});
-          px.in_chunks += int(ch.size());
-        }
-      }
-    }
+    xplan = exchange_passes(sched, ann, rank, p, cfg.exchange_min_chunks, cfg.exchange_skip_last != 0);
     for (const auto& [pid, px] : xplan) {
       x_tout = std::max(x_tout, int(px.out.size()));
       x_cout = std::max(x_cout, px.out_chunks);

@@ -40,6 +40,7 @@ _SIGS = {
     "sp_plan_validate_json": (C.c_int, [C.c_int] * 5 + [_charpp]),
     "sp_plan_balance_json": (C.c_int, [_i64p, _i32p, C.c_int, C.c_int, _charpp]),
     "sp_plan_exchange_json": (C.c_int, [C.c_int] * 5 + [C.c_double, _charpp]),
+    "sp_exchange_passes_json": (C.c_int, [C.c_int] * 7 + [_charpp]),
     "sp_plan_activation_json": (C.c_int, [_i64p, _i64p, _i64p, C.c_double, _charpp]),
     "sp_plan_exchange_volume": (C.c_int, [C.c_int64] * 5 + [_charpp]),
     "sp_plan_analytics_json": (C.c_int, [C.c_int] + [C.c_int64] * 6 + [_charpp]),

@@ -51,6 +51,14 @@ def apply_exchange_text(p: int, v: int, m: int, n: int, mode: str = "on", beta_a
     return N._json_call("sp_plan_exchange_json", p, v, m, n, N.MODES[mode], float(beta_attn))
 
 
+def exchange_passes(p: int, m: int, n: int, mode: str, rank: int, min_chunks: int = 0,
+                    skip_last: bool = False) -> list[dict]:
+    """The executor's per-pass exchange wiring of one rank (xplan.hpp): which
+    passes ship work out and which serve a peer, after the placement filter."""
+    return json.loads(N._json_call("sp_exchange_passes_json", p, m, n, N.MODES[mode], rank, int(min_chunks),
+                                   int(skip_last)))
+
+
 @dataclass
 class ModelShape:
     layers: int
