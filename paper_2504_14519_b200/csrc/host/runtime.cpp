@@ -568,6 +568,13 @@ class Runtime {
   int init_loop_links() {
     if (loop_world_size(loop) != p) return set_error(SP_ERR_INVALID, "loopback world has %d ranks, pp = %d",
                                                      loop_world_size(loop), p);
+    // Receives are posted early here: the loopback's waits are one-CTA
+    // kernels (nothing like an NCCL receive's SMs to save), and with every
+    // rank's streams on one device the extra compute -> receive-stream
+    // dependencies of just-in-time posting measured a stall at PP=4 with
+    // the exchange on (hardware-queue sharing, §2.3).
+    jit_recv = false;
+    xserve_jit = false;
     const bool ring = v > 1;
     const int nx = (rank + 1) % p, pv = (rank + p - 1) % p;
     if (!last_dev || ring) {
