@@ -6,16 +6,17 @@
 #   D: c3 (Llama-13B shapes x8) 256K, n=16, m=4, PP=4: off and the filtered
 #      early exchange
 # Each run writes its bench line and the measured Gantt under gpurun_out/.
-#   E: c2 PP=4 posting A/B: exchange serves posted at the receiving pass
-#      (default) or from the host's run-ahead (SP_XSERVE_JIT=0), stage
-#      receives posted just in time (SP_JIT_RECV=1), NCCL CTAs capped
-#      (SP_NCCL_MAX_CTAS=4); then c3 off / filtered early when the best
-#      c2 exchange variant beats c2 off
+#   E: c2 PP=4 posting A/B (the switches as measured; just-in-time stage
+#      receives have since become the default): stage receives posted
+#      early (SP_JIT_RECV=0) or just in time (=1), exchange serves posted at
+#      the receiving pass (SP_XSERVE_JIT=1, default), NCCL CTAs capped
+#      (SP_NCCL_MAX_CTAS=4); then c3 off / filtered early when the best c2
+#      exchange variant beats c2 off
 #   gpurun --gpus 4 --timeout 3000 -- bash scripts/exchange_placement.sh [C][D][E]
 set -u
 mkdir -p gpurun_out
 which=${1:-CD}
-ENVX=${ENVX:-SP_XSERVE_JIT=1}
+ENVX=${ENVX:-SP_JIT_RECV=0}
 tr() {  # tag, args...   (env: per-run NCCL / posting switches)
   local tag=$1; shift
   timeout 900 env $ENVX python -m torch.distributed.run --nnodes=1 --nproc-per-node=4 --master-addr 127.0.0.1 \
@@ -36,9 +37,9 @@ if [[ $which == *D* ]]; then
   tr c3_early_min3_nolast --model c3 --layers 8 $S --exchange early --exchange-min-chunks 3 --exchange-skip-last
 fi
 if [[ $which == *E* ]]; then
-  ENVX=SP_XSERVE_JIT=1 tr e_c2_off --model c2
+  ENVX=SP_JIT_RECV=0 tr e_c2_off --model c2
   ENVX="SP_JIT_RECV=1" tr e_c2_off_jitrecv --model c2
-  ENVX=SP_XSERVE_JIT=1 tr e_c2_early_min2_nolast --model c2 --exchange early --exchange-min-chunks 2 --exchange-skip-last
+  ENVX="SP_JIT_RECV=0 SP_XSERVE_JIT=1" tr e_c2_early_min2_nolast --model c2 --exchange early --exchange-min-chunks 2 --exchange-skip-last
   ENVX="SP_XSERVE_JIT=1 SP_JIT_RECV=1 SP_NCCL_MAX_CTAS=4" tr e_c2_early_min2_nolast_all --model c2 --exchange early \
     --exchange-min-chunks 2 --exchange-skip-last
   best=$(python - <<'PY'
@@ -57,8 +58,8 @@ PY
   echo "best exchange variant over off: $best"
   if [[ $best != none ]]; then
     S="--seq-len 262144 --slices 16 --microbatches 4"
-    ENVX=SP_XSERVE_JIT=1 tr e_c3_off --model c3 --layers 8 $S
-    ENVX=SP_XSERVE_JIT=1 tr e_c3_early_min3_nolast --model c3 --layers 8 $S --exchange early --exchange-min-chunks 3 \
+    ENVX=SP_JIT_RECV=0 tr e_c3_off --model c3 --layers 8 $S
+    ENVX=SP_JIT_RECV=0 tr e_c3_early_min3_nolast --model c3 --layers 8 $S --exchange early --exchange-min-chunks 3 \
       --exchange-skip-last
   fi
 fi
