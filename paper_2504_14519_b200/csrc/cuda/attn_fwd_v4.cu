@@ -1,12 +1,12 @@
 // K1 (head_dim 128): sliced causal attention forward, ping-pong with a
-// shared S buffer.  Same semantics as attn_fwd.cu / attn_fwd_v3.cu (reference
+// shared S buffer.  Same semantics as attn_fwd.cu (reference
 // chunk_attention, proj/src/attention.cpp:21-111: scale 1/sqrt(d),
 // bottom-right causal, finalize O/l, plus the LSE).
 //
-// attn_fwd_v3.cu keeps S_A, S_B, O_A, O_B in TMEM with P written over S, so
-// S_X(j+1) can only be computed after PV_X(j) has consumed P_X(j): every
-// tile's softmax sits on a serial chain PV + S + softmax (~3.3K cycles per
-// KV step of the CTA, measured).  Here the two tiles SHARE one S buffer and
+// The round-1 predecessor kept S_A, S_B, O_A, O_B in TMEM with P written over
+// S, so S_X(j+1) could only be computed after PV_X(j) had consumed P_X(j):
+// every tile's softmax sat on a serial chain PV + S + softmax (~3.3K cycles
+// per KV step of the CTA, measured).  Here the two tiles SHARE one S buffer and
 // P gets its own columns:
 //   TMEM: S [0,128) | P_A [128,192) P_B [192,256) (bf16, 2 keys/col) |
 //         O_A [256,384) O_B [384,512)
