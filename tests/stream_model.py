@@ -4,7 +4,11 @@ compute stream, one stream per link direction (two-deep receive and send
 rings, CUDA events between streams) and the vocab stream; NCCL sends and
 receives pair in FIFO order per link, collectives need every rank at the same
 op, and optionally the host can only run `Q` ops ahead of completion.
-`deadlocks(p, v, m, n, vp)` explores it to a fixpoint.  Used by
+With the exchange, each class has a request/serve stream cx<c> and a serve
+compute stream rx<c>; its sends and receives pair FIFO per (class, sender,
+receiver) at the heads of the two ranks' cx<c>, and the transfer lists are
+the executor's own (sp_exchange_passes_json).
+`deadlocks(p, v, m, n, vp)` / `exchange_deadlocks(...)` explore it to a fixpoint.  Used by
 tests/test_stream_model.py as a regression check of the protocol (the
 executor's device orders come from the planner)."""
 from __future__ import annotations
@@ -26,18 +30,31 @@ def device_orders(p, v, m, n, vp):
               s["passes"][i]["stage"]) for i in dev] for dev in s["device_order"]]
 
 
-def build(devs, p, v, vp, depth=2, jit_recv=False):
+def build(devs, p, v, vp, depth=2, jit_recv=False, pids=None, xw=None, layers=2, serve_jit=True):
+    """pids[r][j]: pass id of devs[r][j] (F/BW; None for vocab passes); xw[r]:
+    the executor's exchange wiring of rank r ({pass id: px}, from
+    sp_exchange_passes_json) — then every layer of a shipping pass sends its
+    requests on the class stream cx<c> and waits there for the partials, and a
+    serving pass posts its serves (recv request, compute on rx<c>, send the
+    partial) at its start, as runtime.cpp attention_forward / layer_backward /
+    post_remote do (selective recompute)."""
     nst = p * v
     ops = {}  # (rank, stream) -> list of op dicts
     seqs = {}
+    req = defaultdict(int)  # (cls, src, dst) -> requests enqueued by the sender so far
+    res = defaultdict(int)
+    srv_req = defaultdict(int)  # same counters on the serving side (FIFO matching per pair)
+    srv_res = defaultdict(int)
     for r, order in enumerate(devs):
         seqs[r] = []
         st = defaultdict(list)
         ev = {}  # event name -> (stream, index) of latest record
         def rec(name, s):
             ev[name] = (s, len(st[s]) - 1)
+        at = [None]  # the pass being enqueued (diagnostics: where a stream is stuck)
+
         def add(s, kind, deps=(), key=None):
-            st[s].append({"kind": kind, "deps": [d for d in deps if d is not None], "key": key})
+            st[s].append({"kind": kind, "deps": [d for d in deps if d is not None], "key": key, "at": at[0]})
             seqs[r].append((r, s, len(st[s]) - 1))
         def cur(s):
             return (s, len(st[s]) - 1) if st[s] else None
@@ -45,7 +62,42 @@ def build(devs, p, v, vp, depth=2, jit_recv=False):
             for e in ("ain", "out", "gin", "gout"):
                 ev[(e, x)] = None
         ain = out = gin = gout = 0
-        for (kind, k, i, s) in order:
+
+        def serve(px):  # post_remote
+            c = px["cls"]
+            cx, rx = f"cx{c}", f"rx{c}"
+            if serve_jit:
+                add(cx, "wait", [cur("comp"), cur(cx)])
+            for _ in range(layers):
+                for t in px["in"]:
+                    src = t["peer"]
+                    add(cx, "xrecv", [cur(cx)], ("xreq", c, src, r, srv_req[(c, src, r)]))
+                    srv_req[(c, src, r)] += 1
+                    add(rx, "xcomp", [cur(cx), cur(rx)])
+                    add(cx, "xsend", [cur(rx), cur(cx)], ("xres", c, r, src, srv_res[(c, r, src)]))
+                    srv_res[(c, r, src)] += 1
+
+        def attention(px, step):  # attention_forward / the K2 part of layer_backward
+            if not px or not px["out"]:
+                add("comp", step, [cur("comp")])
+                return
+            c = px["cls"]
+            cx = f"cx{c}"
+            add(cx, "wait", [cur("comp"), cur(cx)])
+            for o in px["out"]:
+                add(cx, "xsend", [cur(cx)], ("xreq", c, r, o["peer"], req[(c, r, o["peer"])]))
+                req[(c, r, o["peer"])] += 1
+            add("comp", step, [cur("comp")])
+            for o in px["out"]:
+                add(cx, "xrecv", [cur(cx)], ("xres", c, o["peer"], r, res[(c, o["peer"], r)]))
+                res[(c, o["peer"], r)] += 1
+            add("comp", "wait", [cur(cx), cur("comp")])
+
+        for j, (kind, k, i, s) in enumerate(order):
+            at[0] = (kind, k, i, s)
+            px = xw[r].get(pids[r][j]) if xw is not None and pids[r][j] is not None else None
+            if px and px["in"]:
+                serve(px)
             if kind == 0:  # F
                 if s > 1:
                     b = ain; ain = (ain + 1) % depth
@@ -53,6 +105,9 @@ def build(devs, p, v, vp, depth=2, jit_recv=False):
                         ("act", (r - 1) % p, r, k, i, s - 1))
                     add("comp", "wait", [cur("act_in"), cur("comp")])
                     rec(("ain", b), "comp")
+                if xw is not None:
+                    for _ in range(layers):
+                        attention(px, "fwd")
                 if s < nst:
                     b = out; out = (out + 1) % depth
                     add("comp", "fwd", [ev[("out", b)], cur("comp")])
@@ -75,6 +130,9 @@ def build(devs, p, v, vp, depth=2, jit_recv=False):
                     add("comp", "bwd", [cur("comp")])
                 else:
                     add("comp", "bwd", [ev[("gout", gout)], cur("comp")])
+                if xw is not None:
+                    for _ in range(layers):
+                        attention(px, "bwd")
                 if s == 1:
                     if gb is not None:
                         rec(("gin", gb), "comp")
@@ -100,12 +158,28 @@ def run(ops, p):
         for (r, s), l in ops.items():
             while head[(r, s)] < len(l):
                 o = l[head[(r, s)]]
-                if o["kind"] in ("send", "recv", "coll"):
+                if o["kind"] in ("send", "recv", "coll", "xsend", "xrecv"):
                     break
                 deps = [(r,) + d if d is not None else None for d in o["deps"]]
                 if not all(d in done for d in deps if d is not None):
                     break
                 done.add((r, s, head[(r, s)])); head[(r, s)] += 1; changed = True
+        # exchange p2p: a send at the head of one rank's class stream meets
+        # the matching receive at the head of the peer's
+        for (r, s), l in ops.items():
+            if not s.startswith("cx") or head[(r, s)] >= len(l):
+                continue
+            o = l[head[(r, s)]]
+            if o["kind"] != "xsend" or not all((r,) + d in done for d in o["deps"] if d is not None):
+                continue
+            dst = o["key"][3]
+            l2, h2 = ops.get((dst, s), []), head.get((dst, s), 0)
+            if h2 < len(l2):
+                o2 = l2[h2]
+                if o2["kind"] == "xrecv" and o2["key"] == o["key"] and \
+                        all((dst,) + d in done for d in o2["deps"] if d is not None):
+                    done.add((r, s, head[(r, s)])); head[(r, s)] += 1
+                    done.add((dst, s, h2)); head[(dst, s)] += 1; changed = True
         # p2p matching
         for (r, s), l in ops.items():
             if head[(r, s)] >= len(l): continue
@@ -134,7 +208,8 @@ def run(ops, p):
             for r in range(p):
                 done.add((r, "vocab", head[(r, "vocab")])); head[(r, "vocab")] += 1
             changed = True
-    stuck = {key: (head[key], ops[key][head[key]]["kind"], ops[key][head[key]]["key"]) for key in ops if head[key] < len(ops[key])}
+    stuck = {key: (head[key], ops[key][head[key]]["kind"], ops[key][head[key]]["key"], ops[key][head[key]].get("at"))
+             for key in ops if head[key] < len(ops[key])}
     return stuck
 
 
@@ -189,3 +264,20 @@ def deadlocks(p, v, m, n, vp=False, depth=2, host_queue=None, jit_recv=False) ->
     if host_queue is None:
         return bool(run(ops, p))
     return run_capped(ops, p, host_queue, seqs)
+
+
+def exchange_program(p, m, n, mode, min_chunks=0, skip_last=False, vp=False):
+    """Device orders, pass ids and the executor's exchange wiring (v = 1)."""
+    sch = P.gen_slimpipe(p, 1, m, n)
+    pid_of = {(KIND[q["kind"]], q["microbatch"], q["slice"], q["stage"]): q["id"] for q in sch["passes"]}
+    devs = device_orders(p, 1, m, n, vp)
+    pids = [[pid_of.get(tuple(e)) for e in dev] for dev in devs]
+    xw = [{px["pass"]: px for px in P.exchange_passes(p, m, n, mode, r, min_chunks, skip_last)} for r in range(p)]
+    return devs, pids, xw
+
+
+def exchange_deadlocks(p, m, n, mode, min_chunks=0, skip_last=False, vp=False, serve_jit=True, jit_recv=True,
+                       layers=2) -> dict:
+    devs, pids, xw = exchange_program(p, m, n, mode, min_chunks, skip_last, vp)
+    ops, _ = build(devs, p, 1, vp, 2, jit_recv, pids, xw, layers, serve_jit)
+    return run(ops, p)
