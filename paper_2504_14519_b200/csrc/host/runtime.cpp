@@ -422,8 +422,16 @@ class Runtime {
     SP_CUDA(cudaGetDevice(&device));  // host-side validation above runs without a GPU
     SP_TRY(preload_kernels());        // before any communication (transport.cu)
     SP_CUDA(cudaStreamCreateWithFlags(&comp, cudaStreamNonBlocking));
+    // SP_COMM_PRIORITY=high (experimental, unmeasured): the link
+    // and exchange streams get the highest priority, so their NCCL kernels are
+    // dispatched ahead of the compute stream's queued attention CTAs instead
+    // of after the running K1/K2 launch
+    const char* cp = std::getenv("SP_COMM_PRIORITY");
+    int prio_lo = 0, prio_hi = 0;
+    SP_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    const int comm_prio = (cp && std::strcmp(cp, "high") == 0) ? prio_hi : prio_lo;
     for (cudaStream_t* st : {&s_act_in, &s_act_out, &s_grad_in, &s_grad_out})
-      SP_CUDA(cudaStreamCreateWithFlags(st, cudaStreamNonBlocking));
+      SP_CUDA(cudaStreamCreateWithPriority(st, cudaStreamNonBlocking, comm_prio));
     for (int x = 0; x < 2; ++x) {
       SP_CUDA(cudaEventCreateWithFlags(&ev_out_free[x], cudaEventDisableTiming));
       SP_CUDA(cudaEventCreateWithFlags(&ev_gin_free[x], cudaEventDisableTiming));
@@ -444,7 +452,7 @@ class Runtime {
       int lo = 0, hi = 0;
       SP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
       for (int k = 0; k < 2 && p > 1; ++k) {
-        SP_CUDA(cudaStreamCreateWithFlags(&cx[k], cudaStreamNonBlocking));
+        SP_CUDA(cudaStreamCreateWithPriority(&cx[k], cudaStreamNonBlocking, comm_prio));
         SP_CUDA(cudaStreamCreateWithPriority(&rx[k], cudaStreamNonBlocking, hi));
       }
     }

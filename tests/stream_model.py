@@ -30,14 +30,16 @@ def device_orders(p, v, m, n, vp):
               s["passes"][i]["stage"]) for i in dev] for dev in s["device_order"]]
 
 
-def build(devs, p, v, vp, depth=2, jit_recv=False, pids=None, xw=None, layers=2, serve_jit=True):
+def build(devs, p, v, vp, depth=2, jit_recv=False, pids=None, xw=None, layers=2, serve_jit=True, lanes=False):
     """pids[r][j]: pass id of devs[r][j] (F/BW; None for vocab passes); xw[r]:
     the executor's exchange wiring of rank r ({pass id: px}, from
     sp_exchange_passes_json) — then every layer of a shipping pass sends its
     requests on the class stream cx<c> and waits there for the partials, and a
     serving pass posts its serves (recv request, compute on rx<c>, send the
     partial) at its start, as runtime.cpp attention_forward / layer_backward /
-    post_remote do (selective recompute)."""
+    post_remote do (selective recompute).  lanes=True: each sender's serves on
+    their own stream pair cx<c>s<src> / rx<c>s<src> (a design, not the
+    executor: one communicator per sending stage)."""
     nst = p * v
     ops = {}  # (rank, stream) -> list of op dicts
     seqs = {}
@@ -63,31 +65,37 @@ def build(devs, p, v, vp, depth=2, jit_recv=False, pids=None, xw=None, layers=2,
                 ev[(e, x)] = None
         ain = out = gin = gout = 0
 
+        def lane(c, src):
+            return (f"cx{c}s{src}", f"rx{c}s{src}") if lanes else (f"cx{c}", f"rx{c}")
+
         def serve(px):  # post_remote
             c = px["cls"]
-            cx, rx = f"cx{c}", f"rx{c}"
             if serve_jit:
-                add(cx, "wait", [cur("comp"), cur(cx)])
+                for cx in {lane(c, t["peer"])[0] for t in px["in"]}:
+                    add(cx, "wait", [cur("comp"), cur(cx)])
             for _ in range(layers):
                 for t in px["in"]:
                     src = t["peer"]
+                    cx, rx = lane(c, src)
                     add(cx, "xrecv", [cur(cx)], ("xreq", c, src, r, srv_req[(c, src, r)]))
                     srv_req[(c, src, r)] += 1
-                    add(rx, "xcomp", [cur(cx), cur(rx)])
+                    add(rx, "xcomp", [cur(cx), cur(rx)], ("xwork", c, src, r, len(t["chunks"])))
                     add(cx, "xsend", [cur(rx), cur(cx)], ("xres", c, r, src, srv_res[(c, r, src)]))
+                    st[cx][-1]["to"] = (src, f"cx{c}")
                     srv_res[(c, r, src)] += 1
 
         def attention(px, step):  # attention_forward / the K2 part of layer_backward
             if not px or not px["out"]:
-                add("comp", step, [cur("comp")])
+                add("comp", step, [cur("comp")], ("attn",))
                 return
             c = px["cls"]
             cx = f"cx{c}"
             add(cx, "wait", [cur("comp"), cur(cx)])
             for o in px["out"]:
                 add(cx, "xsend", [cur(cx)], ("xreq", c, r, o["peer"], req[(c, r, o["peer"])]))
+                st[cx][-1]["to"] = (o["peer"], lane(c, r)[0])
                 req[(c, r, o["peer"])] += 1
-            add("comp", step, [cur("comp")])
+            add("comp", step, [cur("comp")], ("attn", sum(len(o["chunks"]) for o in px["out"])))
             for o in px["out"]:
                 add(cx, "xrecv", [cur(cx)], ("xres", c, o["peer"], r, res[(c, o["peer"], r)]))
                 res[(c, o["peer"], r)] += 1
@@ -172,14 +180,14 @@ def run(ops, p):
             o = l[head[(r, s)]]
             if o["kind"] != "xsend" or not all((r,) + d in done for d in o["deps"] if d is not None):
                 continue
-            dst = o["key"][3]
-            l2, h2 = ops.get((dst, s), []), head.get((dst, s), 0)
+            dst, ts = o["to"]
+            l2, h2 = ops.get((dst, ts), []), head.get((dst, ts), 0)
             if h2 < len(l2):
                 o2 = l2[h2]
                 if o2["kind"] == "xrecv" and o2["key"] == o["key"] and \
                         all((dst,) + d in done for d in o2["deps"] if d is not None):
                     done.add((r, s, head[(r, s)])); head[(r, s)] += 1
-                    done.add((dst, s, h2)); head[(dst, s)] += 1; changed = True
+                    done.add((dst, ts, h2)); head[(dst, ts)] += 1; changed = True
         # p2p matching
         for (r, s), l in ops.items():
             if head[(r, s)] >= len(l): continue
@@ -277,7 +285,7 @@ def exchange_program(p, m, n, mode, min_chunks=0, skip_last=False, vp=False):
 
 
 def exchange_deadlocks(p, m, n, mode, min_chunks=0, skip_last=False, vp=False, serve_jit=True, jit_recv=True,
-                       layers=2) -> dict:
+                       layers=2, lanes=False) -> dict:
     devs, pids, xw = exchange_program(p, m, n, mode, min_chunks, skip_last, vp)
-    ops, _ = build(devs, p, 1, vp, 2, jit_recv, pids, xw, layers, serve_jit)
+    ops, _ = build(devs, p, 1, vp, 2, jit_recv, pids, xw, layers, serve_jit, lanes)
     return run(ops, p)
