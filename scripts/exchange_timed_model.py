@@ -43,8 +43,35 @@ def measured(path):
     return g["makespan"], dur, per_chunk
 
 
+def idle_placed(p, m, n, mode, gantt, per_chunk, min_fill=0.5):
+    """The plan's transfers kept only where the receiving GPU is idle, in the
+    measured off step, for at least min_fill of the moved attention inside
+    the sending pass's window (a placement by measured idle time; not built)."""
+    from paper_2504_14519_b200 import plan as P
+    g = json.loads(Path(gantt).read_text())
+    rows = [sorted(r, key=lambda x: x["start"]) for r in g["rows"]]
+    span = {(KCODE[x["kind"]], x["microbatch"], x["slice"], x["stage"]): (x["start"], x["end"]) for r in rows for x in r}
+    passes = P.gen_slimpipe(p, 1, m, n)["passes"]
+    key = {q["id"]: (KCODE[q["kind"]], q["microbatch"], q["slice"], q["stage"]) for q in passes}
+
+    def idle_in(row, a, b):
+        return (b - a) - sum(max(0.0, min(b, x["end"]) - max(a, x["start"])) for x in row)
+
+    keep = set()
+    for t in P.apply_exchange(p, 1, m, n, mode)["ticks"]:
+        pid = {d: q for d, _, q in t["in"]}
+        for tr in t["plan"]["transfers"]:
+            sp, dp = pid[tr["src"]], pid[tr["dst"]]
+            s0, s1 = span[key[sp]]
+            work = per_chunk[(key[sp][0], key[sp][3])] * len(tr["chunks"])
+            if idle_in(rows[tr["dst"] - 1], s0, s1) >= min_fill * work:
+                keep.add((sp, tr["dst"] - 1, tuple(tr["chunks"])))
+                keep.add(("in", dp, tr["src"] - 1, tuple(tr["chunks"])))
+    return keep
+
+
 def simulate(p, m, n, mode, dur, per_chunk, layers, sizes, gbs, min_chunks=0, skip_last=False, lanes=False,
-             gated=False):
+             gated=False, keep=None):
     """gated: a communication kernel (stage or exchange, normal-priority stream)
     is dispatched only once the rank's compute stream is not inside an
     attention kernel (K1/K2: one launch per layer, tens of ms) — the
@@ -53,6 +80,13 @@ def simulate(p, m, n, mode, dur, per_chunk, layers, sizes, gbs, min_chunks=0, sk
     devs, pids, xw = SM.exchange_program(p, m, n, mode if mode != "off" else "on", min_chunks, skip_last)
     if mode == "off":
         xw = [{} for _ in range(p)]
+    elif keep is not None:  # placement by measured idle time
+        for r in range(p):
+            for pid, px in list(xw[r].items()):
+                px = dict(px)
+                px["out"] = [o for o in px["out"] if (pid, o["peer"], tuple(o["chunks"])) in keep]
+                px["in"] = [i for i in px["in"] if ("in", pid, i["peer"], tuple(i["chunks"])) in keep]
+                xw[r][pid] = px
     ops, _ = SM.build(devs, p, 1, False, 2, True, pids, xw, layers, True, lanes)
     Ls, qd, kvd = sizes
 
@@ -205,9 +239,12 @@ def main():
     sizes = (a.seq // a.n, a.hidden, a.kv_dim)
     tok = a.m * a.seq
     out = {"measured_off_makespan_ms": mk}
+    keep = idle_placed(a.p, a.m, a.n, a.mode, a.gantt, per_chunk)
     for gated in (True, False):
         tag = "gated" if gated else "prompt"
         for name, kw in [("off", dict(mode="off")), ("plan", dict(mode=a.mode)),
+                         ("idle_placed", dict(mode=a.mode, keep=keep)),
+                         ("idle_placed_lanes", dict(mode=a.mode, keep=keep, lanes=True)),
                          ("filtered", dict(mode=a.mode, min_chunks=a.min_chunks, skip_last=True)),
                          ("plan_lanes", dict(mode=a.mode, lanes=True)),
                          ("filtered_lanes", dict(mode=a.mode, min_chunks=a.min_chunks, skip_last=True, lanes=True))]:
